@@ -1,0 +1,232 @@
+"""CPU oracle for the Lightplane Renderer hot path -- TEST INFRASTRUCTURE.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this package. The product package
+(paper_2404_19760_b200) never imports, links or executes it, and this package
+never imports the product package: the two share no code. The only shared
+module is `workload` (seeded input generators, no method arithmetic).
+
+The arithmetic lives in lp_oracle.cpp (plain fp64 C++, per-ray store-all
+forward of Eq. 1 and hand-derived backward of Eq. 3; see its header for the
+paper citations). This file only compiles it and marshals numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "lp_oracle.cpp")
+_LIB = os.path.join(_HERE, "liblp_oracle.so")
+_lib = None
+_lock = threading.Lock()
+
+TRIPLANE = 0
+VOXEL = 1
+
+
+def build(force: bool = False) -> str:
+    """Compile lp_oracle.cpp into liblp_oracle.so (g++ -O3, fp64, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-shared", "-fno-fast-math",
+               "-ffp-contract=off", _SRC, "-o", tmp]
+        subprocess.check_call(cmd)
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_LIB)
+            P = ctypes.c_void_p
+            i32, i64, f64 = ctypes.c_int, ctypes.c_int64, ctypes.c_double
+            L.lpo_sample.argtypes = [i32, i32, i32, i32, i32, P, P, P, i64, P, P]
+            L.lpo_splat.argtypes = [i32, i32, i32, i32, i32, i64, P, P, P, P, P]
+            L.lpo_mlp_forward.argtypes = [i32, P, P, i64, P, P]
+            L.lpo_mlp_backward.argtypes = [i32, P, P, i64, P, P, P, P]
+            L.lpo_render_forward.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
+                                             P, P, P, P, i32, P, P, P]
+            L.lpo_render_backward.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
+                                              P, P, P, P, i32, P, P, P, P, P, P, P, i32]
+            L.lpo_trace.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, P, P, f64, f64, i32,
+                                    P, P, P, P, P]
+            for f in (L.lpo_sample, L.lpo_splat, L.lpo_mlp_forward, L.lpo_mlp_backward,
+                      L.lpo_render_forward, L.lpo_render_backward, L.lpo_trace):
+                f.restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def _d(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+class Field:
+    """theta (list of planes or one voxel volume, channel-last) + packed MLP."""
+
+    def __init__(self, kind: int, grid: Sequence[np.ndarray], widths: Sequence[int], params: np.ndarray):
+        self.kind = int(kind)
+        self.grid = [_d(g) for g in grid]
+        if self.kind == TRIPLANE:
+            assert len(self.grid) == 3
+            H, W, K = self.grid[0].shape
+            D = self.grid[1].shape[1]
+            assert self.grid[1].shape == (W, D, K) and self.grid[2].shape == (D, H, K)
+        else:
+            assert len(self.grid) == 1
+            H, W, D, K = self.grid[0].shape
+        self.H, self.W, self.D, self.K = int(H), int(W), int(D), int(K)
+        self.widths = np.ascontiguousarray(np.asarray(widths, dtype=np.int32))
+        self.n_layers = len(widths) - 1
+        self.params = _d(params)
+        self.C = int(widths[-1]) - 1
+        assert self.widths[0] == self.K
+
+    def _planes(self):
+        g = self.grid + [None] * (3 - len(self.grid))
+        return [_p(x) for x in g]
+
+    def _geom(self):
+        return (self.kind, self.H, self.W, self.D, self.K)
+
+
+def sample(field: Field, x: np.ndarray) -> np.ndarray:
+    x = _d(x).reshape(-1, 3)
+    h = np.zeros((len(x), field.K))
+    rc = lib().lpo_sample(*field._geom(), *field._planes(), len(x), _p(x), _p(h))
+    assert rc == 0
+    return h
+
+
+def splat(field: Field, x: np.ndarray, v: np.ndarray):
+    x = _d(x).reshape(-1, 3)
+    v = _d(v).reshape(len(x), field.K)
+    g = [np.zeros_like(a) for a in field.grid]
+    gp = [_p(a) for a in g] + [None] * (3 - len(g))
+    rc = lib().lpo_splat(*field._geom(), len(x), _p(x), _p(v), *gp)
+    assert rc == 0
+    return g
+
+
+def mlp_forward(widths, params, x):
+    widths = np.ascontiguousarray(np.asarray(widths, dtype=np.int32))
+    x = _d(x).reshape(-1, widths[0])
+    params = _d(params)
+    out = np.zeros((len(x), int(widths[-1])))
+    rc = lib().lpo_mlp_forward(len(widths) - 1, _p(widths), _p(params), len(x), _p(x), _p(out))
+    assert rc == 0
+    return out
+
+
+def mlp_backward(widths, params, x, dout):
+    widths = np.ascontiguousarray(np.asarray(widths, dtype=np.int32))
+    x = _d(x).reshape(-1, widths[0])
+    dout = _d(dout).reshape(len(x), int(widths[-1]))
+    params = _d(params)
+    gp = np.zeros_like(params)
+    gin = np.zeros_like(x)
+    rc = lib().lpo_mlp_backward(len(widths) - 1, _p(widths), _p(params), len(x), _p(x), _p(dout),
+                                _p(gp), _p(gin))
+    assert rc == 0
+    return gp, gin
+
+
+class Rays:
+    def __init__(self, origins, dirs, near, far, S: int):
+        self.o = _d(origins).reshape(-1, 3)
+        self.d = _d(dirs).reshape(-1, 3)
+        self.near = _d(near).reshape(-1)
+        self.far = _d(far).reshape(-1)
+        self.S = int(S)
+        self.n = len(self.o)
+
+
+def render_forward(field: Field, rays: Rays, bg=None, r0: int = 0, r1: Optional[int] = None,
+                   out=None, tau=None):
+    r1 = rays.n if r1 is None else r1
+    if out is None:
+        out = np.zeros((rays.n, field.C))
+    if tau is None:
+        tau = np.zeros(rays.n)
+    bgd = None if bg is None else _d(bg)
+    rc = lib().lpo_render_forward(*field._geom(), *field._planes(), field.n_layers, _p(field.widths),
+                                  _p(field.params), r0, r1, _p(rays.o), _p(rays.d), _p(rays.near),
+                                  _p(rays.far), rays.S, _p(bgd), _p(out), _p(tau))
+    assert rc == 0
+    return out, tau
+
+
+def render_backward(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, mode: int = 0,
+                    r0: int = 0, r1: Optional[int] = None, grads=None):
+    """Returns (grad_grid list, grad_params); accumulates into `grads` if given."""
+    r1 = rays.n if r1 is None else r1
+    go = _d(grad_out).reshape(rays.n, field.C)
+    gt = None if grad_tau is None else _d(grad_tau).reshape(rays.n)
+    bgd = None if bg is None else _d(bg)
+    if grads is None:
+        grads = ([np.zeros_like(a) for a in field.grid], np.zeros_like(field.params))
+    gg, gpar = grads
+    gp = [_p(a) for a in gg] + [None] * (3 - len(gg))
+    rc = lib().lpo_render_backward(*field._geom(), *field._planes(), field.n_layers, _p(field.widths),
+                                   _p(field.params), r0, r1, _p(rays.o), _p(rays.d), _p(rays.near),
+                                   _p(rays.far), rays.S, _p(bgd), _p(go), _p(gt), *gp, _p(gpar), mode)
+    assert rc == 0
+    return gg, gpar
+
+
+def trace(field: Field, origin, direction, near: float, far: float, S: int):
+    """Per-sample (sigma, tau, T, w, c) of one ray (store-all forward)."""
+    o = _d(origin).reshape(3)
+    d = _d(direction).reshape(3)
+    sigma, tau, T, w = (np.zeros(S) for _ in range(4))
+    c = np.zeros((S, field.C))
+    rc = lib().lpo_trace(*field._geom(), *field._planes(), field.n_layers, _p(field.widths),
+                         _p(field.params), _p(o), _p(d), float(near), float(far), S, _p(sigma), _p(tau),
+                         _p(T), _p(w), _p(c))
+    assert rc == 0
+    return sigma, tau, T, w, c
+
+
+def render_forward_threaded(field: Field, rays: Rays, bg=None, threads: int = 1):
+    """Forward over disjoint contiguous ray ranges on `threads` host threads
+    (ctypes releases the GIL). Used only for the timed cpu baseline."""
+    out = np.zeros((rays.n, field.C))
+    tau = np.zeros(rays.n)
+    bounds = np.linspace(0, rays.n, threads + 1).astype(np.int64)
+    ts = [threading.Thread(target=render_forward, args=(field, rays, bg, int(bounds[i]), int(bounds[i + 1]),
+                                                        out, tau)) for i in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return out, tau
+
+
+def render_backward_threaded(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, threads: int = 1):
+    """Backward with per-thread private gradient buffers, summed in thread order."""
+    bounds = np.linspace(0, rays.n, threads + 1).astype(np.int64)
+    parts = [([np.zeros_like(a) for a in field.grid], np.zeros_like(field.params)) for _ in range(threads)]
+    ts = [threading.Thread(target=render_backward,
+                           kwargs=dict(field=field, rays=rays, grad_out=grad_out, grad_tau=grad_tau, bg=bg,
+                                       r0=int(bounds[i]), r1=int(bounds[i + 1]), grads=parts[i]))
+          for i in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    gg = [sum(p[0][k] for p in parts) for k in range(len(field.grid))]
+    gp = sum(p[1] for p in parts)
+    return gg, gp

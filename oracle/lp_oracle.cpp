@@ -1,0 +1,419 @@
+// lp_oracle.cpp -- plain, slow, obviously-correct CPU oracle for the Lightplane
+// Renderer (Cao et al., arXiv 2404.19760). TEST INFRASTRUCTURE ONLY: it may be
+// loaded by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+// --impl reference legs, never by the product path. It shares no code, header
+// or constant with paper_2404_19760_b200/ (the CUDA path).
+//
+// Everything is fp64. One ray at a time, rays in index order, gradient sums in
+// ray order. The forward is the "store-all" (naive) evaluation of Eq. 1 that
+// the paper's fused kernel avoids, and the backward is the
+// hand-derived reverse mode over the stored per-sample values (Eq. 3, P:337-348,
+// extended by the background and tau terms, readings R5, R12).
+//
+// Citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n.
+//
+// Parity pins: every function below is pinned by tests/test_oracle_*.py
+// (closed forms, special cases, adjointness, finite differences, literal
+// O(S^2) derivative, invariants). None is "parity unpinned".
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+namespace {
+
+struct Field {
+  int kind;        // 0 = triplane, 1 = voxel
+  int H, W, D, K;  // resolution along x, y, z; channels
+  const double* plane[3];
+  int n_layers;    // number of Linear layers
+  const int* widths;   // n_layers + 1 entries
+  const double* params;  // W_0[w1][w0], b_0[w1], W_1[w2][w1], b_1[w2], ...
+};
+
+struct Tap {
+  int plane;
+  int64_t cell;    // index of the K-vector within its plane / volume
+  double w;
+};
+
+// O1: hashing scheme h (P:202 trilinear on voxels; P:207-210 bilinear on the
+// (x,y), (y,z), (z,x) planes, summed). World cube [-1,1]^3 -> index space
+// [0, N-1] per axis (reading R8); a point with any |x_a| > 1 samples zero and
+// has no taps (reading R11).
+void axis(double x, int N, int* i, double* f) {
+  double u = (x + 1.0) * 0.5 * (double)(N - 1);
+  int ii = (int)std::floor(u);
+  if (ii > N - 2) ii = N - 2;
+  if (ii < 0) ii = 0;
+  *i = ii;
+  *f = u - (double)ii;
+}
+
+void sample_taps(const Field& F, const double x[3], std::vector<Tap>& taps) {
+  taps.clear();
+  if (std::fabs(x[0]) > 1.0 || std::fabs(x[1]) > 1.0 || std::fabs(x[2]) > 1.0) return;
+  int ix, iy, iz;
+  double fx, fy, fz;
+  axis(x[0], F.H, &ix, &fx);
+  axis(x[1], F.W, &iy, &fy);
+  axis(x[2], F.D, &iz, &fz);
+  if (F.kind == 1) {
+    for (int dx = 0; dx < 2; ++dx)
+      for (int dy = 0; dy < 2; ++dy)
+        for (int dz = 0; dz < 2; ++dz) {
+          double w = (dx ? fx : 1.0 - fx) * (dy ? fy : 1.0 - fy) * (dz ? fz : 1.0 - fz);
+          int64_t cell = ((int64_t)(ix + dx) * F.W + (iy + dy)) * F.D + (iz + dz);
+          taps.push_back({0, cell, w});
+        }
+  } else {
+    // plane 0: xy, [H][W]; plane 1: yz, [W][D]; plane 2: zx, [D][H]
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        taps.push_back({0, (int64_t)(ix + a) * F.W + (iy + b), (a ? fx : 1 - fx) * (b ? fy : 1 - fy)});
+      }
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        taps.push_back({1, (int64_t)(iy + a) * F.D + (iz + b), (a ? fy : 1 - fy) * (b ? fz : 1 - fz)});
+      }
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        taps.push_back({2, (int64_t)(iz + a) * F.H + (ix + b), (a ? fz : 1 - fz) * (b ? fx : 1 - fx)});
+      }
+  }
+}
+
+void gather(const Field& F, const std::vector<Tap>& taps, double* h) {
+  for (int k = 0; k < F.K; ++k) h[k] = 0.0;
+  for (const Tap& t : taps) {
+    const double* v = F.plane[t.plane] + t.cell * F.K;
+    for (int k = 0; k < F.K; ++k) h[k] += t.w * v[k];
+  }
+}
+
+void scatter(const Field& F, const std::vector<Tap>& taps, const double* dh, double* const* grad) {
+  for (const Tap& t : taps) {
+    double* g = grad[t.plane] + t.cell * F.K;
+    for (int k = 0; k < F.K; ++k) g[k] += t.w * dh[k];
+  }
+}
+
+// O2: the tiny MLP g, one network K -> H ... -> 1 + C (reading R6):
+// z_l = W_l a_{l-1} + b_l, ReLU on hidden layers, identity on the last.
+// zs[l] holds z_{l}, as[l] holds a_l (as[0] = input).
+struct MlpTrace {
+  std::vector<std::vector<double>> z, a;
+};
+
+void mlp_forward(const Field& F, const double* in, MlpTrace& tr) {
+  const int L = F.n_layers;
+  tr.z.assign(L, {});
+  tr.a.assign(L + 1, {});
+  tr.a[0].assign(in, in + F.widths[0]);
+  const double* p = F.params;
+  for (int l = 0; l < L; ++l) {
+    int fin = F.widths[l], fout = F.widths[l + 1];
+    const double* Wl = p;
+    const double* bl = p + (int64_t)fout * fin;
+    p = bl + fout;
+    tr.z[l].assign(fout, 0.0);
+    for (int i = 0; i < fout; ++i) {
+      double s = bl[i];
+      for (int k = 0; k < fin; ++k) s += Wl[(int64_t)i * fin + k] * tr.a[l][k];
+      tr.z[l][i] = s;
+    }
+    tr.a[l + 1] = tr.z[l];
+    if (l < L - 1)
+      for (double& v : tr.a[l + 1]) v = v > 0.0 ? v : 0.0;
+  }
+}
+
+// Reverse mode through the MLP: given dL/d(output z_{L-1}), accumulate
+// parameter gradients and return dL/d(input).
+void mlp_backward(const Field& F, const MlpTrace& tr, const double* dout, double* grad_params, double* din) {
+  const int L = F.n_layers;
+  std::vector<int64_t> off(L);
+  int64_t o = 0;
+  for (int l = 0; l < L; ++l) {
+    off[l] = o;
+    o += (int64_t)F.widths[l + 1] * F.widths[l] + F.widths[l + 1];
+  }
+  std::vector<double> delta(dout, dout + F.widths[L]);
+  for (int l = L - 1; l >= 0; --l) {
+    int fin = F.widths[l], fout = F.widths[l + 1];
+    const double* Wl = F.params + off[l];
+    double* gW = grad_params + off[l];
+    double* gb = gW + (int64_t)fout * fin;
+    for (int i = 0; i < fout; ++i) {
+      gb[i] += delta[i];
+      for (int k = 0; k < fin; ++k) gW[(int64_t)i * fin + k] += delta[i] * tr.a[l][k];
+    }
+    std::vector<double> prev(fin, 0.0);
+    for (int k = 0; k < fin; ++k) {
+      double s = 0.0;
+      for (int i = 0; i < fout; ++i) s += Wl[(int64_t)i * fin + k] * delta[i];
+      prev[k] = s;
+    }
+    if (l > 0)  // through the ReLU of layer l-1 (ReLU'(0) = 0)
+      for (int k = 0; k < fin; ++k) prev[k] = tr.z[l - 1][k] > 0.0 ? prev[k] : 0.0;
+    delta.swap(prev);
+  }
+  for (int k = 0; k < F.widths[0]; ++k) din[k] = delta[k];
+}
+
+// O3: heads (reading R7): sigma = softplus(o_0), c_k = sigmoid(o_k).
+double softplus(double x) { return (x > 0.0 ? x : 0.0) + std::log1p(std::exp(-std::fabs(x))); }
+double sigmoid(double x) { return 1.0 / (1.0 + std::exp(-x)); }
+
+// Everything stored for one ray by the store-all forward.
+struct RayTrace {
+  int S;
+  double delta;
+  std::vector<std::vector<Tap>> taps;
+  std::vector<MlpTrace> mlp;
+  std::vector<double> sigma, tau, T, w;   // tau_j = sum_{n<=j} Delta sigma_n, T_j = exp(-tau_j)
+  std::vector<std::vector<double>> c;     // colours c_j (C each)
+};
+
+// O4: store-all forward of Eq. 1 for ray r.
+// x_j = o + (near + j Delta) d, Delta = max(far - near, 0)/R, j = 0..R (P:234,
+// P:247; reading R2). Weights w_0 = 0 and, for j >= 1,
+// w_j = T_{j-1} - T_j evaluated as e^{-tau_{j-1}} (-expm1(-Delta sigma_j))
+// (reading R13; the same number, without the cancellation).
+void trace_ray(const Field& F, const double* o, const double* d, double nearv, double farv, int S,
+               RayTrace& rt) {
+  const int C = F.widths[F.n_layers] - 1;
+  const int R = S - 1;
+  rt.S = S;
+  double span = farv - nearv;
+  rt.delta = (span > 0.0 ? span : 0.0) / (double)R;
+  rt.taps.assign(S, {});
+  rt.mlp.assign(S, {});
+  rt.sigma.assign(S, 0.0);
+  rt.tau.assign(S, 0.0);
+  rt.T.assign(S, 0.0);
+  rt.w.assign(S, 0.0);
+  rt.c.assign(S, std::vector<double>(C, 0.0));
+  std::vector<double> h(F.K);
+  double tau_prev = 0.0;
+  for (int j = 0; j < S; ++j) {
+    double t = nearv + (double)j * rt.delta;
+    double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+    sample_taps(F, x, rt.taps[j]);
+    gather(F, rt.taps[j], h.data());
+    mlp_forward(F, h.data(), rt.mlp[j]);
+    const std::vector<double>& out = rt.mlp[j].a[F.n_layers];
+    rt.sigma[j] = softplus(out[0]);
+    for (int k = 0; k < C; ++k) rt.c[j][k] = sigmoid(out[1 + k]);
+    double ds = rt.delta * rt.sigma[j];
+    rt.tau[j] = tau_prev + ds;
+    rt.T[j] = std::exp(-rt.tau[j]);
+    rt.w[j] = (j == 0) ? 0.0 : std::exp(-tau_prev) * (-std::expm1(-ds));
+    tau_prev = rt.tau[j];
+  }
+}
+
+void finish_forward(const Field& F, const RayTrace& rt, const double* bg, double* out, double* tau_out) {
+  const int C = F.widths[F.n_layers] - 1;
+  const int R = rt.S - 1;
+  for (int k = 0; k < C; ++k) {
+    double v = 0.0;
+    for (int j = 1; j <= R; ++j) v += rt.w[j] * rt.c[j][k];
+    out[k] = v + rt.T[R] * (bg ? bg[k] : 0.0);
+  }
+  *tau_out = rt.tau[R];
+}
+
+// O5 / O7: backward for one ray. Loss convention L = p.out + g_tau * tau_R.
+// mode 0: Eq. 3 via suffix sums over the stored w_j a_j:
+//   dL/dsigma_q = -Delta (G_q - [q>=1] T_q a_q) + Delta g_tau,
+//   G_q = sum_{j>q} w_j a_j + T_R (p.bg),
+//   dL/dc_q = [q>=1] w_q p.
+// mode 1: literal derivative of Eq. 1 (O(S^2)):
+//   dout/dsigma_q = sum_{j>=1} (dT_{j-1}/dsigma_q - dT_j/dsigma_q) c_j + dT_R/dsigma_q bg,
+//   dT_j/dsigma_q = -Delta T_j [q <= j], T_{-1} = 1 (constant).
+void backward_ray(const Field& F, const RayTrace& rt, const double* bg, const double* p, double gtau, int mode,
+                  double* const* grad_planes, double* grad_params) {
+  const int C = F.widths[F.n_layers] - 1;
+  const int S = rt.S, R = S - 1;
+  const double Dl = rt.delta;
+  std::vector<double> a(S), dsig(S);
+  for (int j = 0; j < S; ++j) {
+    double s = 0.0;
+    for (int k = 0; k < C; ++k) s += p[k] * rt.c[j][k];
+    a[j] = s;
+  }
+  double b = 0.0;
+  if (bg)
+    for (int k = 0; k < C; ++k) b += p[k] * bg[k];
+  if (mode == 0) {
+    double G = rt.T[R] * b;  // G_R
+    for (int q = R; q >= 0; --q) {
+      dsig[q] = -Dl * (G - (q >= 1 ? rt.T[q] * a[q] : 0.0)) + Dl * gtau;
+      G += rt.w[q] * a[q];     // G_{q-1} = G_q + w_q a_q
+    }
+  } else {
+    for (int q = 0; q < S; ++q) {
+      double s = 0.0;
+      for (int j = 1; j <= R; ++j) {
+        double dTjm1 = (q <= j - 1) ? -Dl * rt.T[j - 1] : 0.0;
+        double dTj = (q <= j) ? -Dl * rt.T[j] : 0.0;
+        s += (dTjm1 - dTj) * a[j];
+      }
+      s += -Dl * rt.T[R] * b;  // q <= R always
+      dsig[q] = s + Dl * gtau;
+    }
+  }
+  std::vector<double> dout(1 + C), dh(F.K);
+  for (int q = 0; q < S; ++q) {
+    const std::vector<double>& o = rt.mlp[q].a[F.n_layers];
+    dout[0] = dsig[q] * sigmoid(o[0]);  // softplus' = sigmoid
+    for (int k = 0; k < C; ++k) {
+      double dc = (q >= 1) ? rt.w[q] * p[k] : 0.0;
+      dout[1 + k] = dc * rt.c[q][k] * (1.0 - rt.c[q][k]);
+    }
+    mlp_backward(F, rt.mlp[q], dout.data(), grad_params, dh.data());
+    scatter(F, rt.taps[q], dh.data(), grad_planes);
+  }
+}
+
+Field make_field(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
+                 int n_layers, const int* widths, const double* params) {
+  Field F;
+  F.kind = kind;
+  F.H = H;
+  F.W = W;
+  F.D = D;
+  F.K = K;
+  F.plane[0] = p0;
+  F.plane[1] = p1;
+  F.plane[2] = p2;
+  F.n_layers = n_layers;
+  F.widths = widths;
+  F.params = params;
+  return F;
+}
+
+int check(int kind, int H, int W, int D, int K, int n_layers, const int* widths, int S) {
+  if (kind != 0 && kind != 1) return 1;
+  if (H < 2 || W < 2 || D < 2 || K < 1) return 1;
+  if (n_layers < 1 || n_layers > 8) return 1;
+  if (widths[0] != K || widths[n_layers] < 2) return 1;
+  if (S < 2) return 1;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lpo_version(void) { return 1; }
+
+// h(x) for n points: h_out[n][K].
+int lpo_sample(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
+               int64_t n, const double* x, double* h_out) {
+  int w1[2] = {K, 2};
+  if (check(kind, H, W, D, K, 1, w1, 2)) return 1;
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, 0, nullptr, nullptr);
+  std::vector<Tap> taps;
+  for (int64_t i = 0; i < n; ++i) {
+    sample_taps(F, x + 3 * i, taps);
+    gather(F, taps, h_out + i * K);
+  }
+  return 0;
+}
+
+// Transpose of lpo_sample: g_planes[c] += sum_i w_{i,c} v_i (accumulates).
+int lpo_splat(int kind, int H, int W, int D, int K, int64_t n, const double* x, const double* v, double* g0,
+              double* g1, double* g2) {
+  int w1[2] = {K, 2};
+  if (check(kind, H, W, D, K, 1, w1, 2)) return 1;
+  Field F = make_field(kind, H, W, D, K, nullptr, nullptr, nullptr, 0, nullptr, nullptr);
+  double* g[3] = {g0, g1, g2};
+  std::vector<Tap> taps;
+  for (int64_t i = 0; i < n; ++i) {
+    sample_taps(F, x + 3 * i, taps);
+    scatter(F, taps, v + i * K, g);
+  }
+  return 0;
+}
+
+// MLP forward for n inputs: out[n][widths[n_layers]].
+int lpo_mlp_forward(int n_layers, const int* widths, const double* params, int64_t n, const double* in,
+                    double* out) {
+  Field F = make_field(0, 2, 2, 2, widths[0], nullptr, nullptr, nullptr, n_layers, widths, params);
+  MlpTrace tr;
+  for (int64_t i = 0; i < n; ++i) {
+    mlp_forward(F, in + i * widths[0], tr);
+    for (int k = 0; k < widths[n_layers]; ++k) out[i * widths[n_layers] + k] = tr.a[n_layers][k];
+  }
+  return 0;
+}
+
+// MLP VJP for n inputs: accumulates grad_params, writes grad_in[n][K].
+int lpo_mlp_backward(int n_layers, const int* widths, const double* params, int64_t n, const double* in,
+                     const double* dout, double* grad_params, double* grad_in) {
+  Field F = make_field(0, 2, 2, 2, widths[0], nullptr, nullptr, nullptr, n_layers, widths, params);
+  MlpTrace tr;
+  for (int64_t i = 0; i < n; ++i) {
+    mlp_forward(F, in + i * widths[0], tr);
+    mlp_backward(F, tr, dout + i * widths[n_layers], grad_params, grad_in + i * widths[0]);
+  }
+  return 0;
+}
+
+// Forward render of rays [r0, r1): out[M][C], tau_out[M] (optical depth tau_R).
+int lpo_render_forward(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
+                       int n_layers, const int* widths, const double* params, int64_t r0, int64_t r1,
+                       const double* origins, const double* dirs, const double* nearv, const double* farv, int S,
+                       const double* bg, double* out, double* tau_out) {
+  if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params);
+  const int C = widths[n_layers] - 1;
+  RayTrace rt;
+  for (int64_t r = r0; r < r1; ++r) {
+    trace_ray(F, origins + 3 * r, dirs + 3 * r, nearv[r], farv[r], S, rt);
+    finish_forward(F, rt, bg, out + r * C, tau_out + r);
+  }
+  return 0;
+}
+
+// Backward of rays [r0, r1). grad_* are ACCUMULATED (+=). grad_tau may be NULL.
+// mode 0 = Eq. 3 suffix sums, mode 1 = literal O(S^2) derivative.
+int lpo_render_backward(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
+                        int n_layers, const int* widths, const double* params, int64_t r0, int64_t r1,
+                        const double* origins, const double* dirs, const double* nearv, const double* farv, int S,
+                        const double* bg, const double* grad_out, const double* grad_tau, double* g0, double* g1,
+                        double* g2, double* grad_params, int mode) {
+  if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params);
+  const int C = widths[n_layers] - 1;
+  double* g[3] = {g0, g1, g2};
+  RayTrace rt;
+  for (int64_t r = r0; r < r1; ++r) {
+    trace_ray(F, origins + 3 * r, dirs + 3 * r, nearv[r], farv[r], S, rt);
+    backward_ray(F, rt, bg, grad_out + r * C, grad_tau ? grad_tau[r] : 0.0, mode, g, grad_params);
+  }
+  return 0;
+}
+
+// Per-sample trace of one ray for invariant tests: sigma[S], tau[S], T[S], w[S], c[S][C].
+int lpo_trace(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
+              int n_layers, const int* widths, const double* params, const double* origin, const double* dir,
+              double nearv, double farv, int S, double* sigma, double* tau, double* T, double* w, double* c) {
+  if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params);
+  const int C = widths[n_layers] - 1;
+  RayTrace rt;
+  trace_ray(F, origin, dir, nearv, farv, S, rt);
+  for (int j = 0; j < S; ++j) {
+    sigma[j] = rt.sigma[j];
+    tau[j] = rt.tau[j];
+    T[j] = rt.T[j];
+    w[j] = rt.w[j];
+    for (int k = 0; k < C; ++k) c[j * C + k] = rt.c[j][k];
+  }
+  return 0;
+}
+
+}  // extern "C"

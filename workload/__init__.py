@@ -1,0 +1,282 @@
+"""Seeded synthetic workload generator shared by the oracle tests and the CUDA path.
+
+This module holds NONE of the method's arithmetic (no sampling, no MLP, no
+compositing): it only produces inputs -- grids, MLP parameters, rays, near/far,
+background colours and upstream gradients -- as plain float32 numpy arrays.
+Both `oracle/` (through `tests/` and `bench.py`'s cpu_baseline) and the CUDA
+path consume these arrays; neither side imports the other.
+
+Recipe:
+
+* Counter-based randomness: value(seed, i) = splitmix64 of (seed, i), so any
+  shard or subset of a tensor reproduces exactly the same numbers.
+* Cameras: V views on a Fibonacci sphere of radius 4 looking at the origin,
+  up = +z (fallback +y), pinhole with 30 deg field of view, one ray per pixel
+  centre (u+0.5, v+0.5), unit directions, raster order within a view, views in
+  index order. (Rays: "M rays ... R+1 points per ray";
+  pixel centres as SPEC.md S:193.)
+* near/far: per-ray slab intersection with the cube [-1+1e-4, 1-1e-4]^3, so
+  every sample of a hitting ray lies in the grid's domain (the paper's
+  contracted setting). Misses get near = far = 0 (Delta = 0).
+* Grid theta: i.i.d. U(-0.5, 0.5), seed 0, per element index.
+* MLP: W_l ~ U(+-1/sqrt(d_{l-1})) seed 1; hidden/colour biases 0;
+  sigma bias softplus^-1(1.2) unless overridden.
+* bg: U(0,1) seed 2 (parity) or zeros (throughput).
+* grad_out: U(-1,1) seed 3 keyed on (global ray index, channel);
+  grad_tau: U(-1,1) seed 4 keyed on global ray index (or None).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "Config", "CONFIGS", "get_config", "counter_uniform", "make_grid",
+    "make_mlp", "make_rays", "make_bg", "make_grad_out", "make_grad_tau",
+    "camera_positions", "softplus_inv", "subset_indices",
+]
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_C1 = np.uint64(0xBF58476D1CE4E5B9)
+_C2 = np.uint64(0x94D049BB133111EB)
+
+TRIPLANE = 0
+VOXEL = 1
+
+
+def _mix64(z: np.ndarray) -> np.ndarray:
+    """splitmix64 finaliser (Steele, Lea, Flood 2014) on a uint64 array."""
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * _C1
+        z = (z ^ (z >> np.uint64(27))) * _C2
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def counter_uniform(seed: int, idx: np.ndarray, lo: float, hi: float) -> np.ndarray:
+    """U(lo, hi) float32 values that depend only on (seed, idx).
+
+    24 random mantissa bits -> the value before scaling is exact in float32.
+    """
+    idx = np.asarray(idx, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        key = _mix64(np.uint64(seed) * _GOLDEN + _GOLDEN)
+        u = _mix64(key + idx * _GOLDEN)
+    u01 = (u >> np.uint64(40)).astype(np.float64) * (1.0 / (1 << 24))
+    return (lo + (hi - lo) * u01).astype(np.float32)
+
+
+def softplus_inv(y: float) -> float:
+    """x such that log(1 + e^x) = y (used only to pick a bias value)."""
+    return float(math.log(math.expm1(y)))
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    kind: int                 # TRIPLANE or VOXEL
+    res: int                  # H = W = D
+    K: int                    # grid channels
+    widths: tuple             # MLP widths (K, hidden..., 1 + C)
+    views: int
+    img: int                  # square image side
+    S: int                    # samples per ray = R + 1
+    note: str = ""
+
+    @property
+    def n_rays(self) -> int:
+        return self.views * self.img * self.img
+
+    @property
+    def C(self) -> int:
+        return self.widths[-1] - 1
+
+    @property
+    def grid_shapes(self) -> List[tuple]:
+        H = W = D = self.res
+        if self.kind == TRIPLANE:
+            return [(H, W, self.K), (W, D, self.K), (D, H, self.K)]
+        return [(H, W, D, self.K)]
+
+    @property
+    def grid_numel(self) -> int:
+        return int(sum(int(np.prod(s)) for s in self.grid_shapes))
+
+    @property
+    def n_params(self) -> int:
+        w = self.widths
+        return int(sum(w[i + 1] * w[i] + w[i + 1] for i in range(len(w) - 1)))
+
+
+# BASELINE.json "configs", read as in SURVEY.md §8.0 (A21-A24).
+CONFIGS = {
+    "c1": Config("c1", TRIPLANE, 16, 8, (8, 16, 4), 1, 64, 32,
+                 "triplane 3x16x16 C=8, MLP 8->16->4, 64x64 image, 32 samples/ray"),
+    "c2": Config("c2", VOXEL, 128, 16, (16, 32, 4), 1, 512, 256,
+                 "voxel 128^3 C=16, MLP hidden 32, 512x512 view, 256 samples/ray"),
+    "c3": Config("c3", TRIPLANE, 256, 32, (32, 64, 4), 1, 800, 512,
+                 "triplane 3x256x256 C=32, MLP hidden 64, 800x800, 512 samples/ray"),
+    "c4": Config("c4", TRIPLANE, 256, 32, (32, 64, 4), 128, 256, 128,
+                 "triplane 3x256x256 C=32, 128 views at 256x256 (8.4M rays), 128 samples/ray"),
+    "c5": Config("c5", VOXEL, 256, 32, (32, 64, 4), 64, 1024, 256,
+                 "voxel 256^3 C=32, 64 views at 1024x1024, 256 samples/ray"),
+    # The paper's own renderer MLP depth ("3-layer MLPs with a width of 64")
+    "c3p": Config("c3p", TRIPLANE, 256, 32, (32, 64, 64, 4), 1, 800, 512,
+                  "c3 with the paper's 3-layer width-64 MLP"),
+    "c4p": Config("c4p", TRIPLANE, 256, 32, (32, 64, 64, 4), 128, 256, 128,
+                  "c4 with the paper's 3-layer width-64 MLP"),
+}
+
+
+def get_config(name: str, **overrides) -> Config:
+    cfg = CONFIGS[name]
+    if overrides:
+        d = dict(cfg.__dict__)
+        d.update(overrides)
+        cfg = Config(**d)
+    return cfg
+
+
+def make_grid(cfg: Config, seed: int = 0, chunk: int = 1 << 24) -> List[np.ndarray]:
+    """theta ~ U(-0.5, 0.5) i.i.d., channel-last, keyed on the flat element index
+    (planes concatenated in xy, yz, zx order)."""
+    out = []
+    base = 0
+    for shape in cfg.grid_shapes:
+        n = int(np.prod(shape))
+        arr = np.empty(n, dtype=np.float32)
+        for s in range(0, n, chunk):
+            e = min(n, s + chunk)
+            arr[s:e] = counter_uniform(seed, np.arange(base + s, base + e, dtype=np.uint64), -0.5, 0.5)
+        out.append(arr.reshape(shape))
+        base += n
+    return out
+
+
+def make_mlp(widths: Sequence[int], seed: int = 1, sigma_bias: Optional[float] = None,
+             hidden_bias_scale: float = 0.0) -> np.ndarray:
+    """Packed params: W_0[w1][w0], b_0[w1], W_1[w2][w1], b_1[w2], ... (row-major out x in).
+
+    Output unit 0 is the density logit; its bias is sigma_bias
+    (default softplus^-1(1.2)); colour biases are 0.
+    hidden_bias_scale > 0 draws hidden biases U(+-scale) (tests only).
+    """
+    if sigma_bias is None:
+        sigma_bias = softplus_inv(1.2)
+    parts = []
+    off = 0
+    for l in range(len(widths) - 1):
+        fin, fout = widths[l], widths[l + 1]
+        a = 1.0 / math.sqrt(fin)
+        W = counter_uniform(seed, np.arange(off, off + fout * fin, dtype=np.uint64), -a, a)
+        off += fout * fin
+        if l < len(widths) - 2 and hidden_bias_scale > 0:
+            b = counter_uniform(seed + 1000, np.arange(off, off + fout, dtype=np.uint64),
+                                -hidden_bias_scale, hidden_bias_scale)
+        else:
+            b = np.zeros(fout, dtype=np.float32)
+        off += fout
+        if l == len(widths) - 2:
+            b[0] = np.float32(sigma_bias)
+        parts += [W.reshape(-1), b]
+    return np.concatenate(parts).astype(np.float32)
+
+
+def camera_positions(views: int, radius: float = 4.0) -> np.ndarray:
+    """Fibonacci-sphere camera centres (float64 [V][3])."""
+    i = np.arange(views, dtype=np.float64)
+    z = 1.0 - (2.0 * i + 1.0) / views
+    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    phi = i * math.pi * (3.0 - math.sqrt(5.0))
+    return radius * np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=1)
+
+
+def _camera_basis(c: np.ndarray):
+    fwd = -c / np.linalg.norm(c)
+    up = np.array([0.0, 0.0, 1.0])
+    if abs(float(fwd @ up)) > 0.999:
+        up = np.array([0.0, 1.0, 0.0])
+    right = np.cross(fwd, up)
+    right /= np.linalg.norm(right)
+    down = np.cross(fwd, right)
+    return right, down, fwd
+
+
+def make_rays(cfg: Config, idx: Optional[np.ndarray] = None, start: int = 0,
+              count: Optional[int] = None, fov_deg: float = 30.0, margin: float = 1e-4):
+    """Rays for global ray indices `idx` (or the contiguous range [start, start+count)).
+
+    Returns float32 arrays origins [n][3], dirs [n][3], near [n], far [n].
+    """
+    if idx is None:
+        if count is None:
+            count = cfg.n_rays - start
+        idx = np.arange(start, start + count, dtype=np.int64)
+    idx = np.asarray(idx, dtype=np.int64)
+    npix = cfg.img * cfg.img
+    view = idx // npix
+    pix = idx % npix
+    row = (pix // cfg.img).astype(np.float64)
+    col = (pix % cfg.img).astype(np.float64)
+    f = cfg.img / (2.0 * math.tan(math.radians(fov_deg) / 2.0))
+    cx = cy = cfg.img / 2.0
+    cams = camera_positions(cfg.views)
+    bases = np.stack([np.stack(_camera_basis(c), axis=0) for c in cams], axis=0)  # [V][3 axes][3]
+    xc = (col + 0.5 - cx) / f
+    yc = (row + 0.5 - cy) / f
+    B = bases[view]                                     # [n][3][3]
+    d = xc[:, None] * B[:, 0] + yc[:, None] * B[:, 1] + B[:, 2]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    o = cams[view]
+    # slab intersection with [-b, b]^3
+    b = 1.0 - margin
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inv = 1.0 / d
+        t1 = (-b - o) * inv
+        t2 = (b - o) * inv
+    tmin = np.max(np.minimum(t1, t2), axis=1)
+    tmax = np.min(np.maximum(t1, t2), axis=1)
+    near = np.maximum(tmin, 0.0)
+    hit = tmax > near
+    near = np.where(hit, near, 0.0)
+    far = np.where(hit, tmax, 0.0)
+    # pull [near, far] in by a relative hair so float32 rounding cannot leave the cube
+    span = far - near
+    near32 = np.where(hit, near + 1e-6 * span, 0.0).astype(np.float32)
+    far32 = np.where(hit, far - 1e-6 * span, 0.0).astype(np.float32)
+    return (o.astype(np.float32), d.astype(np.float32), near32, far32)
+
+
+def make_bg(C: int = 3, seed: int = 2, zero: bool = False) -> np.ndarray:
+    if zero:
+        return np.zeros(C, dtype=np.float32)
+    return counter_uniform(seed, np.arange(C, dtype=np.uint64), 0.0, 1.0)
+
+
+def make_grad_out(idx: np.ndarray, C: int = 3, seed: int = 3) -> np.ndarray:
+    idx = np.asarray(idx, dtype=np.uint64)
+    e = idx[:, None] * np.uint64(C) + np.arange(C, dtype=np.uint64)[None, :]
+    return counter_uniform(seed, e.reshape(-1), -1.0, 1.0).reshape(len(idx), C)
+
+
+def make_grad_tau(idx: np.ndarray, seed: int = 4) -> np.ndarray:
+    return counter_uniform(seed, np.asarray(idx, dtype=np.uint64), -1.0, 1.0)
+
+
+def subset_indices(cfg: Config, n: int = 4096, seed: int = 5) -> np.ndarray:
+    """The fixed parity / cpu-baseline subset: the first n/2 rays of view 0 taken
+    from the image centre rows (so most of them hit the cube) plus n/2
+    counter-random rays over the whole batch. Sorted, unique."""
+    if n >= cfg.n_rays:
+        return np.arange(cfg.n_rays, dtype=np.int64)
+    half = n // 2
+    npix = cfg.img * cfg.img
+    first = (npix // 2 - cfg.img // 2 + np.arange(half, dtype=np.int64)) % npix
+    r = counter_uniform(seed, np.arange(n - half, dtype=np.uint64), 0.0, 1.0).astype(np.float64)
+    rnd = np.minimum((r * cfg.n_rays).astype(np.int64), cfg.n_rays - 1)
+    allidx = np.unique(np.concatenate([first, rnd]))
+    return allidx
