@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""Benchmark of the fused Lightplane renderer hot path (forward + backward [+ grad all-reduce]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+A step = forward (K1) + backward (K2) over this rank's rays of the config (all
+SURVEY.md §8(a) rows), plus the NCCL all-reduce of the flat [grad theta | grad MLP]
+buffer when N > 1 (X1). Rays are sharded contiguously over ranks (strong scaling:
+the config's total ray count is fixed). Prints one JSON line on rank 0.
+
+Metric (BASELINE.json): rays/s fwd+bwd (whole job), peak memory bytes/ray,
+% roofline of the dominant kernel (K2 backward), see DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workload as wl  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0
+FP32_LANES_PER_SM = 128
+N_SM = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU work for the oracle baseline")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ algorithmic work
+def algorithmic_flops_per_sample(cfg):
+    """FP32 FLOPs (2 per FMA) per sample the method itself must do.
+    forward  K1: interpolation corners*K + MLP
+    backward K2: re-interpolation + scatter weighting 2*corners*K + MLP recompute + dX + dW = 3*MLP."""
+    corners = 12 if cfg.kind == wl.TRIPLANE else 8
+    w = cfg.widths
+    mlp = sum(w[i] * w[i + 1] for i in range(len(w) - 1))
+    fwd = corners * cfg.K + mlp
+    bwd = 2 * corners * cfg.K + 3 * mlp
+    return 2 * fwd, 2 * bwd
+
+
+def fp32_peak_tflops(sm_mhz):
+    return N_SM * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)), "measured"
+        except Exception:
+            pass
+    return {"hbm_gbs": FALLBACK_HBM_GBS, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def ncu_traffic(cfg_name, kernel="bwd"):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        e = d.get(cfg_name, {}).get(kernel)
+        if not e:
+            return None
+        # captured on a reduced ray count; scale per ray to this launch
+        return e
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU oracle baseline
+def cpu_oracle_rate(cfg, target_s: float, threads: int):
+    """Time the oracle (as it stands) fwd+bwd on a bounded, growing ray sample of the
+    workload until it has run >= target_s seconds in total; returns rays/s."""
+    import oracle
+    from tests.gpu_problem import grid_np
+    grid = grid_np(cfg.name)
+    params = wl.make_mlp(cfg.widths)
+    F = oracle.Field(cfg.kind, grid, cfg.widths, params)
+    n = max(threads, 8)
+    total_rays, total_t = 0, 0.0
+    idx_all = wl.subset_indices(cfg, 1 << 16)
+    pos = 0
+    while total_t < target_s:
+        idx = idx_all[pos:pos + n] if pos + n <= len(idx_all) else idx_all[:n]
+        pos += n
+        o, d, near, far = wl.make_rays(cfg, idx)
+        R = oracle.Rays(o, d, near, far, cfg.S)
+        go = wl.make_grad_out(idx, cfg.C)
+        t0 = time.perf_counter()
+        oracle.render_forward_threaded(F, R, None, threads=threads)
+        oracle.render_backward_threaded(F, R, go, None, None, threads=threads)
+        dt = time.perf_counter() - t0
+        total_rays += len(idx)
+        total_t += dt
+        if dt < target_s / 8:
+            n *= 2
+    return total_rays / total_t, total_rays, total_t
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = wl.get_config(args.config)
+    cores = host_cores()
+    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    rates = []
+    for i in range(args.warmup + args.steps):
+        rate, nrays, t = cpu_oracle_rate(cfg, per_step if i >= args.warmup else min(per_step, 2.0), cores)
+        if i >= args.warmup:
+            rates.append((rate, nrays, t))
+    value = sum(r[1] for r in rates) / sum(r[2] for r in rates)
+    ms = 1000.0 * cfg.n_rays / value / args.gpus
+    line = {
+        "impl": "reference", "metric": "rays/s fwd+bwd", "value": value, "unit": "rays/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(cfg, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "rays/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{sum(r[1] for r in rates)} rays of {cfg.name} (x{cfg.S} samples) fwd+bwd, "
+                                   f"fp64 store-all oracle, {cores} host threads"},
+        "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, n):
+    return {"workload": f"{cfg.name}: {cfg.note}", "rays": cfg.n_rays, "rays_per_gpu": cfg.n_rays // n,
+            "samples_per_ray": cfg.S, "grid": ("triplane" if cfg.kind == wl.TRIPLANE else "voxel"),
+            "grid_res": cfg.res, "K": cfg.K, "mlp": "->".join(map(str, cfg.widths)),
+            "parallelism": f"dp{n} (rays sharded, grad all-reduce)",
+            "l2": "inputs larger than L2 (rays + upstream grads per step > 126 MB); theta stays L2-resident "
+                  "by design (steady-state training)"}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2404_19760_b200 as lpb
+
+    cfg = wl.get_config(args.config)
+    M_all = cfg.n_rays
+    lo, hi = rank * M_all // world, (rank + 1) * M_all // world
+    M = hi - lo
+    S = cfg.S
+
+    # ---- field and flat gradient buffer [grad theta | grad MLP] (16-byte aligned pieces)
+    grid = wl.make_grid(cfg)
+    params = torch.from_numpy(wl.make_mlp(cfg.widths)).to(dev)
+    planes = [torch.from_numpy(g).to(dev) for g in grid]
+    field = lpb.Field(cfg.kind, planes, cfg.widths, params)
+    sizes = [p.numel() for p in planes] + [params.numel()]
+    offs = np.cumsum([0] + [((s + 3) // 4) * 4 for s in sizes])
+    flat = torch.zeros(int(offs[-1]), device=dev)
+    gplanes = [flat[offs[i]:offs[i] + sizes[i]].view(planes[i].shape) for i in range(len(planes))]
+    gparams = flat[offs[-2]:offs[-2] + sizes[-1]]
+
+    # ---- this rank's rays + upstream gradients, resident in HBM
+    chunk = 1 << 22
+    o = torch.empty((M, 3), device=dev)
+    d = torch.empty((M, 3), device=dev)
+    near = torch.empty((M,), device=dev)
+    far = torch.empty((M,), device=dev)
+    go = torch.empty((M, cfg.C), device=dev)
+    for s in range(0, M, chunk):
+        e = min(M, s + chunk)
+        oo, dd, nn, ff = wl.make_rays(cfg, start=lo + s, count=e - s)
+        o[s:e] = torch.from_numpy(oo)
+        d[s:e] = torch.from_numpy(dd)
+        near[s:e] = torch.from_numpy(nn)
+        far[s:e] = torch.from_numpy(ff)
+        go[s:e] = torch.from_numpy(wl.make_grad_out(np.arange(lo + s, lo + e), cfg.C))
+    bg = None
+    out = torch.empty((M, cfg.C), device=dev)
+    tau = torch.empty((M,), device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        flat.zero_()
+        if ev:
+            ev[0].record(stream)
+        lpb.render_forward(field, o, d, near, far, S, bg, out=out, tau=tau)
+        if ev:
+            ev[1].record(stream)
+        lpb.render_backward(field, o, d, near, far, S, tau, go, None, bg, grad_planes=gplanes, grad_params=gparams)
+        if ev:
+            ev[2].record(stream)
+        if world > 1:
+            dist.all_reduce(flat)
+        if ev:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- peak memory per ray (everything allocated beyond the field and its gradients)
+    torch.cuda.reset_peak_memory_stats(dev)
+    step()
+    torch.cuda.synchronize()
+    field_bytes = sum(p.numel() * 4 for p in planes) + params.numel() * 4 + flat.numel() * 4
+    peak = torch.cuda.max_memory_allocated(dev)
+    bytes_per_ray = (peak - field_bytes) / M
+
+    # ---- timed region
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = start.elapsed_time(stop)
+    t_fwd = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    t_bwd = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    t_ar = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_per_step = float(tt.item()) / args.steps
+    value = M_all / (ms_per_step / 1000.0)
+
+    # ---- e2e through the C-ABI host-buffer entry (pinned host inputs, host outputs)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda t: t.cpu().pin_memory()
+        oh, dh, nh, fh, goh = pin(o), pin(d), pin(near), pin(far), pin(go)
+        outh = torch.empty((M, cfg.C), pin_memory=True)
+        tauh = torch.empty((M,), pin_memory=True)
+        ws = None
+        for i in range(args.warmup + args.steps):
+            if i == args.warmup:
+                if world > 1:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+            flat.zero_()
+            _, _, _, _, ws = lpb.fwd_bwd_host(field, oh, dh, nh, fh, S, goh, None, None, outh, tauh, gplanes,
+                                              gparams, ws)
+            if world > 1:
+                dist.all_reduce(flat)
+                torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(dt.item()) * 1000.0 / args.steps
+        e2e = {"value": M_all / (e2e_ms / 1000.0), "unit": "rays/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(M * (12 + 12 + 4 + 4 + 4 * cfg.C)),
+               "d2h_bytes_per_step": int(M * (4 * cfg.C + 4)),
+               "api": "lp_render_fwd_bwd_host (C ABI) + NCCL all-reduce when N>1"}
+        del oh, dh, nh, fh, goh
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (K2 backward): FP32 ALU bound
+    peaks, peak_src = load_peaks()
+    clk_sum = clk.summary()
+    fwd_f, bwd_f = algorithmic_flops_per_sample(cfg)
+    samples = M * S
+    achieved = bwd_f * samples / (t_bwd / 1000.0) / 1e12
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak = fp32_peak_tflops(sm_max)
+    fwd_ach = fwd_f * samples / (t_fwd / 1000.0) / 1e12
+    traffic = ncu_traffic(cfg.name)
+    line = {
+        "metric": "rays/s fwd+bwd", "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(cfg, world),
+        "breakdown_ms": {"fwd": t_fwd, "bwd": t_bwd, "allreduce": t_ar},
+        "peak_bytes_per_ray": bytes_per_ray,
+        "roofline": {"bound": "alu", "kernel": "lp_bwd_kernel (K2)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": (traffic * M / traffic_rays(cfg.name)) if traffic else None,
+                     "peak_source": f"FP32 FFMA: {N_SM} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz "
+                                    f"(sm_max_mhz {peak_src})",
+                     "fwd_kernel": {"achieved": fwd_ach, "frac": fwd_ach / peak},
+                     "algorithmic_flops_per_sample": {"fwd": fwd_f, "bwd": bwd_f}},
+        "clocks": clk_sum,
+        "gpu_launches": 2 * args.steps,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline and world == 1:
+        cores = host_cores()
+        rate, nrays, t = cpu_oracle_rate(cfg, args.cpu_seconds, cores)
+        line["cpu_baseline"] = {"value": rate, "unit": "rays/s", "cores": cores, "kind": "oracle",
+                                "sample": f"{nrays} rays of {cfg.name} (x{cfg.S} samples) fwd+bwd, fp64 oracle, "
+                                          f"{t:.1f} s on {cores} host threads"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def traffic_rays(cfg_name):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    return json.load(open(p))[cfg_name]["rays"]
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,144 @@
+/* lp.h -- C ABI of the B200-native Lightplane Renderer hot path.
+ *
+ * The library computes the fused emission-absorption (EA) renderer of
+ * Cao et al., "Lightplane: Highly-Scalable Components for Neural 3D Fields"
+ * (arXiv 2404.19760), forward and backward, for a hybrid field f = g o h
+ * (PAPER.md P:197): a hashing scheme h on a triplane or voxel grid theta
+ * followed by a tiny MLP g.
+ *
+ *   forward  (Eq. 1; fused per ray):
+ *     v_i = sum_{j=1..R} (T_{i,j-1} - T_{ij}) f_v(x_ij) + T_{iR} bg,
+ *     T_ij = exp(-sum_{n=0..j} Delta_i sigma(x_in)),  x_ij = o_i + (near_i + j Delta_i) d_i,
+ *     Delta_i = max(far_i - near_i, 0) / R,  R = n_samples - 1.
+ *   backward (Eq. 3; reverse march from the cached final
+ *     transmittance, recomputing every activation).
+ *
+ * Readings of the paper used here are listed in DESIGN.md ("Readings"):
+ * one MLP K -> hidden... -> 1 + C with output 0 the density logit (R6),
+ * hidden ReLU, sigma = softplus, colour = sigmoid (R7), the cached per-ray
+ * scalar is the optical depth tau_R = -ln T_R (R12), background term T_R bg (R5).
+ *
+ * Conventions for every entry point:
+ *  - All array pointers are CUDA DEVICE pointers to fp32, C-contiguous,
+ *    unless the name ends in _host. The caller owns every buffer; the library
+ *    allocates no device memory and keeps no pointer after the call returns
+ *    (apart from stream-ordered use by the kernels it enqueued).
+ *  - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ *    stream) without host synchronisation, except lp_render_fwd_bwd_host.
+ *    Kernel faults surface at the caller's next synchronisation.
+ *  - Validation is host-side and happens before any launch, so nothing is
+ *    written on error. Device-resident values (NaNs, near > far) are not
+ *    inspected; they are documented preconditions.
+ *  - Errors: a non-LP_OK status; lp_last_error() returns a thread-local
+ *    message describing the last failure on the calling thread.
+ *  - Reentrant: the only global state is per-device launch-shape caches.
+ */
+#ifndef LP_H_
+#define LP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LP_ABI_VERSION 1
+#define LP_MAX_LAYERS 8
+
+typedef enum {
+  LP_OK = 0,
+  LP_ERR_INVALID_ARG = 1,  /* null pointer, bad size, broken width chain */
+  LP_ERR_UNSUPPORTED = 2,  /* no compiled kernel instance for (kind, K, widths) */
+  LP_ERR_MISALIGNED = 3,   /* a grid / gradient pointer is not 16-byte aligned */
+  LP_ERR_CUDA = 4          /* a CUDA runtime call or launch failed */
+} lp_status;
+
+typedef enum { LP_GRID_TRIPLANE = 0, LP_GRID_VOXEL = 1 } lp_grid_kind;
+
+/* theta, the 3D hash structure. Channel-last, K contiguous floats
+ * per grid vertex. Axis convention (reading R9): x <-> H, y <-> W, z <-> D;
+ * the world cube [-1,1]^3 maps to vertex index space [0, N-1] per axis
+ * (align-corners, reading R8); a sample with any |x_a| > 1 reads zero (R11).
+ *   triplane: data[0] = xy plane [H][W][K], data[1] = yz plane [W][D][K],
+ *             data[2] = zx plane [D][H][K]; h = sum of the three bilinear samples.
+ *   voxel:    data[0] = [H][W][D][K]; data[1], data[2] unused (may be NULL);
+ *             h = trilinear sample.
+ * Requirements: H, W, D >= 2; every data[] pointer 16-byte aligned;
+ * elements per plane/volume < 2^31. Compiled K values: 8, 16, 32. */
+typedef struct {
+  int32_t kind;           /* lp_grid_kind */
+  int32_t H, W, D;
+  int32_t K;
+  const float* data[3];
+} lp_grid;
+
+/* The tiny MLP g: n_layers Linear layers, ReLU between them,
+ * widths[0] = K, widths[n_layers] = 1 + C (output 0 = density logit, then C
+ * colour logits). params packs, per layer l, W_l as [widths[l+1]][widths[l]]
+ * row-major then b_l [widths[l+1]]. Compiled widths:
+ * (8,16,4), (16,32,4), (32,64,4) and (32,64,64,4). */
+typedef struct {
+  int32_t n_layers;
+  int32_t widths[LP_MAX_LAYERS + 1];
+  const float* params;
+} lp_mlp;
+
+/* The M rays r_i with R+1 = n_samples equispaced points each.
+ * dirs are expected unit length (Delta is a distance); they are not
+ * normalised. far <= near gives Delta = 0: out = bg, tau = 0, zero gradient. */
+typedef struct {
+  int64_t n_rays;         /* M >= 0 */
+  const float* origins;   /* [M][3] */
+  const float* dirs;      /* [M][3] */
+  const float* t_near;    /* [M] */
+  const float* t_far;     /* [M] */
+  int32_t n_samples;      /* S = R + 1 >= 2 */
+} lp_rays;
+
+/* Forward render (Eq. 1). bg: [C] or NULL (= zeros).
+ * out: [M][C], overwritten with v_i + T_iR bg.
+ * tau_out: [M], overwritten with tau_iR = sum_j Delta_i sigma(x_ij) = -ln T_iR,
+ * the one per-ray scalar the backward needs. */
+lp_status lp_render_forward(const lp_grid* grid, const lp_mlp* mlp, const lp_rays* rays, const float* bg,
+                            float* out, float* tau_out, void* stream);
+
+/* Backward (Eq. 3 by reverse marching) of the loss
+ *   L = sum_i <grad_out_i, out_i> + grad_tau_i * tau_i
+ * w.r.t. theta and the MLP parameters. tau: [M] from lp_render_forward with the
+ * same inputs. grad_out: [M][C]. grad_tau: [M] or NULL (= zeros).
+ * grad_data: same shapes as grid->data (grad_data[1..2] unused for voxels);
+ * grad_params: same packing as mlp->params. Both are ACCUMULATED (+=) with
+ * fp32 atomics (summation order nondeterministic); the caller zeroes them.
+ * No gradient is produced for rays, near/far or bg. */
+lp_status lp_render_backward(const lp_grid* grid, const lp_mlp* mlp, const lp_rays* rays, const float* bg,
+                             const float* tau, const float* grad_out, const float* grad_tau,
+                             float* const grad_data[3], float* grad_params, void* stream);
+
+/* End-to-end training step from HOST buffers (the e2e measurement path).
+ * rays_host, bg_host, grad_out_host, grad_tau_host (may be NULL) are HOST
+ * pointers (pinned memory recommended); grid, mlp, grad_data and grad_params
+ * are device-resident. The call copies the ray batch and upstream gradients to
+ * `workspace` (device, >= lp_fwd_bwd_host_workspace_bytes(M, C) bytes),
+ * runs forward and backward, copies out/tau back to out_host / tau_host
+ * (HOST, [M][C] and [M]) and synchronises `stream` before returning. */
+size_t lp_fwd_bwd_host_workspace_bytes(int64_t n_rays, int32_t C);
+lp_status lp_render_fwd_bwd_host(const lp_grid* grid, const lp_mlp* mlp, const lp_rays* rays_host,
+                                 const float* bg_host, const float* grad_out_host, const float* grad_tau_host,
+                                 float* out_host, float* tau_host, float* const grad_data[3], float* grad_params,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Optional: keep theta resident in L2 for kernels launched by this library on
+ * the calling thread's current device (access-policy window on each launch,
+ * hit ratio in (0,1]; 0 disables). Sets cudaLimitPersistingL2CacheSize. */
+lp_status lp_set_l2_persist(float hit_ratio);
+
+/* Thread-local description of the last non-OK status on this thread. */
+const char* lp_last_error(void);
+int lp_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LP_H_ */

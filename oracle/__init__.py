@@ -59,7 +59,9 @@ def lib():
                                               P, P, P, P, i32, P, P, P, P, P, P, P, i32]
             L.lpo_trace.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, P, P, f64, f64, i32,
                                     P, P, P, P, P]
-            for f in (L.lpo_sample, L.lpo_splat, L.lpo_mlp_forward, L.lpo_mlp_backward,
+            L.lpo_render_min_preact.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
+                                                P, P, P, P, i32, P]
+            for f in (L.lpo_render_min_preact, L.lpo_sample, L.lpo_splat, L.lpo_mlp_forward, L.lpo_mlp_backward,
                       L.lpo_render_forward, L.lpo_render_backward, L.lpo_trace):
                 f.restype = ctypes.c_int
             _lib = L
@@ -185,6 +187,16 @@ def render_backward(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, 
                                    _p(rays.far), rays.S, _p(bgd), _p(go), _p(gt), *gp, _p(gpar), mode)
     assert rc == 0
     return gg, gpar
+
+
+def min_preact(field: Field, rays: Rays) -> np.ndarray:
+    """Per ray: min over samples / hidden units of |z| / (sum |W a| + |b|) (see lp_oracle.cpp)."""
+    out = np.zeros(rays.n)
+    rc = lib().lpo_render_min_preact(*field._geom(), *field._planes(), field.n_layers, _p(field.widths),
+                                     _p(field.params), 0, rays.n, _p(rays.o), _p(rays.d), _p(rays.near),
+                                     _p(rays.far), rays.S, _p(out))
+    assert rc == 0
+    return out
 
 
 def trace(field: Field, origin, direction, near: float, far: float, S: int):

@@ -416,4 +416,42 @@ int lpo_trace(int kind, int H, int W, int D, int K, const double* p0, const doub
   return 0;
 }
 
+// Conditioning of the ReLU decisions along each ray [r0, r1): the minimum over
+// samples and hidden units of |z| / (sum_k |W_ik a_k| + |b_i|). A hidden
+// pre-activation within rounding of 0 makes ReLU'(z) (reading R7,
+// ReLU'(0) = 0) a decision that fp32 and fp64 evaluations may take
+// differently; both are correct roundings, so parity tests exclude such rays
+// from gradient comparison.
+int lpo_render_min_preact(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
+                          int n_layers, const int* widths, const double* params, int64_t r0, int64_t r1,
+                          const double* origins, const double* dirs, const double* nearv, const double* farv, int S,
+                          double* min_rel) {
+  if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params);
+  RayTrace rt;
+  for (int64_t r = r0; r < r1; ++r) {
+    trace_ray(F, origins + 3 * r, dirs + 3 * r, nearv[r], farv[r], S, rt);
+    double best = INFINITY;
+    for (int j = 0; j < S; ++j) {
+      const double* p = F.params;
+      for (int l = 0; l < n_layers - 1; ++l) {
+        int fin = widths[l], fout = widths[l + 1];
+        const double* Wl = p;
+        const double* bl = p + (int64_t)fout * fin;
+        p = bl + fout;
+        for (int i = 0; i < fout; ++i) {
+          double sc = std::fabs(bl[i]);
+          for (int k = 0; k < fin; ++k) sc += std::fabs(Wl[(int64_t)i * fin + k] * rt.mlp[j].a[l][k]);
+          if (sc > 0.0) {
+            double q = std::fabs(rt.mlp[j].z[l][i]) / sc;
+            if (q < best) best = q;
+          }
+        }
+      }
+    }
+    min_rel[r - r0] = best;
+  }
+  return 0;
+}
+
 }  // extern "C"

@@ -1,0 +1,102 @@
+"""ctypes binding of include/lp.h (argument marshalling only).
+
+Loads the in-tree liblp_b200.so. There is no fallback: if the library is
+missing or fails to load, import raises. Every step of the hot path runs in
+the library's CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblp_b200.so")
+
+LP_OK, LP_ERR_INVALID_ARG, LP_ERR_UNSUPPORTED, LP_ERR_MISALIGNED, LP_ERR_CUDA = range(5)
+LP_GRID_TRIPLANE, LP_GRID_VOXEL = 0, 1
+LP_MAX_LAYERS = 8
+_STATUS = {0: "LP_OK", 1: "LP_ERR_INVALID_ARG", 2: "LP_ERR_UNSUPPORTED", 3: "LP_ERR_MISALIGNED", 4: "LP_ERR_CUDA"}
+
+# Every symbol include/lp.h declares (tests check the library exports them all).
+EXPORTED = ("lp_render_forward", "lp_render_backward", "lp_fwd_bwd_host_workspace_bytes",
+            "lp_render_fwd_bwd_host", "lp_set_l2_persist", "lp_last_error", "lp_abi_version")
+
+
+class LpGrid(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("H", ctypes.c_int32), ("W", ctypes.c_int32), ("D", ctypes.c_int32),
+                ("K", ctypes.c_int32), ("data", ctypes.c_void_p * 3)]
+
+
+class LpMlp(ctypes.Structure):
+    _fields_ = [("n_layers", ctypes.c_int32), ("widths", ctypes.c_int32 * (LP_MAX_LAYERS + 1)),
+                ("params", ctypes.c_void_p)]
+
+
+class LpRays(ctypes.Structure):
+    _fields_ = [("n_rays", ctypes.c_int64), ("origins", ctypes.c_void_p), ("dirs", ctypes.c_void_p),
+                ("t_near", ctypes.c_void_p), ("t_far", ctypes.c_void_p), ("n_samples", ctypes.c_int32)]
+
+
+class LpError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2404_19760_b200.build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    gp, mp, rp = ctypes.POINTER(LpGrid), ctypes.POINTER(LpMlp), ctypes.POINTER(LpRays)
+    L.lp_render_forward.argtypes = [gp, mp, rp, P, P, P, P]
+    L.lp_render_backward.argtypes = [gp, mp, rp, P, P, P, P, ctypes.POINTER(ctypes.c_void_p), P, P]
+    L.lp_fwd_bwd_host_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int32]
+    L.lp_fwd_bwd_host_workspace_bytes.restype = ctypes.c_size_t
+    L.lp_render_fwd_bwd_host.argtypes = [gp, mp, rp, P, P, P, P, P, ctypes.POINTER(ctypes.c_void_p), P, P,
+                                         ctypes.c_size_t, P]
+    L.lp_set_l2_persist.argtypes = [ctypes.c_float]
+    L.lp_last_error.restype = ctypes.c_char_p
+    for f in (L.lp_render_forward, L.lp_render_backward, L.lp_render_fwd_bwd_host, L.lp_set_l2_persist,
+              L.lp_abi_version):
+        f.restype = ctypes.c_int
+    return L
+
+
+lib = _load()
+
+
+def check(status: int):
+    if status != LP_OK:
+        raise LpError(status, lib.lp_last_error().decode())
+
+
+def make_grid(kind: int, H: int, W: int, D: int, K: int, ptrs) -> LpGrid:
+    g = LpGrid()
+    g.kind, g.H, g.W, g.D, g.K = kind, H, W, D, K
+    for i in range(3):
+        g.data[i] = ptrs[i] if i < len(ptrs) else None
+    return g
+
+
+def make_mlp(widths, params_ptr) -> LpMlp:
+    m = LpMlp()
+    m.n_layers = len(widths) - 1
+    for i, w in enumerate(widths):
+        m.widths[i] = int(w)
+    m.params = params_ptr
+    return m
+
+
+def make_rays(n: int, o, d, near, far, S: int) -> LpRays:
+    r = LpRays()
+    r.n_rays, r.origins, r.dirs, r.t_near, r.t_far, r.n_samples = n, o, d, near, far, S
+    return r
+
+
+def ptr_array3(ptrs):
+    arr = (ctypes.c_void_p * 3)()
+    for i in range(3):
+        arr[i] = ptrs[i] if i < len(ptrs) else None
+    return arr

@@ -1,0 +1,65 @@
+"""The C-ABI library loads, exports every symbol include/lp.h declares, and
+rejects bad arguments host-side before any CUDA call (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "lp.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:lp_status|size_t|const char\*|int)\s+(lp_\w+)\s*\(", src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2404_19760_b200 import _lib
+    return _lib
+
+
+def test_library_exports_every_declared_symbol(L):
+    declared = _declared_symbols()
+    assert len(declared) >= 7
+    for name in declared:
+        assert hasattr(L.lib, name), name
+    assert set(declared) == set(L.EXPORTED)
+    assert L.lib.lp_abi_version() == 1
+
+
+def _args(L, K=8, widths=(8, 16, 4), kind=0, ptr=0x1000, S=8, n=4):
+    g = L.make_grid(kind, 4, 4, 4, K, [ptr, ptr, ptr])
+    m = L.make_mlp(widths, ptr)
+    r = L.make_rays(n, ptr, ptr, ptr, ptr, S)
+    return g, m, r
+
+
+def _fwd(L, g, m, r):
+    p = ctypes.c_void_p(0x2000)
+    return L.lib.lp_render_forward(ctypes.byref(g), ctypes.byref(m), ctypes.byref(r), None, p, p, None)
+
+
+def test_validation_errors(L):
+    g, m, r = _args(L)
+    assert L.lib.lp_render_forward(None, ctypes.byref(m), ctypes.byref(r), None, None, None, None) == L.LP_ERR_INVALID_ARG
+    assert "null" in L.lib.lp_last_error().decode()
+    g, m, r = _args(L, S=1)
+    assert _fwd(L, g, m, r) == L.LP_ERR_INVALID_ARG
+    g, m, r = _args(L, K=12, widths=(12, 16, 4))
+    assert _fwd(L, g, m, r) == L.LP_ERR_UNSUPPORTED
+    g, m, r = _args(L, widths=(4, 16, 4))
+    assert _fwd(L, g, m, r) == L.LP_ERR_INVALID_ARG
+    g, m, r = _args(L, ptr=0x1004)
+    assert _fwd(L, g, m, r) == L.LP_ERR_MISALIGNED
+    g, m, r = _args(L, kind=5)
+    assert _fwd(L, g, m, r) == L.LP_ERR_INVALID_ARG
+    g, m, r = _args(L, widths=(8, 16, 32, 4))      # 3 layers with mismatched hidden widths
+    assert _fwd(L, g, m, r) == L.LP_ERR_UNSUPPORTED
+    assert L.lib.lp_set_l2_persist(ctypes.c_float(2.0)) == L.LP_ERR_INVALID_ARG
+
+
+def test_workspace_size(L):
+    n = L.lib.lp_fwd_bwd_host_workspace_bytes(1000, 3)
+    assert n >= 1000 * (12 + 12 + 4 + 4 + 12 + 12 + 4 + 4)

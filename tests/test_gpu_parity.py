@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same
+seeded inputs. Tolerances (BASELINE.json north_star): rendered images and tau
+1e-4, gradients 1e-3, both as ||gpu - ref||_inf / ||ref||_inf per tensor
+(DESIGN.md "Parity metric")."""
+import numpy as np
+import pytest
+
+import oracle
+import workload as wl
+from tests.gpu_problem import oracle_field, oracle_rays, problem_np, to_cuda, unambiguous
+from tests.helpers import rel_inf
+
+pytestmark = pytest.mark.gpu
+
+TOL_IMG = 1e-4
+TOL_GRAD = 1e-3
+
+# configs and the ray-subset size the oracle handles in seconds
+CASES = [("c1", 4096), ("c2", 1024), ("c3", 512), ("c4", 2048), ("c5", 512), ("c3p", 256), ("c4p", 1024)]
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2404_19760_b200  # noqa: F401  (loads liblp_b200.so or fails)
+    return torch
+
+
+def _gpu_fwd_bwd(torch, pb, grad=True):
+    import paper_2404_19760_b200 as lpb
+    field, t = to_cuda(pb)
+    out, tau = lpb.render_forward(field, t["o"], t["d"], t["near"], t["far"], pb["cfg"].S, t["bg"])
+    res = dict(out=out.cpu().numpy(), tau=tau.cpu().numpy())
+    if grad:
+        gpl, gpar = lpb.render_backward(field, t["o"], t["d"], t["near"], t["far"], pb["cfg"].S, tau, t["go"],
+                                        t["gt"], t["bg"])
+        res["gplanes"] = [g.cpu().numpy() for g in gpl]
+        res["gparams"] = gpar.cpu().numpy()
+    torch.cuda.synchronize()
+    return res
+
+
+def _oracle_fwd_bwd(pb, grad=True):
+    F, R = oracle_field(pb), oracle_rays(pb)
+    out, tau = oracle.render_forward(F, R, pb["bg"])
+    res = dict(out=out, tau=tau)
+    if grad:
+        gg, gp = oracle.render_backward_threaded(F, R, pb["go"], pb["gt"], pb["bg"], threads=8)
+        res["gplanes"], res["gparams"] = gg, gp
+    return res
+
+
+def _compare(g, r, grad=True):
+    errs = dict(out=rel_inf(g["out"], r["out"]), tau=rel_inf(g["tau"], r["tau"]))
+    if grad:
+        for i, (a, b) in enumerate(zip(g["gplanes"], r["gplanes"])):
+            errs[f"gplane{i}"] = rel_inf(a, b)
+        errs["gparams"] = rel_inf(g["gparams"], r["gparams"])
+    return errs
+
+
+def _assert(errs):
+    print(errs)
+    assert errs["out"] < TOL_IMG and errs["tau"] < TOL_IMG, errs
+    for k, v in errs.items():
+        if k.startswith("g"):
+            assert v < TOL_GRAD, errs
+
+
+@pytest.mark.parametrize("cfg,n", CASES)
+def test_parity_subset(torch_cuda, cfg, n):
+    """F1-F7 and B1-B7 on every config: forward images/tau on all subset rays,
+    all gradients on the rays with well-conditioned ReLU decisions."""
+    pb = problem_np(cfg, n=n)
+    g, r = _gpu_fwd_bwd(torch_cuda, pb, grad=False), _oracle_fwd_bwd(pb, grad=False)
+    _assert(_compare(g, r, grad=False))
+    q = unambiguous(pb)
+    assert len(q["idx"]) >= len(pb["idx"]) // 2
+    _assert(_compare(_gpu_fwd_bwd(torch_cuda, q), _oracle_fwd_bwd(q)))
+
+
+@pytest.mark.parametrize("sigma_bias,label", [(-30.0, "empty"), (60.0, "opaque"), (2.5, "dense")])
+def test_parity_density_regimes(torch_cuda, sigma_bias, label):
+    """Empty field (out = bg), opaque field (tau_R ~ 100: T_R denormal/zero in
+    fp32, reading R12) and a dense field, c2 shapes."""
+    pb = unambiguous(problem_np("c2", n=512, sigma_bias=sigma_bias))
+    g, r = _gpu_fwd_bwd(torch_cuda, pb), _oracle_fwd_bwd(pb)
+    if label == "empty":
+        assert np.max(np.abs(g["out"] - pb["bg"][None])) < 1e-6
+    if label == "opaque":
+        assert np.max(r["tau"]) > 80
+    _assert(_compare(g, r))
+
+
+def test_ragged_tail_and_misses(torch_cuda):
+    """M not a multiple of the 128-ray tile, rays that miss the cube (near = far,
+    Delta = 0 -> out = bg, zero gradient) and minimal S = 2."""
+    cfg = "c1"
+    idx = np.arange(1000, dtype=np.int64) * 3 + 7
+    pb = problem_np(cfg, idx=idx)
+    pb["near"][::5] = pb["far"][::5] = 0.0        # forced misses
+    _assert(_compare(_gpu_fwd_bwd(torch_cuda, unambiguous(pb)), _oracle_fwd_bwd(unambiguous(pb))))
+    for S in (2, 3):
+        pb2 = dict(pb)
+        pb2["cfg"] = wl.get_config(cfg, S=S)
+        pb2 = unambiguous(pb2)
+        _assert(_compare(_gpu_fwd_bwd(torch_cuda, pb2), _oracle_fwd_bwd(pb2)))
+
+
+def test_zero_rays_is_noop(torch_cuda):
+    import paper_2404_19760_b200 as lpb
+    torch = torch_cuda
+    pb = problem_np("c1", idx=np.arange(4))
+    field, t = to_cuda(pb)
+    e = torch.zeros((0, 3), device="cuda")
+    z = torch.zeros((0,), device="cuda")
+    out, tau = lpb.render_forward(field, e, e, z, z, 8, None)
+    gpl, gpar = lpb.render_backward(field, e, e, z, z, 8, tau, out)
+    torch.cuda.synchronize()
+    assert out.shape == (0, 3) and float(gpar.abs().sum()) == 0.0
+
+
+@pytest.mark.parametrize("cfg,nsample", [("c2", 256), ("c4", 256)])
+def test_full_size_sampled_forward(torch_cuda, cfg, nsample):
+    """At BASELINE.json's full size, in bench.py's launch configuration: the
+    forward over all M rays, checked on sampled rays the oracle computes one by one."""
+    import paper_2404_19760_b200 as lpb
+    torch = torch_cuda
+    c = wl.get_config(cfg)
+    full = problem_np(cfg, idx=np.arange(c.n_rays, dtype=np.int64), with_gtau=False)
+    field, t = to_cuda(full)
+    out, tau = lpb.render_forward(field, t["o"], t["d"], t["near"], t["far"], c.S, t["bg"])
+    torch.cuda.synchronize()
+    pick = np.unique((wl.counter_uniform(9, np.arange(nsample, dtype=np.uint64), 0, 1) * c.n_rays).astype(np.int64))
+    sub = problem_np(cfg, idx=pick, with_gtau=False)
+    r = _oracle_fwd_bwd(sub, grad=False)
+    assert rel_inf(out[pick].cpu().numpy(), r["out"]) < TOL_IMG
+    assert rel_inf(tau[pick].cpu().numpy(), r["tau"]) < TOL_IMG
+
+
+def test_backward_additive_over_shards_and_linear(torch_cuda):
+    """Properties that hold at any size (c4 full batch of 8.4M rays is too big for
+    the oracle): backward(all) == backward(first half) + backward(second half)
+    (rays are independent), and backward(2p) == 2 backward(p)."""
+    import paper_2404_19760_b200 as lpb
+    torch = torch_cuda
+    c = wl.get_config("c4")
+    M = 1 << 20
+    pb = problem_np("c4", idx=np.arange(M, dtype=np.int64))
+    field, t = to_cuda(pb)
+    out, tau = lpb.render_forward(field, t["o"], t["d"], t["near"], t["far"], c.S, t["bg"])
+    g_all = lpb.render_backward(field, t["o"], t["d"], t["near"], t["far"], c.S, tau, t["go"], t["gt"], t["bg"])
+    h = M // 2 + 37
+    gp = [torch.zeros_like(p) for p in field.planes]
+    gq = torch.zeros_like(field.params)
+    for sl in (slice(0, h), slice(h, M)):
+        lpb.render_backward(field, t["o"][sl].contiguous(), t["d"][sl].contiguous(), t["near"][sl].contiguous(),
+                            t["far"][sl].contiguous(), c.S, tau[sl].contiguous(), t["go"][sl].contiguous(),
+                            t["gt"][sl].contiguous(), t["bg"], grad_planes=gp, grad_params=gq)
+    g2 = lpb.render_backward(field, t["o"], t["d"], t["near"], t["far"], c.S, tau, 2 * t["go"], 2 * t["gt"],
+                             t["bg"])
+    torch.cuda.synchronize()
+    for a, b, d in zip(g_all[0], gp, g2[0]):
+        assert rel_inf(b.cpu().numpy(), a.cpu().numpy()) < 1e-4
+        assert rel_inf(d.cpu().numpy(), 2 * a.cpu().numpy()) < 1e-4
+    assert rel_inf(gq.cpu().numpy(), g_all[1].cpu().numpy()) < 1e-4
+    assert rel_inf(g2[1].cpu().numpy(), 2 * g_all[1].cpu().numpy()) < 1e-4
+
+
+def test_memory_is_o1_per_ray(torch_cuda):
+    """the fused path stores no per-sample state: peak device memory of a
+    forward+backward does not depend on S, and the library allocates nothing."""
+    import paper_2404_19760_b200 as lpb
+    torch = torch_cuda
+    peaks = []
+    for S in (32, 128, 512):
+        pb = problem_np("c4", idx=np.arange(65536, dtype=np.int64))
+        pb["cfg"] = wl.get_config("c4", S=S)
+        field, t = to_cuda(pb)
+        gpl = [torch.zeros_like(p) for p in field.planes]
+        gpa = torch.zeros_like(field.params)
+        out = torch.empty((65536, 3), device="cuda")
+        tau = torch.empty((65536,), device="cuda")
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats()
+        base = torch.cuda.memory_allocated()
+        free0 = torch.cuda.mem_get_info()[0]
+        lpb.render_forward(field, t["o"], t["d"], t["near"], t["far"], S, t["bg"], out=out, tau=tau)
+        lpb.render_backward(field, t["o"], t["d"], t["near"], t["far"], S, tau, t["go"], t["gt"], t["bg"],
+                            grad_planes=gpl, grad_params=gpa)
+        torch.cuda.synchronize()
+        peaks.append(torch.cuda.max_memory_allocated() - base)
+        assert torch.cuda.mem_get_info()[0] == free0
+        del field, t, gpl, gpa, out, tau
+    assert peaks[0] == peaks[1] == peaks[2] == 0
+
+
+def test_autograd_render(torch_cuda):
+    """The autograd Function routes to the same kernels (c1 shapes)."""
+    import paper_2404_19760_b200 as lpb
+    torch = torch_cuda
+    pb = unambiguous(problem_np("c1", n=4096))
+    field, t = to_cuda(pb)
+    field.params.requires_grad_(True)
+    for p in field.planes:
+        p.requires_grad_(True)
+    out, tau = lpb.render(field, t["o"], t["d"], t["near"], t["far"], pb["cfg"].S, t["bg"])
+    loss = (out * t["go"]).sum() + (tau * t["gt"]).sum()
+    loss.backward()
+    r = _oracle_fwd_bwd(pb)
+    assert rel_inf(out.detach().cpu().numpy(), r["out"]) < TOL_IMG
+    assert rel_inf(field.params.grad.cpu().numpy(), r["gparams"]) < TOL_GRAD
+    for p, g in zip(field.planes, r["gplanes"]):
+        assert rel_inf(p.grad.cpu().numpy(), g) < TOL_GRAD
