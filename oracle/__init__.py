@@ -61,7 +61,9 @@ def lib():
                                     P, P, P, P, P]
             L.lpo_render_min_preact.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
                                                 P, P, P, P, i32, P]
-            for f in (L.lpo_render_min_preact, L.lpo_sample, L.lpo_splat, L.lpo_mlp_forward, L.lpo_mlp_backward,
+            L.lpo_render_relu_slack.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
+                                                P, P, P, P, i32, P, P, P, f64, P, P, P, P]
+            for f in (L.lpo_render_relu_slack, L.lpo_render_min_preact, L.lpo_sample, L.lpo_splat, L.lpo_mlp_forward, L.lpo_mlp_backward,
                       L.lpo_render_forward, L.lpo_render_backward, L.lpo_trace):
                 f.restype = ctypes.c_int
             _lib = L
@@ -197,6 +199,41 @@ def min_preact(field: Field, rays: Rays) -> np.ndarray:
                                      _p(rays.far), rays.S, _p(out))
     assert rc == 0
     return out
+
+
+def relu_slack(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, band: float = 2e-5,
+               r0: int = 0, r1: Optional[int] = None, out=None):
+    """Elementwise bound of how much the gradients may change when any ReLU
+    decision with |z| < band * scale is taken the other way (lp_oracle.cpp
+    mlp_slack). Returns (slack_grid list, slack_params)."""
+    r1 = rays.n if r1 is None else r1
+    go = _d(grad_out).reshape(rays.n, field.C)
+    gt = None if grad_tau is None else _d(grad_tau).reshape(rays.n)
+    bgd = None if bg is None else _d(bg)
+    if out is None:
+        out = ([np.zeros_like(a) for a in field.grid], np.zeros_like(field.params))
+    sg, sp = out
+    ptrs = [_p(a) for a in sg] + [None] * (3 - len(sg))
+    rc = lib().lpo_render_relu_slack(*field._geom(), *field._planes(), field.n_layers, _p(field.widths),
+                                     _p(field.params), r0, r1, _p(rays.o), _p(rays.d), _p(rays.near),
+                                     _p(rays.far), rays.S, _p(bgd), _p(go), _p(gt), float(band), *ptrs, _p(sp))
+    assert rc == 0
+    return sg, sp
+
+
+def relu_slack_threaded(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, band: float = 2e-5,
+                        threads: int = 1):
+    bounds = np.linspace(0, rays.n, threads + 1).astype(np.int64)
+    parts = [([np.zeros_like(a) for a in field.grid], np.zeros_like(field.params)) for _ in range(threads)]
+    ts = [threading.Thread(target=relu_slack, kwargs=dict(field=field, rays=rays, grad_out=grad_out,
+                                                          grad_tau=grad_tau, bg=bg, band=band, r0=int(bounds[i]),
+                                                          r1=int(bounds[i + 1]), out=parts[i]))
+          for i in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return [sum(p[0][k] for p in parts) for k in range(len(field.grid))], sum(p[1] for p in parts)
 
 
 def trace(field: Field, origin, direction, near: float, far: float, S: int):

@@ -224,6 +224,9 @@ void finish_forward(const Field& F, const RayTrace& rt, const double* bg, double
   *tau_out = rt.tau[R];
 }
 
+void mlp_slack(const Field& F, const MlpTrace& tr, const double* dout, double band, double* slack_params,
+               double* dh_slack);
+
 // O5 / O7: backward for one ray. Loss convention L = p.out + g_tau * tau_R.
 // mode 0: Eq. 3 via suffix sums over the stored w_j a_j:
 //   dL/dsigma_q = -Delta (G_q - [q>=1] T_q a_q) + Delta g_tau,
@@ -233,7 +236,8 @@ void finish_forward(const Field& F, const RayTrace& rt, const double* bg, double
 //   dout/dsigma_q = sum_{j>=1} (dT_{j-1}/dsigma_q - dT_j/dsigma_q) c_j + dT_R/dsigma_q bg,
 //   dT_j/dsigma_q = -Delta T_j [q <= j], T_{-1} = 1 (constant).
 void backward_ray(const Field& F, const RayTrace& rt, const double* bg, const double* p, double gtau, int mode,
-                  double* const* grad_planes, double* grad_params) {
+                  double* const* grad_planes, double* grad_params, double band = 0.0,
+                  double* const* slack_planes = nullptr, double* slack_params = nullptr) {
   const int C = F.widths[F.n_layers] - 1;
   const int S = rt.S, R = S - 1;
   const double Dl = rt.delta;
@@ -274,6 +278,74 @@ void backward_ray(const Field& F, const RayTrace& rt, const double* bg, const do
     }
     mlp_backward(F, rt.mlp[q], dout.data(), grad_params, dh.data());
     scatter(F, rt.taps[q], dh.data(), grad_planes);
+    if (slack_params) {
+      std::vector<double> ds(F.K);
+      mlp_slack(F, rt.mlp[q], dout.data(), band, slack_params, ds.data());
+      scatter(F, rt.taps[q], ds.data(), slack_planes);
+    }
+  }
+}
+
+// Slack bound for ambiguous ReLU decisions (test infrastructure for the parity
+// metric). For every sample and hidden unit whose
+// pre-activation is within band * scale of 0 (scale = sum_k |W_ik a_k| + |b_i|),
+// ReLU'(z) may legitimately be evaluated either way by a finite-precision
+// implementation. Flipping that one decision changes the unit's delta by
+// |s_i| (s = W_{l+1}^T delta_{l+1}, before the mask) and, through the lower
+// layers, the parameter and grid gradients. This accumulates an elementwise
+// upper bound of |change| (absolute values at every step, masks ignored
+// below the flipped unit) into slack buffers with the gradients' shapes.
+void mlp_slack(const Field& F, const MlpTrace& tr, const double* dout, double band, double* slack_params,
+               double* dh_slack) {
+  const int L = F.n_layers;
+  std::vector<int64_t> off(L);
+  int64_t o = 0;
+  for (int l = 0; l < L; ++l) {
+    off[l] = o;
+    o += (int64_t)F.widths[l + 1] * F.widths[l] + F.widths[l + 1];
+  }
+  for (int k = 0; k < F.widths[0]; ++k) dh_slack[k] = 0.0;
+  // pre-mask upstream s_l for every hidden layer l (the delta of z[l] before ReLU')
+  std::vector<std::vector<double>> pre(L);
+  std::vector<double> delta(dout, dout + F.widths[L]);
+  for (int l = L - 1; l >= 1; --l) {
+    int fin = F.widths[l], fout = F.widths[l + 1];
+    const double* Wl = F.params + off[l];
+    std::vector<double> s(fin, 0.0);
+    for (int k = 0; k < fin; ++k)
+      for (int i = 0; i < fout; ++i) s[k] += Wl[(int64_t)i * fin + k] * delta[i];
+    pre[l - 1] = s;
+    for (int k = 0; k < fin; ++k) s[k] = tr.z[l - 1][k] > 0.0 ? s[k] : 0.0;
+    delta.swap(s);
+  }
+  for (int h = 0; h < L - 1; ++h) {
+    const int fin = F.widths[h], fout = F.widths[h + 1];
+    const double* Wh = F.params + off[h];
+    const double* bh = Wh + (int64_t)fout * fin;
+    for (int i = 0; i < fout; ++i) {
+      double sc = std::fabs(bh[i]);
+      for (int k = 0; k < fin; ++k) sc += std::fabs(Wh[(int64_t)i * fin + k] * tr.a[h][k]);
+      if (!(std::fabs(tr.z[h][i]) < band * sc)) continue;
+      std::vector<double> v(fout, 0.0);
+      v[i] = std::fabs(pre[h][i]);
+      for (int l = h; l >= 0; --l) {
+        const int li = F.widths[l], lo = F.widths[l + 1];
+        const double* Wl = F.params + off[l];
+        double* sW = slack_params + off[l];
+        double* sb = sW + (int64_t)lo * li;
+        for (int r = 0; r < lo; ++r) {
+          if (v[r] == 0.0) continue;
+          sb[r] += v[r];
+          for (int k = 0; k < li; ++k) sW[(int64_t)r * li + k] += v[r] * std::fabs(tr.a[l][k]);
+        }
+        std::vector<double> nv(li, 0.0);
+        for (int k = 0; k < li; ++k)
+          for (int r = 0; r < lo; ++r) nv[k] += std::fabs(Wl[(int64_t)r * li + k]) * v[r];
+        if (l == 0)
+          for (int k = 0; k < li; ++k) dh_slack[k] += nv[k];
+        v.swap(nv);
+      }
+    }
   }
 }
 
@@ -393,6 +465,37 @@ int lpo_render_backward(int kind, int H, int W, int D, int K, const double* p0, 
   for (int64_t r = r0; r < r1; ++r) {
     trace_ray(F, origins + 3 * r, dirs + 3 * r, nearv[r], farv[r], S, rt);
     backward_ray(F, rt, bg, grad_out + r * C, grad_tau ? grad_tau[r] : 0.0, mode, g, grad_params);
+  }
+  return 0;
+}
+
+// Slack bound (see mlp_slack) of rays [r0, r1) accumulated into slack_* with the
+// gradient shapes; band = relative |z| below which a ReLU decision is ambiguous.
+int lpo_render_relu_slack(int kind, int H, int W, int D, int K, const double* p0, const double* p1,
+                          const double* p2, int n_layers, const int* widths, const double* params, int64_t r0,
+                          int64_t r1, const double* origins, const double* dirs, const double* nearv,
+                          const double* farv, int S, const double* bg, const double* grad_out,
+                          const double* grad_tau, double band, double* s0, double* s1, double* s2,
+                          double* slack_params) {
+  if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params);
+  const int C = widths[n_layers] - 1;
+  double* sg[3] = {s0, s1, s2};
+  int64_t np = 0;
+  for (int l = 0; l < n_layers; ++l) np += (int64_t)widths[l + 1] * widths[l] + widths[l + 1];
+  std::vector<double> gp(np, 0.0);
+  std::vector<std::vector<double>> gg(3);
+  double* gptr[3] = {nullptr, nullptr, nullptr};
+  const int64_t nel[3] = {(int64_t)H * W * (kind == 1 ? D : 1) * K, (int64_t)W * D * K, (int64_t)D * H * K};
+  for (int i = 0; i < (kind == 1 ? 1 : 3); ++i) {
+    gg[i].assign(nel[i], 0.0);
+    gptr[i] = gg[i].data();
+  }
+  RayTrace rt;
+  for (int64_t r = r0; r < r1; ++r) {
+    trace_ray(F, origins + 3 * r, dirs + 3 * r, nearv[r], farv[r], S, rt);
+    backward_ray(F, rt, bg, grad_out + r * C, grad_tau ? grad_tau[r] : 0.0, 0, gptr, gp.data(), band, sg,
+                 slack_params);
   }
   return 0;
 }

@@ -54,3 +54,14 @@ def tiny_rays(n=6, S_list=(2, 3, 5, 8, 11, 12), seed=21, inside_start=False):
         near = np.full(n, 0.2)
         far = np.full(n, 3.4)
     return o.astype(np.float32), d.astype(np.float32), near.astype(np.float32), far.astype(np.float32)
+
+
+def rel_inf_slack(a, b, slack):
+    """Parity error with an elementwise allowance for ambiguous ReLU decisions:
+    max(|a - b| - slack, 0) / ||b||_inf (DESIGN.md "Parity metric")."""
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    s = np.asarray(slack, dtype=np.float64).ravel()
+    den = np.max(np.abs(b))
+    num = np.max(np.maximum(np.abs(a - b) - s, 0.0))
+    return float(num / den) if den > 0 else float(num)

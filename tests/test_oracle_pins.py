@@ -414,3 +414,41 @@ def test_paper_memory_accounting_golden():
     assert a["M"] * a["R"] * a["L"] * a["K"] * 4 == a["bytes"] == 12 * 2 ** 30
     b = g["pull_grid_P174"]
     assert b["N"] ** 3 * b["K"] * 4 == b["bytes"] == 512 * 2 ** 20
+
+
+# ---------------------------------------------------------------- parity-metric helper
+@pytest.mark.parametrize("widths", [(3, 5, 4), (3, 6, 5, 4)])
+def test_relu_slack_bounds_a_flipped_decision(widths):
+    """The ReLU-ambiguity slack (test infrastructure for the parity metric) bounds
+    the gradient jump when one hidden pre-activation crosses 0: put unit 0 of the
+    first layer exactly at z = 0 on one sample, evaluate the oracle gradient with
+    the bias nudged to either side (the decision flips, the forward does not
+    move), and check |g+ - g-| <= slack elementwise; slack is 0 for band 0."""
+    F = _field(wl.TRIPLANE, widths=widths, sigma_bias=0.4)
+    o, d, near, far = tiny_rays(2, inside_start=True)
+    S = 7
+    rays = oracle.Rays(o[:1], d[:1], near[:1], far[:1], S)
+    p = np.array([[0.7, -0.4, 0.9]])
+    gt = np.array([0.3])
+    bg = np.array([0.1, 0.2, 0.3])
+    K, H1 = widths[0], widths[1]
+    Dl = (float(far[0]) - float(near[0])) / (S - 1)
+    x = o[0].astype(np.float64) + (float(near[0]) + 3 * Dl) * d[0].astype(np.float64)
+    h = oracle.sample(F, x[None])[0]
+    W0 = F.params[:H1 * K].reshape(H1, K)
+    b0 = F.params[H1 * K:H1 * K + H1]
+    F.params[H1 * K] -= float(W0[0] @ h + b0[0])       # z_0 = 0 at sample 3
+    base = F.params[H1 * K]
+    res = []
+    for eps in (+1e-12, -1e-12):
+        F.params[H1 * K] = base + eps
+        res.append(oracle.render_backward(F, rays, p, gt, bg))
+    F.params[H1 * K] = base
+    sg, sp = oracle.relu_slack(F, rays, p, gt, bg, band=1e-9)
+    z0, _ = oracle.relu_slack(F, rays, p, gt, bg, band=0.0)
+    jump_p = np.abs(res[0][1] - res[1][1])
+    assert jump_p.max() > 1e-6, "the flip must change the gradient"
+    assert np.all(jump_p <= sp + 1e-9)
+    for a, b, s in zip(res[0][0], res[1][0], sg):
+        assert np.all(np.abs(a - b) <= s + 1e-9)
+    assert all(np.all(z == 0) for z in z0)
