@@ -1,9 +1,11 @@
 // lp_launch.cuh -- persistent launch of one kernel instance (included only by
 // the generated per-instance translation units under csrc/inst/).
 #pragma once
+#include <cstdlib>
 #include <mutex>
 
 #include "lp_internal.h"
+#include "lp_tc_kernels.cuh"
 
 namespace lpi {
 
@@ -14,9 +16,10 @@ struct LaunchShape {
   cudaError_t err = cudaSuccess;
 };
 
+// Launch a persistent kernel whose CTAs each march `groups` tiles of 128 rays at a time.
 template <typename KernelT>
-lp_status launch(KernelT kernel, LaunchShape& shape, size_t smem, int64_t M, const lp::KernelArgs& args,
-                 const L2Window& win, cudaStream_t stream) {
+lp_status launch(KernelT kernel, LaunchShape& shape, size_t smem, int threads, int groups, int64_t M,
+                 const lp::KernelArgs& args, const L2Window& win, cudaStream_t stream) {
   std::call_once(shape.once, [&] {
     int dev = 0, sms = 0, occ = 0;
     shape.err = cudaGetDevice(&dev);
@@ -24,18 +27,19 @@ lp_status launch(KernelT kernel, LaunchShape& shape, size_t smem, int64_t M, con
     if (shape.err == cudaSuccess)
       shape.err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (shape.err == cudaSuccess)
-      shape.err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, lp::kThreads, smem);
+      shape.err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
     if (shape.err == cudaSuccess && occ < 1) shape.err = cudaErrorInvalidConfiguration;
     shape.ctas = sms * occ;
   });
   if (shape.err != cudaSuccess) return cuda_check(shape.err, "kernel setup");
   if (M == 0) return LP_OK;
-  const int64_t tiles = (M + lp::kThreads - 1) / lp::kThreads;
-  const int grid = (int)(tiles < shape.ctas ? tiles : shape.ctas);
+  const int64_t tiles = (M + 127) / 128;
+  const int64_t need = (tiles + groups - 1) / groups;
+  const int grid = (int)(need < shape.ctas ? need : shape.ctas);
 
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(lp::kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -56,15 +60,45 @@ lp_status launch(KernelT kernel, LaunchShape& shape, size_t smem, int64_t M, con
   return cuda_check(cudaGetLastError(), "kernel launch");
 }
 
+// Kernel variant: tensor-core kernels (K1tc/K2tc) for one-hidden-layer MLPs,
+// FFMA kernels (K1/K2) for two hidden layers. LP_KERNELS=fma forces the FFMA
+// kernels (A/B measurements only).
+inline bool force_fma() {
+  static const bool f = [] {
+    const char* e = getenv("LP_KERNELS");
+    return e && e[0] == 'f';
+  }();
+  return f;
+}
+
+constexpr int kFwdGroups = 2;
+constexpr int kBwdGroups = 2;
+
 template <int KIND, int K, int HID, int NH>
 lp_status run_fwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
+  if constexpr (NH == 1) {
+    if (!force_fma()) {
+      static LaunchShape shape;
+      constexpr int G = kFwdGroups;
+      return launch(lp::lp_fwd_tc_kernel<KIND, K, HID, G>, shape, lp::FwdTcSmem<KIND, K, HID, G>::BYTES, 128 * G, G,
+                    a.M, a, w, s);
+    }
+  }
   static LaunchShape shape;
-  return launch(lp::lp_fwd_kernel<KIND, K, HID, NH>, shape, lp::fwd_smem_bytes<K, HID, NH>(), a.M, a, w, s);
+  return launch(lp::lp_fwd_kernel<KIND, K, HID, NH>, shape, lp::fwd_smem_bytes<K, HID, NH>(), 128, 1, a.M, a, w, s);
 }
 template <int KIND, int K, int HID, int NH>
 lp_status run_bwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
+  if constexpr (NH == 1) {
+    if (!force_fma()) {
+      static LaunchShape shape;
+      constexpr int G = kBwdGroups;
+      return launch(lp::lp_bwd_tc_kernel<KIND, K, HID, G>, shape, lp::BwdTcSmem<KIND, K, HID, G>::BYTES, 128 * G, G,
+                    a.M, a, w, s);
+    }
+  }
   static LaunchShape shape;
-  return launch(lp::lp_bwd_kernel<KIND, K, HID, NH>, shape, lp::bwd_smem_bytes<K, HID, NH>(), a.M, a, w, s);
+  return launch(lp::lp_bwd_kernel<KIND, K, HID, NH>, shape, lp::bwd_smem_bytes<K, HID, NH>(), 128, 1, a.M, a, w, s);
 }
 
 }  // namespace lpi

@@ -1,0 +1,588 @@
+// lp_tc_kernels.cuh -- tensor-core (tcgen05) versions of the fused ray march for
+// one-hidden-layer MLPs: K1tc (forward, Eq. 1) and K2tc (backward, Eq. 3).
+//
+// Work decomposition. A CTA holds G independent "groups" of 128 threads; a group
+// owns a tile of 128 rays (one ray per thread for the per-ray EA state) and
+// marches it step by step (j = 0..R forward, q = R..0 backward).
+// Per step:
+//   taps     each thread turns its ray's point x_j (fp64) into compact
+//            per-plane cell records (shared memory);
+//   gather   the warp cooperatively reads the corner vectors of its 32 rays:
+//            lane = (ray, 4-channel chunk), so one 16-byte load instruction
+//            fetches whole 128-byte corner lines of 32/(K/4) rays, and the
+//            lane accumulates its chunk over all corners of its ray
+//            (h = sum_c w_c theta_c);
+//            h is written as bf16 pieces into the A tile (sample-major);
+//   MMA      one elected thread issues tcgen05.mma: Z = H W0^T into TMEM
+//            (M = 128 samples, N = hidden, fp32 accumulate);
+//   epilogue each thread loads its sample's row of Z from TMEM and runs bias,
+//            ReLU, the 4-wide output layer, heads and the EA update.
+// Backward additionally stages delta1, a1 and dL/do as bf16 pieces and issues
+//   dH  = D1 W0            (M = 128, N = K, K = hidden)   -> grid gradient,
+//   dW0 += D1^T H          (M = 64,  N = K, K = 128 samples) -- stays in TMEM,
+//   dWo += A1^T DOUT       (M = 64,  N = 8, K = 128 samples) -- stays in TMEM,
+// and scatters dH cooperatively with 16-byte vector reductions (one full
+// 128-byte line per instruction group), the transpose of the gather.
+// The weight-gradient accumulators live in TMEM for the CTA's lifetime and are
+// flushed once (B7); bias gradients accumulate per thread in registers.
+#pragma once
+
+#include "lp_kernels.cuh"
+#include "lp_tc.cuh"
+
+namespace lp {
+
+template <int KIND, int K, int HID>
+struct TcShape {
+  static constexpr int KP = K < 16 ? 16 : K;     // H tile columns / MMA K for Z, N for dH
+  static constexpr int HP = HID < 64 ? 64 : HID; // D1 / A1 tile columns (M = 64 of dW MMAs)
+  static constexpr int KC = K / 4;               // 16-byte chunks per corner vector
+  static constexpr int RPI = 32 / KC;            // rays per cooperative iteration
+  static constexpr int NPL = KIND == 0 ? 3 : 1;  // tap records per ray
+  static constexpr int TILE = 128;
+  // bytes
+  static constexpr uint32_t W0_PIECE = HID * KP * 2;
+  static constexpr uint32_t H_PIECE = TILE * KP * 2;
+  static constexpr uint32_t D_PIECE = TILE * HP * 2;
+  static constexpr uint32_t DO_PIECE = TILE * 8 * 2;
+  static constexpr uint32_t TAPS = TILE * NPL * 16;
+  static_assert(HID % 16 == 0 && HID <= 64, "hidden width");
+  static_assert(K % 4 == 0 && K <= 32, "channels");
+};
+
+// ---------------------------------------------------------------- taps (F2, F3)
+// Compact per-plane record of a sample: (element offset of corner (0,0[,0]),
+// f_a, f_b[, f_c]) as float4; offset -1 marks a point outside the cube (R11).
+template <int KIND, int K>
+__device__ __forceinline__ void write_taps(float4* rec, const double x[3], const GridDims& g) {
+  const bool inside = fabs(x[0]) <= 1.0 && fabs(x[1]) <= 1.0 && fabs(x[2]) <= 1.0;
+  int ix, iy, iz;
+  float fx, fy, fz;
+  axis_cell(x[0], g.H, ix, fx);
+  axis_cell(x[1], g.W, iy, fy);
+  axis_cell(x[2], g.D, iz, fz);
+  if constexpr (KIND == 1) {
+    const int base = inside ? (((ix * g.W + iy) * g.D + iz) * K) : -1;
+    rec[0] = make_float4(__int_as_float(base), fx, fy, fz);
+  } else {
+    rec[0] = make_float4(__int_as_float(inside ? (ix * g.W + iy) * K : -1), fx, fy, 0.0f);
+    rec[1] = make_float4(__int_as_float(inside ? (iy * g.D + iz) * K : -1), fy, fz, 0.0f);
+    rec[2] = make_float4(__int_as_float(inside ? (iz * g.H + ix) * K : -1), fz, fx, 0.0f);
+  }
+}
+
+// Corner set of one record: up to 8 (element offset, weight) pairs.
+template <int KIND, int K>
+struct Corners {
+  static constexpr int N = KIND == 1 ? 8 : 4;
+  int off[N];
+  float w[N];
+};
+
+template <int KIND, int K>
+__device__ __forceinline__ void record_corners(const float4 rec, int p, const GridDims& g, Corners<KIND, K>& c) {
+  int base = __float_as_int(rec.x);
+  const float m = base >= 0 ? 1.0f : 0.0f;
+  base = base >= 0 ? base : 0;
+  if constexpr (KIND == 1) {
+    const int sy = g.D * K, sx = g.W * g.D * K;
+    const float ax[2] = {1.0f - rec.y, rec.y}, ay[2] = {1.0f - rec.z, rec.z}, az[2] = {1.0f - rec.w, rec.w};
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const int dx = (cc >> 2) & 1, dy = (cc >> 1) & 1, dz = cc & 1;
+      c.off[cc] = base + dx * sx + dy * sy + dz * K;
+      c.w[cc] = ax[dx] * ay[dy] * az[dz] * m;
+    }
+  } else {
+    const int sa = (p == 0 ? g.W : p == 1 ? g.D : g.H) * K;
+    const float fa = rec.y, fb = rec.z;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      const int a = (cc >> 1) & 1, b = cc & 1;
+      c.off[cc] = base + a * sa + b * K;
+      c.w[cc] = (a ? fa : 1.0f - fa) * (b ? fb : 1.0f - fb) * m;
+    }
+  }
+}
+
+// Warp-cooperative gather of the warp's 32 rays: lane = (ray RPI-subgroup, chunk).
+// Writes h into rows [row0, row0 + 32) of the H tile (NP bf16 pieces).
+template <int KIND, int K, int KP, int NP>
+__device__ __forceinline__ void coop_gather(const float* const* planes, const float4* taps, const GridDims& g,
+                                            uint8_t* Htile, uint32_t piece_stride, int row0, int lane) {
+  constexpr int KC = K / 4, RPI = 32 / KC, NPL = KIND == 0 ? 3 : 1;
+  const int ch = lane % KC, sub = lane / KC;
+#pragma unroll 1
+  for (int it = 0; it < KC; ++it) {
+    const int row = row0 + it * RPI + sub;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int p = 0; p < NPL; ++p) {
+      const float4 rec = taps[row * NPL + p];
+      Corners<KIND, K> c;
+      record_corners<KIND, K>(rec, p, g, c);
+      const float* pl = planes[p] + 4 * ch;
+      float4 v[Corners<KIND, K>::N];
+#pragma unroll
+      for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) v[cc] = __ldg(reinterpret_cast<const float4*>(pl + c.off[cc]));
+#pragma unroll
+      for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) {
+        acc[0] = fmaf(c.w[cc], v[cc].x, acc[0]);
+        acc[1] = fmaf(c.w[cc], v[cc].y, acc[1]);
+        acc[2] = fmaf(c.w[cc], v[cc].z, acc[2]);
+        acc[3] = fmaf(c.w[cc], v[cc].w, acc[3]);
+      }
+    }
+    tc::store4<NP>(Htile, piece_stride, row, 4 * ch, KP, acc);
+  }
+}
+
+// Warp-cooperative scatter (B6): grad_theta[c] += w_c dh for the warp's 32 rays;
+// dh rows are fp32 in `dhs` ([128][K + 4]).
+template <int KIND, int K>
+__device__ __forceinline__ void coop_scatter(float* const* gplanes, const float4* taps, const GridDims& g,
+                                             const float* dhs, int row0, int lane) {
+  constexpr int KC = K / 4, RPI = 32 / KC, NPL = KIND == 0 ? 3 : 1;
+  const int ch = lane % KC, sub = lane / KC;
+#pragma unroll 1
+  for (int it = 0; it < KC; ++it) {
+    const int row = row0 + it * RPI + sub;
+    const float4 d = *reinterpret_cast<const float4*>(dhs + row * (K + 4) + 4 * ch);
+#pragma unroll
+    for (int p = 0; p < NPL; ++p) {
+      const float4 rec = taps[row * NPL + p];
+      if (__float_as_int(rec.x) < 0) continue;
+      Corners<KIND, K> c;
+      record_corners<KIND, K>(rec, p, g, c);
+      float* pl = gplanes[p] + 4 * ch;
+#pragma unroll
+      for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) {
+        const float w = c.w[cc];
+        atomicAdd(reinterpret_cast<float4*>(pl + c.off[cc]), make_float4(w * d.x, w * d.y, w * d.z, w * d.w));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- shared staging of the weights
+template <int K, int HID>
+struct TcParams {  // fp32 copies used on CUDA cores
+  static constexpr int B0 = 0;               // [HID]
+  static constexpr int WOT = HID;            // [HID][4]
+  static constexpr int BO = HID + 4 * HID;   // [4]
+  static constexpr int N = round4(BO + 4);
+};
+
+template <int K, int HID, int KP>
+__device__ __forceinline__ void stage_tc_weights(uint8_t* w0p, float* fp, const float* __restrict__ g) {
+  using P = PackedParams<K, HID, 1>;
+  using F = TcParams<K, HID>;
+  // W0 [HID][KP] as 3 bf16 pieces (columns >= K stay zero)
+  for (int i = threadIdx.x; i < HID * K; i += blockDim.x) {
+    const int r = i / K, c = i % K;
+    float v = g[P::W0 + i];
+#pragma unroll
+    for (int pc = 0; pc < 3; ++pc) {
+      __nv_bfloat16 b = __float2bfloat16_rn(v);
+      *reinterpret_cast<__nv_bfloat16*>(w0p + pc * (HID * KP * 2) + tc::cm_off(r, c, KP)) = b;
+      v -= __bfloat162float(b);
+    }
+  }
+  for (int i = threadIdx.x; i < HID; i += blockDim.x) fp[F::B0 + i] = g[P::B0 + i];
+  for (int i = threadIdx.x; i < 4 * HID; i += blockDim.x) {
+    const int r = i / HID, c = i % HID;
+    fp[F::WOT + c * 4 + r] = g[P::WO + i];
+  }
+  if (threadIdx.x < 4) fp[F::BO + threadIdx.x] = g[P::BO + threadIdx.x];
+}
+
+// o = bo + Wo relu(z + b0); also returns a = relu(z + b0)
+template <int HID>
+__device__ __forceinline__ void tc_head_layer(const float* fp_b0, const float* fp_wot, const float* fp_bo,
+                                              float (&z)[HID], float (&o)[kOut]) {
+  lds<kOut>(fp_bo, o);
+#pragma unroll
+  for (int i = 0; i < HID; ++i) {
+    z[i] = fmaxf(z[i] + fp_b0[i], 0.0f);
+    const float4 w = reinterpret_cast<const float4*>(fp_wot)[i];
+    o[0] = fmaf(w.x, z[i], o[0]);
+    o[1] = fmaf(w.y, z[i], o[1]);
+    o[2] = fmaf(w.z, z[i], o[2]);
+    o[3] = fmaf(w.w, z[i], o[3]);
+  }
+}
+
+// ================================================================= K1tc forward
+template <int KIND, int K, int HID, int G>
+struct FwdTcSmem {
+  using S = TcShape<KIND, K, HID>;
+  static constexpr uint32_t W0P = 0;                                   // 3 pieces
+  static constexpr uint32_t FP = W0P + 3 * S::W0_PIECE;                // fp32 params
+  static constexpr uint32_t GRP = (FP + TcParams<K, HID>::N * 4 + 127) & ~127u;
+  static constexpr uint32_t H = 0;                                     // per group: H (3 pieces), taps
+  static constexpr uint32_t TAPS = H + 3 * S::H_PIECE;
+  static constexpr uint32_t GSIZE = (TAPS + S::TAPS + 127) & ~127u;
+  static constexpr uint32_t BAR = GRP + G * GSIZE;                     // G mbarriers + tmem slot
+  static constexpr uint32_t BYTES = BAR + 8 * G + 16;
+  static constexpr uint32_t TMEM_COLS = G * 64 <= 32 ? 32 : G * 64 <= 64 ? 64 : G * 64 <= 128 ? 128 : 256;
+};
+
+template <int KIND, int K, int HID, int G>
+__global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs a) {
+  using S = TcShape<KIND, K, HID>;
+  using L = FwdTcSmem<KIND, K, HID, G>;
+  using F = TcParams<K, HID>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* w0p = smem + L::W0P;
+  float* fp = reinterpret_cast<float*>(smem + L::FP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 8 * G);
+
+  const int g = threadIdx.x >> 7, gt = threadIdx.x & 127, wg = gt >> 5, lane = gt & 31;
+  uint8_t* gsm = smem + L::GRP + g * L::GSIZE;
+  uint8_t* Ht = gsm + L::H;
+  float4* taps = reinterpret_cast<float4*>(gsm + L::TAPS);
+
+  for (uint32_t i = threadIdx.x * 16; i < L::BAR; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  stage_tc_weights<K, HID, S::KP>(w0p, fp, a.params);
+  if (threadIdx.x < G) tc::mbar_init(&bars[threadIdx.x], 1);
+  if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
+  tc::fence_async_smem();
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tslot + (uint32_t)(g * 64);
+  const uint32_t tlane = (uint32_t)(wg * 32) << 16;
+
+  const int R = a.S - 1;
+  const float* planes[3] = {a.grid[0], a.grid[1], a.grid[2]};
+  float bg[kC];
+#pragma unroll
+  for (int c = 0; c < kC; ++c) bg[c] = a.bg ? __ldg(a.bg + c) : 0.0f;
+  const uint32_t idesc = tc::idesc_bf16(128, HID, 0, 0);
+  const uint32_t h_addr = tc::smem_u32(Ht), w_addr = tc::smem_u32(w0p);
+  uint32_t phase = 0;
+
+  const int64_t ntiles = (a.M + 127) / 128;
+  for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
+    const int64_t r0 = tile * 128 + gt;
+    const bool valid = r0 < a.M;
+    const int64_t r = valid ? r0 : a.M - 1;
+    const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
+    float tau = 0.0f, tau_e = 0.0f;
+    float v[kC] = {0.0f, 0.0f, 0.0f};
+    for (int j = 0; j <= R; ++j) {
+      double x[3];
+      ray_point(ray, j, x);                                        // F2
+      write_taps<KIND, K>(taps + gt * S::NPL, x, a.dims);          // F3 (cells)
+      __syncwarp();
+      coop_gather<KIND, K, S::KP, 3>(planes, taps, a.dims, Ht, S::H_PIECE, wg * 32, lane);  // F3 (gather)
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      tc::named_bar(1 + g, 128);
+      if (gt == 0) {                                               // F4: Z = H W0^T on the tensor core
+        tc::fence_after_sync();
+        constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
+        uint32_t acc = 0;
+#pragma unroll
+        for (int ks = 0; ks < S::KP / 16; ++ks)
+#pragma unroll
+          for (int c = 0; c < 6; ++c) {
+            tc::mma_bf16(tmem, tc::desc_kmajor(h_addr + PA[c] * S::H_PIECE, S::KP, ks),
+                         tc::desc_kmajor(w_addr + PB[c] * S::W0_PIECE, S::KP, ks), idesc, acc);
+            acc = 1;
+          }
+        tc::mma_commit(&bars[g]);
+      }
+      tc::mbar_wait(&bars[g], phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+      float z[HID];
+      tc::tmem_ld<HID>(tmem + tlane, z);
+      tc::fence_before_sync();
+      float o[kOut];
+      tc_head_layer<HID>(fp + F::B0, fp + F::WOT, fp + F::BO, z, o);
+      const float ds = (float)ray.delta * softplus_f(o[0]);       // F5
+      if (j > 0) {                                                 // F6
+        const float w = expf(-(tau + tau_e)) * (-expm1f(-ds));
+#pragma unroll
+        for (int c = 0; c < kC; ++c) v[c] = fmaf(w, sigmoid_f(o[1 + c]), v[c]);
+      }
+      two_sum_add(tau, tau_e, ds);
+    }
+    if (valid) {                                                   // F7
+      const float tauR = tau + tau_e;
+      const float TR = expf(-tauR);
+#pragma unroll
+      for (int c = 0; c < kC; ++c) a.out[3 * r + c] = fmaf(TR, bg[c], v[c]);
+      a.tau[r] = tauR;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(*tslot, L::TMEM_COLS);
+  }
+}
+
+// ================================================================= K2tc backward
+template <int KIND, int K, int HID, int G>
+struct BwdTcSmem {
+  using S = TcShape<KIND, K, HID>;
+  static constexpr uint32_t W0P = 0;
+  static constexpr uint32_t FP = W0P + 3 * S::W0_PIECE;
+  static constexpr uint32_t GRP = (FP + TcParams<K, HID>::N * 4 + 127) & ~127u;
+  static constexpr uint32_t H = 0;                             // 3 pieces
+  static constexpr uint32_t D1 = H + 3 * S::H_PIECE;           // 2 pieces (reused as fp32 dH staging)
+  static constexpr uint32_t A1 = D1 + 2 * S::D_PIECE;          // 2 pieces
+  static constexpr uint32_t DO = A1 + 2 * S::D_PIECE;          // 2 pieces
+  static constexpr uint32_t TAPS = DO + 2 * S::DO_PIECE;
+  static constexpr uint32_t GSIZE = (TAPS + S::TAPS + 127) & ~127u;
+  static constexpr uint32_t BAR = GRP + G * GSIZE;             // 2 mbarriers per group + tmem slot
+  static constexpr uint32_t BYTES = BAR + 16 * G + 16;
+  static constexpr uint32_t TMEM_COLS = G == 1 ? 256 : 512;
+  static_assert(2 * S::D_PIECE >= 128 * (K + 4) * 4, "dH staging fits the D1 region");
+};
+
+// TMEM columns of a group (bwd): Z [0,64), dH [64,96), dW0 [96,128), dWo [128,136)
+template <int KIND, int K, int HID, int G>
+__global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs a) {
+  using S = TcShape<KIND, K, HID>;
+  using L = BwdTcSmem<KIND, K, HID, G>;
+  using F = TcParams<K, HID>;
+  using P = PackedParams<K, HID, 1>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* w0p = smem + L::W0P;
+  float* fp = reinterpret_cast<float*>(smem + L::FP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 16 * G);
+
+  const int g = threadIdx.x >> 7, gt = threadIdx.x & 127, wg = gt >> 5, lane = gt & 31;
+  uint8_t* gsm = smem + L::GRP + g * L::GSIZE;
+  uint8_t* Ht = gsm + L::H;
+  uint8_t* D1t = gsm + L::D1;
+  uint8_t* A1t = gsm + L::A1;
+  uint8_t* DOt = gsm + L::DO;
+  float* dhs = reinterpret_cast<float*>(gsm + L::D1);
+  float4* taps = reinterpret_cast<float4*>(gsm + L::TAPS);
+
+  for (uint32_t i = threadIdx.x * 16; i < L::BAR; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  stage_tc_weights<K, HID, S::KP>(w0p, fp, a.params);
+  if (threadIdx.x < 2 * G) tc::mbar_init(&bars[threadIdx.x], 1);
+  if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
+  tc::fence_async_smem();
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *tslot + (uint32_t)(g * 256);
+  const uint32_t tZ = tbase, tDH = tbase + 64, tW0 = tbase + 96, tWo = tbase + 128;
+  const uint32_t tlane = (uint32_t)(wg * 32) << 16;
+  uint64_t* bar_z = &bars[2 * g];
+  uint64_t* bar_d = &bars[2 * g + 1];
+
+  const int R = a.S - 1;
+  const float* planes[3] = {a.grid[0], a.grid[1], a.grid[2]};
+  float* gplanes[3] = {a.ggrid[0], a.ggrid[1], a.ggrid[2]};
+  float bg[kC];
+#pragma unroll
+  for (int c = 0; c < kC; ++c) bg[c] = a.bg ? __ldg(a.bg + c) : 0.0f;
+  const uint32_t id_z = tc::idesc_bf16(128, HID, 0, 0);
+  const uint32_t id_dh = tc::idesc_bf16(128, S::KP, 0, 1);
+  const uint32_t id_w0 = tc::idesc_bf16(64, S::KP, 1, 1);
+  const uint32_t id_wo = tc::idesc_bf16(64, 8, 1, 1);
+  const uint32_t h_addr = tc::smem_u32(Ht), w_addr = tc::smem_u32(w0p);
+  const uint32_t d1_addr = tc::smem_u32(D1t), a1_addr = tc::smem_u32(A1t), do_addr = tc::smem_u32(DOt);
+  uint32_t phase = 0, wacc = 0;   // wacc: weight-gradient accumulators initialised (issuing thread)
+  float db0[HID], dbo[kOut];
+#pragma unroll
+  for (int i = 0; i < HID; ++i) db0[i] = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kOut; ++i) dbo[i] = 0.0f;
+
+  const int64_t ntiles = (a.M + 127) / 128;
+  for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
+    const int64_t r0 = tile * 128 + gt;
+    const bool valid = r0 < a.M;
+    const int64_t r = valid ? r0 : a.M - 1;   // tail rows march a real ray with zero upstream
+    const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
+    float p[kC];
+#pragma unroll
+    for (int c = 0; c < kC; ++c) p[c] = valid ? __ldg(a.grad_out + 3 * r + c) : 0.0f;
+    const float gtau = (valid && a.grad_tau) ? __ldg(a.grad_tau + r) : 0.0f;
+    const float tauR = __ldg(a.tau + r);
+    float pbg = 0.0f;
+#pragma unroll
+    for (int c = 0; c < kC; ++c) pbg = fmaf(p[c], bg[c], pbg);
+    float G_ = expf(-tauR) * pbg;      // B1
+    float U = 0.0f, Ue = 0.0f;
+
+    for (int q = R; q >= 0; --q) {
+      // ---- B2: recompute sample q: taps, cooperative gather, Z = H W0^T
+      double x[3];
+      ray_point(ray, q, x);
+      write_taps<KIND, K>(taps + gt * S::NPL, x, a.dims);
+      __syncwarp();
+      coop_gather<KIND, K, S::KP, 3>(planes, taps, a.dims, Ht, S::H_PIECE, wg * 32, lane);
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      tc::named_bar(1 + g, 128);
+      if (gt == 0) {
+        tc::fence_after_sync();
+        constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
+        uint32_t acc = 0;
+#pragma unroll
+        for (int ks = 0; ks < S::KP / 16; ++ks)
+#pragma unroll
+          for (int c = 0; c < 6; ++c) {
+            tc::mma_bf16(tZ, tc::desc_kmajor(h_addr + PA[c] * S::H_PIECE, S::KP, ks),
+                         tc::desc_kmajor(w_addr + PB[c] * S::W0_PIECE, S::KP, ks), id_z, acc);
+            acc = 1;
+          }
+        tc::mma_commit(bar_z);
+      }
+      tc::mbar_wait(bar_z, phase);
+      tc::fence_after_sync();
+      float a1[HID];
+      tc::tmem_ld<HID>(tZ + tlane, a1);
+      float o[kOut];
+      tc_head_layer<HID>(fp + F::B0, fp + F::WOT, fp + F::BO, a1, o);   // a1 = relu(z + b0)
+      const float s_sig = sigmoid_f(o[0]);
+      const float ds = (float)ray.delta * softplus_f(o[0]);
+      float col[kC];
+#pragma unroll
+      for (int c = 0; c < kC; ++c) col[c] = sigmoid_f(o[1 + c]);
+      // ---- B3: Eq. 3, log-domain reverse update (R12)
+      const float tau_q = (tauR - U) - Ue;
+      two_sum_add(U, Ue, ds);
+      const float tau_qm1 = (tauR - U) - Ue;
+      float aq = 0.0f;
+#pragma unroll
+      for (int c = 0; c < kC; ++c) aq = fmaf(p[c], col[c], aq);
+      const float wq = q > 0 ? expf(-tau_qm1) * (-expm1f(-ds)) : 0.0f;
+      const float Tq_aq = q > 0 ? expf(-tau_q) * aq : 0.0f;
+      const float dsig = (float)ray.delta * (gtau - (G_ - Tq_aq));
+      G_ = fmaf(wq, aq, G_);
+      // ---- B4: head VJP
+      float dout[8];
+      dout[0] = dsig * s_sig;
+#pragma unroll
+      for (int c = 0; c < kC; ++c) dout[1 + c] = wq * p[c] * col[c] * (1.0f - col[c]);
+#pragma unroll
+      for (int c = 4; c < 8; ++c) dout[c] = 0.0f;
+      // ---- B5: delta1 = ReLU'(z) (Wo^T dout); bias gradients in registers
+      float d1[HID];
+#pragma unroll
+      for (int i = 0; i < HID; ++i) {
+        const float4 w = reinterpret_cast<const float4*>(fp + F::WOT)[i];
+        float sacc = w.x * dout[0];
+        sacc = fmaf(w.y, dout[1], sacc);
+        sacc = fmaf(w.z, dout[2], sacc);
+        sacc = fmaf(w.w, dout[3], sacc);
+        d1[i] = a1[i] > 0.0f ? sacc : 0.0f;
+        db0[i] += d1[i];
+      }
+#pragma unroll
+      for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
+#pragma unroll
+      for (int c = 0; c < HID / 8; ++c) {
+        tc::store8<2>(D1t, S::D_PIECE, gt, 8 * c, S::HP, d1 + 8 * c);
+        tc::store8<2>(A1t, S::D_PIECE, gt, 8 * c, S::HP, a1 + 8 * c);
+      }
+      tc::store8<2>(DOt, S::DO_PIECE, gt, 0, 8, dout);
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      tc::named_bar(1 + g, 128);
+      if (gt == 0) {
+        tc::fence_after_sync();
+        constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
+        // dH = D1 W0   (B = W0 viewed MN-major: MN = channel, K = hidden)
+#pragma unroll
+        for (int ks = 0; ks < HID / 16; ++ks)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            tc::mma_bf16(tDH, tc::desc_kmajor(d1_addr + QA[c] * S::D_PIECE, S::HP, ks),
+                         tc::desc_mnmajor(w_addr + QB[c] * S::W0_PIECE, S::KP, ks), id_dh, (ks | c) != 0);
+        // dW0 += D1^T H ; dWo^T += A1^T DOUT   (K = the 128 samples of this step)
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            tc::mma_bf16(tW0, tc::desc_mnmajor(d1_addr + QA[c] * S::D_PIECE, S::HP, ks),
+                         tc::desc_mnmajor(h_addr + QB[c] * S::H_PIECE, S::KP, ks), id_w0, wacc);
+            tc::mma_bf16(tWo, tc::desc_mnmajor(a1_addr + QA[c] * S::D_PIECE, S::HP, ks),
+                         tc::desc_mnmajor(do_addr + QB[c] * S::DO_PIECE, 8, ks), id_wo, wacc);
+            wacc = 1;
+          }
+        tc::mma_commit(bar_d);
+      }
+      tc::mbar_wait(bar_d, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+      // ---- B6: dH row -> fp32 staging -> cooperative scatter
+      {
+        float dh[S::KP];
+        tc::tmem_ld<S::KP>(tDH + tlane, dh);
+#pragma unroll
+        for (int k4 = 0; k4 < K / 4; ++k4)
+          *reinterpret_cast<float4*>(dhs + gt * (K + 4) + 4 * k4) =
+              make_float4(dh[4 * k4], dh[4 * k4 + 1], dh[4 * k4 + 2], dh[4 * k4 + 3]);
+      }
+      tc::fence_before_sync();
+      __syncwarp();
+      coop_scatter<KIND, K>(gplanes, taps, a.dims, dhs, wg * 32, lane);
+      __syncwarp();
+    }
+  }
+
+  // ---- B7: flush this group's gradient partials (TMEM accumulators + register bias sums)
+  tc::fence_after_sync();
+  const bool had_tiles = (int64_t)blockIdx.x * G + g < ntiles;
+  {
+    // M = 64 accumulators: row i lives in TMEM lane (i/16)*32 + i%16 -> warp wg, lanes 0..15
+    float w0row[S::KP], worow[8];
+    tc::tmem_ld<S::KP>(tW0 + tlane, w0row);
+    tc::tmem_ld<8>(tWo + tlane, worow);
+    const int row = 16 * wg + lane;
+    if (had_tiles && lane < 16 && row < HID) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) atomicAdd(a.gparams + P::W0 + row * K + c, w0row[c]);
+#pragma unroll
+      for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + row, worow[rr]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < HID; ++i) {
+    float s = db0[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    db0[i] = s;
+  }
+#pragma unroll
+  for (int i = 0; i < kOut; ++i) {
+    float s = dbo[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    dbo[i] = s;
+  }
+  if (lane == 0 && had_tiles) {
+#pragma unroll
+    for (int i = 0; i < HID; ++i) atomicAdd(a.gparams + P::B0 + i, db0[i]);
+#pragma unroll
+    for (int i = 0; i < kOut; ++i) atomicAdd(a.gparams + P::BO + i, dbo[i]);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(*tslot, L::TMEM_COLS);
+  }
+}
+
+}  // namespace lp

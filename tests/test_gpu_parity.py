@@ -145,11 +145,13 @@ def test_backward_additive_over_shards_and_linear(torch_cuda):
     g2 = lpb.render_backward(field, t["o"], t["d"], t["near"], t["far"], c.S, tau, 2 * t["go"], 2 * t["gt"],
                              t["bg"])
     torch.cuda.synchronize()
+    # fp32 accumulation order differs between the runs (atomics, per-CTA TMEM
+    # accumulators over different sample sets): the gradient tolerance applies
     for a, b, d in zip(g_all[0], gp, g2[0]):
-        assert rel_inf(b.cpu().numpy(), a.cpu().numpy()) < 1e-4
-        assert rel_inf(d.cpu().numpy(), 2 * a.cpu().numpy()) < 1e-4
-    assert rel_inf(gq.cpu().numpy(), g_all[1].cpu().numpy()) < 1e-4
-    assert rel_inf(g2[1].cpu().numpy(), 2 * g_all[1].cpu().numpy()) < 1e-4
+        assert rel_inf(b.cpu().numpy(), a.cpu().numpy()) < TOL_GRAD
+        assert rel_inf(d.cpu().numpy(), 2 * a.cpu().numpy()) < TOL_GRAD
+    assert rel_inf(gq.cpu().numpy(), g_all[1].cpu().numpy()) < TOL_GRAD
+    assert rel_inf(g2[1].cpu().numpy(), 2 * g_all[1].cpu().numpy()) < TOL_GRAD
 
 
 def test_memory_is_o1_per_ray(torch_cuda):
