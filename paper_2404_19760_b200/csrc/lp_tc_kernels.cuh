@@ -43,6 +43,10 @@ struct TcShape {
   // bytes
   static constexpr uint32_t W0_PIECE = HID * KP * 2;
   static constexpr uint32_t H_PIECE = TILE * KP * 2;
+  // backward H tile: channels + one 8-wide group whose first column is 1, so that
+  // the dW0 contraction D1^T [H | 1] also yields db0 = sum_s delta1 (no registers)
+  static constexpr int HC = KP + 8;
+  static constexpr uint32_t HB_PIECE = TILE * HC * 2;
   static constexpr uint32_t D_PIECE = TILE * HP * 2;
   static constexpr uint32_t DO_PIECE = TILE * 8 * 2;
   static constexpr uint32_t TAPS = TILE * NPL * 16;
@@ -107,7 +111,7 @@ __device__ __forceinline__ void record_corners(const float4 rec, int p, const Gr
 
 // Warp-cooperative gather of the warp's 32 rays: lane = (ray RPI-subgroup, chunk).
 // Writes h into rows [row0, row0 + 32) of the H tile (NP bf16 pieces).
-template <int KIND, int K, int KP, int NP>
+template <int KIND, int K, int C, int NP>
 __device__ __forceinline__ void coop_gather(const float* const* planes, const float4* taps, const GridDims& g,
                                             uint8_t* Htile, uint32_t piece_stride, int row0, int lane) {
   constexpr int KC = K / 4, RPI = 32 / KC, NPL = KIND == 0 ? 3 : 1;
@@ -133,7 +137,7 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
         acc[3] = fmaf(c.w[cc], v[cc].w, acc[3]);
       }
     }
-    tc::store4<NP>(Htile, piece_stride, row, 4 * ch, KP, acc);
+    tc::store4<NP>(Htile, piece_stride, row, 4 * ch, C, acc);
   }
 }
 
@@ -337,7 +341,7 @@ struct BwdTcSmem {
   static constexpr uint32_t FP = W0P + 3 * S::W0_PIECE;
   static constexpr uint32_t GRP = (FP + TcParams<K, HID>::N * 4 + 127) & ~127u;
   static constexpr uint32_t H = 0;                             // 3 pieces
-  static constexpr uint32_t D1 = H + 3 * S::H_PIECE;           // 2 pieces (reused as fp32 dH staging)
+  static constexpr uint32_t D1 = H + 3 * S::HB_PIECE;          // 2 pieces (reused as fp32 dH staging)
   static constexpr uint32_t A1 = D1 + 2 * S::D_PIECE;          // 2 pieces
   static constexpr uint32_t DO = A1 + 2 * S::D_PIECE;          // 2 pieces
   static constexpr uint32_t TAPS = DO + 2 * S::DO_PIECE;
@@ -348,7 +352,7 @@ struct BwdTcSmem {
   static_assert(2 * S::D_PIECE >= 128 * (K + 4) * 4, "dH staging fits the D1 region");
 };
 
-// TMEM columns of a group (bwd): Z [0,64), dH [64,96), dW0 [96,128), dWo [128,136)
+// TMEM columns of a group (bwd): Z [0,64), dH [64,96), [dW0 | db0] [96,136), dWo [144,152)
 template <int KIND, int K, int HID, int G>
 __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs a) {
   using S = TcShape<KIND, K, HID>;
@@ -382,7 +386,10 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = *tslot + (uint32_t)(g * 256);
-  const uint32_t tZ = tbase, tDH = tbase + 64, tW0 = tbase + 96, tWo = tbase + 128;
+  const uint32_t tZ = tbase, tDH = tbase + 64, tW0 = tbase + 96, tWo = tbase + 144;
+  // ones column of the H tile (piece 0 = 1, pieces 1, 2 = 0; written once, never overwritten)
+  *reinterpret_cast<__nv_bfloat16*>(Ht + tc::cm_off(gt, S::KP, S::HC)) = __float2bfloat16_rn(1.0f);
+  tc::fence_async_smem();
   const uint32_t tlane = (uint32_t)(wg * 32) << 16;
   uint64_t* bar_z = &bars[2 * g];
   uint64_t* bar_d = &bars[2 * g + 1];
@@ -395,14 +402,12 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   for (int c = 0; c < kC; ++c) bg[c] = a.bg ? __ldg(a.bg + c) : 0.0f;
   const uint32_t id_z = tc::idesc_bf16(128, HID, 0, 0);
   const uint32_t id_dh = tc::idesc_bf16(128, S::KP, 0, 1);
-  const uint32_t id_w0 = tc::idesc_bf16(64, S::KP, 1, 1);
+  const uint32_t id_w0 = tc::idesc_bf16(64, S::HC, 1, 1);
   const uint32_t id_wo = tc::idesc_bf16(64, 8, 1, 1);
   const uint32_t h_addr = tc::smem_u32(Ht), w_addr = tc::smem_u32(w0p);
   const uint32_t d1_addr = tc::smem_u32(D1t), a1_addr = tc::smem_u32(A1t), do_addr = tc::smem_u32(DOt);
   uint32_t phase = 0, wacc = 0;   // wacc: weight-gradient accumulators initialised (issuing thread)
-  float db0[HID], dbo[kOut];
-#pragma unroll
-  for (int i = 0; i < HID; ++i) db0[i] = 0.0f;
+  float dbo[kOut];
 #pragma unroll
   for (int i = 0; i < kOut; ++i) dbo[i] = 0.0f;
 
@@ -429,7 +434,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       ray_point(ray, q, x);
       write_taps<KIND, K>(taps + gt * S::NPL, x, a.dims);
       __syncwarp();
-      coop_gather<KIND, K, S::KP, 3>(planes, taps, a.dims, Ht, S::H_PIECE, wg * 32, lane);
+      coop_gather<KIND, K, S::HC, 3>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane);
       tc::fence_async_smem();
       tc::fence_before_sync();
       tc::named_bar(1 + g, 128);
@@ -441,7 +446,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
         for (int ks = 0; ks < S::KP / 16; ++ks)
 #pragma unroll
           for (int c = 0; c < 6; ++c) {
-            tc::mma_bf16(tZ, tc::desc_kmajor(h_addr + PA[c] * S::H_PIECE, S::KP, ks),
+            tc::mma_bf16(tZ, tc::desc_kmajor(h_addr + PA[c] * S::HB_PIECE, S::HC, ks),
                          tc::desc_kmajor(w_addr + PB[c] * S::W0_PIECE, S::KP, ks), id_z, acc);
             acc = 1;
           }
@@ -476,24 +481,23 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       for (int c = 0; c < kC; ++c) dout[1 + c] = wq * p[c] * col[c] * (1.0f - col[c]);
 #pragma unroll
       for (int c = 4; c < 8; ++c) dout[c] = 0.0f;
-      // ---- B5: delta1 = ReLU'(z) (Wo^T dout); bias gradients in registers
-      float d1[HID];
-#pragma unroll
-      for (int i = 0; i < HID; ++i) {
-        const float4 w = reinterpret_cast<const float4*>(fp + F::WOT)[i];
-        float sacc = w.x * dout[0];
-        sacc = fmaf(w.y, dout[1], sacc);
-        sacc = fmaf(w.z, dout[2], sacc);
-        sacc = fmaf(w.w, dout[3], sacc);
-        d1[i] = a1[i] > 0.0f ? sacc : 0.0f;
-        db0[i] += d1[i];
-      }
+      // ---- B5: per 8-unit chunk: stage a1, delta1 = ReLU'(z) (Wo^T dout), stage delta1
 #pragma unroll
       for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
 #pragma unroll
       for (int c = 0; c < HID / 8; ++c) {
-        tc::store8<2>(D1t, S::D_PIECE, gt, 8 * c, S::HP, d1 + 8 * c);
         tc::store8<2>(A1t, S::D_PIECE, gt, 8 * c, S::HP, a1 + 8 * c);
+        float d1[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float4 w = reinterpret_cast<const float4*>(fp + F::WOT)[8 * c + u];
+          float sacc = w.x * dout[0];
+          sacc = fmaf(w.y, dout[1], sacc);
+          sacc = fmaf(w.z, dout[2], sacc);
+          sacc = fmaf(w.w, dout[3], sacc);
+          d1[u] = a1[8 * c + u] > 0.0f ? sacc : 0.0f;
+        }
+        tc::store8<2>(D1t, S::D_PIECE, gt, 8 * c, S::HP, d1);
       }
       tc::store8<2>(DOt, S::DO_PIECE, gt, 0, 8, dout);
       tc::fence_async_smem();
@@ -515,7 +519,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             tc::mma_bf16(tW0, tc::desc_mnmajor(d1_addr + QA[c] * S::D_PIECE, S::HP, ks),
-                         tc::desc_mnmajor(h_addr + QB[c] * S::H_PIECE, S::KP, ks), id_w0, wacc);
+                         tc::desc_mnmajor(h_addr + QB[c] * S::HB_PIECE, S::HC, ks), id_w0, wacc);
             tc::mma_bf16(tWo, tc::desc_mnmajor(a1_addr + QA[c] * S::D_PIECE, S::HP, ks),
                          tc::desc_mnmajor(do_addr + QB[c] * S::DO_PIECE, 8, ks), id_wo, wacc);
             wacc = 1;
@@ -546,8 +550,8 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   const bool had_tiles = (int64_t)blockIdx.x * G + g < ntiles;
   {
     // M = 64 accumulators: row i lives in TMEM lane (i/16)*32 + i%16 -> warp wg, lanes 0..15
-    float w0row[S::KP], worow[8];
-    tc::tmem_ld<S::KP>(tW0 + tlane, w0row);
+    float w0row[S::HC], worow[8];
+    tc::tmem_ld<S::HC>(tW0 + tlane, w0row);
     tc::tmem_ld<8>(tWo + tlane, worow);
     const int row = 16 * wg + lane;
     if (had_tiles && lane < 16 && row < HID) {
@@ -555,14 +559,8 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       for (int c = 0; c < K; ++c) atomicAdd(a.gparams + P::W0 + row * K + c, w0row[c]);
 #pragma unroll
       for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + row, worow[rr]);
+      atomicAdd(a.gparams + P::B0 + row, w0row[S::KP]);   // ones column: db0
     }
-  }
-#pragma unroll
-  for (int i = 0; i < HID; ++i) {
-    float s = db0[i];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    db0[i] = s;
   }
 #pragma unroll
   for (int i = 0; i < kOut; ++i) {
@@ -572,8 +570,6 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
     dbo[i] = s;
   }
   if (lane == 0 && had_tiles) {
-#pragma unroll
-    for (int i = 0; i < HID; ++i) atomicAdd(a.gparams + P::B0 + i, db0[i]);
 #pragma unroll
     for (int i = 0; i < kOut; ++i) atomicAdd(a.gparams + P::BO + i, dbo[i]);
   }
