@@ -32,6 +32,9 @@ import workload as wl  # noqa: E402
 FALLBACK_HBM_GBS = 6650.0
 FP32_LANES_PER_SM = 128
 N_SM = 148
+# Measured L2 reduction throughput for full 128-byte fp32 lines (scripts/red_bench.cu,
+# profiles/r1_red_bench.txt): the roofline of the backward's grid-gradient scatter.
+L2_RED_GBS = 6070.0
 
 
 def parse():
@@ -48,6 +51,12 @@ def parse():
 
 
 # ------------------------------------------------------------------ algorithmic work
+def algorithmic_red_bytes_per_sample(cfg):
+    """Grid-gradient bytes the backward must reduce per sample (B6): corners x K fp32."""
+    corners = 12 if cfg.kind == wl.TRIPLANE else 8
+    return corners * cfg.K * 4
+
+
 def algorithmic_flops_per_sample(cfg):
     """FP32 FLOPs (2 per FMA) per sample the method itself must do.
     forward  K1: interpolation corners*K + MLP
@@ -228,10 +237,11 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_2404_19760_b200 as lpb
+    from paper_2404_19760_b200.dist import FlatGrads, allreduce_grads, shard_range
 
     cfg = wl.get_config(args.config)
     M_all = cfg.n_rays
-    lo, hi = rank * M_all // world, (rank + 1) * M_all // world
+    lo, hi = shard_range(M_all, rank, world)
     M = hi - lo
     S = cfg.S
 
@@ -240,11 +250,9 @@ def run_ours(args):
     params = torch.from_numpy(wl.make_mlp(cfg.widths)).to(dev)
     planes = [torch.from_numpy(g).to(dev) for g in grid]
     field = lpb.Field(cfg.kind, planes, cfg.widths, params)
-    sizes = [p.numel() for p in planes] + [params.numel()]
-    offs = np.cumsum([0] + [((s + 3) // 4) * 4 for s in sizes])
-    flat = torch.zeros(int(offs[-1]), device=dev)
-    gplanes = [flat[offs[i]:offs[i] + sizes[i]].view(planes[i].shape) for i in range(len(planes))]
-    gparams = flat[offs[-2]:offs[-2] + sizes[-1]]
+    grads = FlatGrads([p.shape for p in planes] + [params.shape], device=dev)
+    flat = grads.flat
+    gplanes, gparams = grads.views[:-1], grads.views[-1]
 
     # ---- this rank's rays + upstream gradients, resident in HBM
     chunk = 1 << 22
@@ -276,8 +284,7 @@ def run_ours(args):
         lpb.render_backward(field, o, d, near, far, S, tau, go, None, bg, grad_planes=gplanes, grad_params=gparams)
         if ev:
             ev[2].record(stream)
-        if world > 1:
-            dist.all_reduce(flat)
+        allreduce_grads(grads)
         if ev:
             ev[3].record(stream)
 
@@ -335,7 +342,7 @@ def run_ours(args):
             _, _, _, _, ws = lpb.fwd_bwd_host(field, oh, dh, nh, fh, S, goh, None, None, outh, tauh, gplanes,
                                               gparams, ws)
             if world > 1:
-                dist.all_reduce(flat)
+                allreduce_grads(grads)
                 torch.cuda.synchronize()
         dt = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
         if world > 1:
@@ -352,15 +359,18 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (K2 backward): FP32 ALU bound
+    # ---- roofline of the dominant kernel (K2tc backward, ~78% of the step). Its binding
+    # resource is the L2 reduction path of the grid-gradient scatter (B6): ncu shows the
+    # FP32 and tensor pipes <25% busy, HBM traffic ~70 B/ray, and the scatter's full-line
+    # reds at ~half the measured line-reduction rate.
     peaks, peak_src = load_peaks()
     clk_sum = clk.summary()
     fwd_f, bwd_f = algorithmic_flops_per_sample(cfg)
     samples = M * S
-    achieved = bwd_f * samples / (t_bwd / 1000.0) / 1e12
+    red_b = algorithmic_red_bytes_per_sample(cfg)
+    achieved_red = red_b * samples / (t_bwd / 1000.0) / 1e9
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    peak = fp32_peak_tflops(sm_max)
-    fwd_ach = fwd_f * samples / (t_fwd / 1000.0) / 1e12
+    alu_peak = fp32_peak_tflops(sm_max)
     traffic = ncu_traffic(cfg.name)
     line = {
         "metric": "rays/s fwd+bwd", "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
@@ -368,13 +378,20 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(cfg, world),
         "breakdown_ms": {"fwd": t_fwd, "bwd": t_bwd, "allreduce": t_ar},
         "peak_bytes_per_ray": bytes_per_ray,
-        "roofline": {"bound": "alu", "kernel": "lp_bwd_kernel (K2)", "achieved": achieved,
-                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+        "roofline": {"bound": "l2_atomic", "kernel": "lp_bwd_tc_kernel (K2tc, backward)",
+                     "achieved": achieved_red, "peak": L2_RED_GBS, "unit": "GB/s",
+                     "frac": achieved_red / L2_RED_GBS,
                      "traffic": (traffic * M / traffic_rays(cfg.name)) if traffic else None,
-                     "peak_source": f"FP32 FFMA: {N_SM} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz "
-                                    f"(sm_max_mhz {peak_src})",
-                     "fwd_kernel": {"achieved": fwd_ach, "frac": fwd_ach / peak},
-                     "algorithmic_flops_per_sample": {"fwd": fwd_f, "bwd": bwd_f}},
+                     "algorithmic": f"{red_b} B of fp32 grid-gradient reductions per sample (corners x K x 4)",
+                     "peak_source": "measured: scripts/red_bench.cu full-line red.global.add.v4.f32 into a "
+                                    "24 MB buffer, profiles/r1_red_bench.txt",
+                     "alu": {"achieved_tflops": bwd_f * samples / (t_bwd / 1000.0) / 1e12,
+                             "peak_tflops": alu_peak,
+                             "peak_source": f"FP32 FFMA {N_SM} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz "
+                                            f"(sm_max_mhz {peak_src}); algorithmic {bwd_f} FLOP/sample"},
+                     "fwd_kernel": {"kernel": "lp_fwd_tc_kernel (K1tc)",
+                                    "achieved_tflops": fwd_f * samples / (t_fwd / 1000.0) / 1e12,
+                                    "alu_frac": fwd_f * samples / (t_fwd / 1000.0) / 1e12 / alu_peak}},
         "clocks": clk_sum,
         "gpu_launches": 2 * args.steps,
     }

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblp_b200.so")
+LIB_PATH = os.environ.get("LP_LIB_PATH") or os.path.join(_HERE, "liblp_b200.so")  # override: A/B builds only
 
 LP_OK, LP_ERR_INVALID_ARG, LP_ERR_UNSUPPORTED, LP_ERR_MISALIGNED, LP_ERR_CUDA = range(5)
 LP_GRID_TRIPLANE, LP_GRID_VOXEL = 0, 1

@@ -127,8 +127,29 @@ lp_status dispatch(const Inst& in, const lp_grid* g, const lp::KernelArgs& a, cu
   return in.kind == LP_GRID_TRIPLANE ? dispatch_kind<FWD, 0>(in, a, w, s) : dispatch_kind<FWD, 1>(in, a, w, s);
 }
 
+}  // namespace
+
+namespace lpi {
+#ifdef LP_PHASES
+unsigned long long* dbg_buffer() {
+  static unsigned long long* d = [] {
+    unsigned long long* p = nullptr;
+    cudaMalloc(&p, sizeof(unsigned long long) * 16);
+    cudaMemset(p, 0, sizeof(unsigned long long) * 16);
+    return p;
+  }();
+  return d;
+}
+#endif
+}  // namespace lpi
+
+namespace {
+
 lp::KernelArgs make_args(const lp_grid* g, const lp_mlp* m, const lp_rays* r, const float* bg) {
   lp::KernelArgs a{};
+#ifdef LP_PHASES
+  a.dbg = lpi::dbg_buffer();
+#endif
   for (int i = 0; i < 3; ++i) a.grid[i] = g->data[i];
   if (g->kind == LP_GRID_VOXEL) a.grid[1] = a.grid[2] = nullptr;
   a.dims = lp::GridDims{g->H, g->W, g->D};
@@ -258,5 +279,15 @@ lp_status lp_set_l2_persist(float hit_ratio) {
   lpi::g_l2_hit.store(hit_ratio);
   return LP_OK;
 }
+
+#ifdef LP_PHASES
+// Debug-only (variant builds): per-phase warp-cycle sums of the tensor-core kernels.
+int lp_debug_phase_cycles(unsigned long long* host16, int reset) {
+  unsigned long long* d = lpi::dbg_buffer();
+  if (cudaMemcpy(host16, d, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+  if (reset && cudaMemset(d, 0, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+  return 0;
+}
+#endif
 
 }  // extern "C"

@@ -34,6 +34,7 @@ struct KernelArgs {
   float* tau;            // fwd: out [M]; bwd: in [M]
   const float* grad_out; // bwd: [M][3]
   const float* grad_tau; // bwd: [M] or null
+  unsigned long long* dbg;  // debug phase timers (LP_PHASES variant builds only), else null
 };
 
 // ---------------------------------------------------------------- MLP pieces (F4)

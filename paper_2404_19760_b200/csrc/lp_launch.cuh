@@ -71,8 +71,14 @@ inline bool force_fma() {
   return f;
 }
 
-constexpr int kFwdGroups = 2;
-constexpr int kBwdGroups = 2;
+#ifndef LP_FWD_GROUPS
+#define LP_FWD_GROUPS 2
+#endif
+#ifndef LP_BWD_GROUPS
+#define LP_BWD_GROUPS 2
+#endif
+constexpr int kFwdGroups = LP_FWD_GROUPS;
+constexpr int kBwdGroups = LP_BWD_GROUPS;
 
 template <int KIND, int K, int HID, int NH>
 lp_status run_fwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {

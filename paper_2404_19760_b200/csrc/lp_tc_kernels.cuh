@@ -30,7 +30,33 @@
 #include "lp_kernels.cuh"
 #include "lp_tc.cuh"
 
+#ifndef LP_GATHER_UNROLL
+#define LP_GATHER_UNROLL 2
+#endif
+
+#ifdef LP_PHASES
+// Debug-only phase timers (variant builds): per-warp clock64 deltas summed into
+// a.dbg[kernel * 8 + phase]; read with lp_debug_phase_cycles().
+#define LP_PT_DECL unsigned long long lp_pt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long lp_pt_t = clock64();
+#define LP_PT(i)                                  \
+  {                                               \
+    long long now_ = clock64();                   \
+    lp_pt_acc[i] += (unsigned long long)(now_ - lp_pt_t); \
+    lp_pt_t = now_;                               \
+  }
+#define LP_PT_FLUSH(k)                                                              \
+  if ((threadIdx.x & 31) == 0)                                                      \
+    for (int i_ = 0; i_ < 8; ++i_) atomicAdd(a.dbg + (k) * 8 + i_, lp_pt_acc[i_]);
+#else
+#define LP_PT_DECL
+#define LP_PT(i)
+#define LP_PT_FLUSH(k)
+#endif
+
 namespace lp {
+
+// iterations of the cooperative gather whose loads are kept in flight together
+constexpr int kGatherUnroll = LP_GATHER_UNROLL;
 
 template <int KIND, int K, int HID>
 struct TcShape {
@@ -116,7 +142,7 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
                                             uint8_t* Htile, uint32_t piece_stride, int row0, int lane) {
   constexpr int KC = K / 4, RPI = 32 / KC, NPL = KIND == 0 ? 3 : 1;
   const int ch = lane % KC, sub = lane / KC;
-#pragma unroll 1
+#pragma unroll kGatherUnroll
   for (int it = 0; it < KC; ++it) {
     const int row = row0 + it * RPI + sub;
     float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -269,6 +295,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
   const uint32_t idesc = tc::idesc_bf16(128, HID, 0, 0);
   const uint32_t h_addr = tc::smem_u32(Ht), w_addr = tc::smem_u32(w0p);
   uint32_t phase = 0;
+  LP_PT_DECL
 
   const int64_t ntiles = (a.M + 127) / 128;
   for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
@@ -283,10 +310,13 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
       ray_point(ray, j, x);                                        // F2
       write_taps<KIND, K>(taps + gt * S::NPL, x, a.dims);          // F3 (cells)
       __syncwarp();
+      LP_PT(0)
       coop_gather<KIND, K, S::KP, 3>(planes, taps, a.dims, Ht, S::H_PIECE, wg * 32, lane);  // F3 (gather)
+      LP_PT(1)
       tc::fence_async_smem();
       tc::fence_before_sync();
       tc::named_bar(1 + g, 128);
+      LP_PT(2)
       if (gt == 0) {                                               // F4: Z = H W0^T on the tensor core
         tc::fence_after_sync();
         constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
@@ -301,8 +331,10 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
           }
         tc::mma_commit(&bars[g]);
       }
+      LP_PT(3)
       tc::mbar_wait(&bars[g], phase);
       phase ^= 1;
+      LP_PT(4)
       tc::fence_after_sync();
       float z[HID];
       tc::tmem_ld<HID>(tmem + tlane, z);
@@ -316,6 +348,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
         for (int c = 0; c < kC; ++c) v[c] = fmaf(w, sigmoid_f(o[1 + c]), v[c]);
       }
       two_sum_add(tau, tau_e, ds);
+      LP_PT(5)
     }
     if (valid) {                                                   // F7
       const float tauR = tau + tau_e;
@@ -325,6 +358,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
       a.tau[r] = tauR;
     }
   }
+  LP_PT_FLUSH(0)
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -410,6 +444,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   float dbo[kOut];
 #pragma unroll
   for (int i = 0; i < kOut; ++i) dbo[i] = 0.0f;
+  LP_PT_DECL
 
   const int64_t ntiles = (a.M + 127) / 128;
   for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
@@ -434,10 +469,13 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       ray_point(ray, q, x);
       write_taps<KIND, K>(taps + gt * S::NPL, x, a.dims);
       __syncwarp();
+      LP_PT(0)
       coop_gather<KIND, K, S::HC, 3>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane);
+      LP_PT(1)
       tc::fence_async_smem();
       tc::fence_before_sync();
       tc::named_bar(1 + g, 128);
+      LP_PT(2)
       if (gt == 0) {
         tc::fence_after_sync();
         constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
@@ -453,6 +491,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
         tc::mma_commit(bar_z);
       }
       tc::mbar_wait(bar_z, phase);
+      LP_PT(3)
       tc::fence_after_sync();
       float a1[HID];
       tc::tmem_ld<HID>(tZ + tlane, a1);
@@ -500,6 +539,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
         tc::store8<2>(D1t, S::D_PIECE, gt, 8 * c, S::HP, d1);
       }
       tc::store8<2>(DOt, S::DO_PIECE, gt, 0, 8, dout);
+      LP_PT(4)
       tc::fence_async_smem();
       tc::fence_before_sync();
       tc::named_bar(1 + g, 128);
@@ -528,6 +568,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       }
       tc::mbar_wait(bar_d, phase);
       phase ^= 1;
+      LP_PT(5)
       tc::fence_after_sync();
       // ---- B6: dH row -> fp32 staging -> cooperative scatter
       {
@@ -542,8 +583,10 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       __syncwarp();
       coop_scatter<KIND, K>(gplanes, taps, a.dims, dhs, wg * 32, lane);
       __syncwarp();
+      LP_PT(6)
     }
   }
+  LP_PT_FLUSH(1)
 
   // ---- B7: flush this group's gradient partials (TMEM accumulators + register bias sums)
   tc::fence_after_sync();

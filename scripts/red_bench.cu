@@ -1,0 +1,64 @@
+// red_bench.cu -- throughput of full-line (128 B) gradient scatters into a 24 MB fp32 buffer:
+//   A: 8 lanes x red.global.add.v4.f32 per line (4 lines per warp instruction)
+//   B: stage the line in shared memory, cp.reduce.async.bulk (UBLKRED) per line
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__global__ void redA(float* g, const int* lines, int nl_per_warp, int nlines_total) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int* L = lines + (size_t)warp * nl_per_warp;
+  const int sub = lane >> 3, ch = lane & 7;
+  for (int i = 0; i < nl_per_warp; i += 4) {
+    int line = L[i + sub];
+    float4 v = make_float4(1.f, 1.f, 1.f, 1.f);
+    atomicAdd(reinterpret_cast<float4*>(g + (size_t)line * 32 + 4 * ch), v);
+  }
+}
+
+__global__ void redB(float* g, const int* lines, int nl_per_warp, int nlines_total) {
+  __shared__ __align__(128) float st[8][4][32];
+  const int w = threadIdx.x >> 5, warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int* L = lines + (size_t)warp * nl_per_warp;
+  const int sub = lane >> 3, ch = lane & 7;
+  for (int i = 0; i < nl_per_warp; i += 4) {
+    *reinterpret_cast<float4*>(&st[w][sub][4 * ch]) = make_float4(1.f, 1.f, 1.f, 1.f);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane < 4) {
+      int line = L[i + lane];
+      asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], 128;" ::"l"(g + (size_t)line * 32),
+                   "r"((unsigned)__cvta_generic_to_shared(&st[w][lane][0]))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    __syncwarp();
+  }
+}
+
+int main() {
+  const int nlines = 24 * 1024 * 1024 / 128;  // 24 MB buffer
+  const int blocks = 148 * 4, threads = 256, warps = blocks * threads / 32;
+  const int per = 4096;
+  float* g; int* lines;
+  cudaMalloc(&g, (size_t)nlines * 128); cudaMemset(g, 0, (size_t)nlines * 128);
+  cudaMalloc(&lines, (size_t)warps * per * 4);
+  int* h = new int[(size_t)warps * per];
+  uint32_t s = 1;
+  for (size_t i = 0; i < (size_t)warps * per; ++i) { s = s * 1664525u + 1013904223u; h[i] = (s >> 4) % nlines; }
+  cudaMemcpy(lines, h, (size_t)warps * per * 4, cudaMemcpyHostToDevice);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int v = 0; v < 2; ++v) {
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(a);
+      if (v == 0) redA<<<blocks, threads>>>(g, lines, per, nlines); else redB<<<blocks, threads>>>(g, lines, per, nlines);
+      cudaEventRecord(b); cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b);
+      double nl = (double)warps * per;
+      printf("%s: %.3f ms  %.2f G lines/s  %.2f TB/s payload  (%s)\n", v == 0 ? "A red.v4 x8 lanes" : "B bulk reduce   ", ms,
+             nl / ms / 1e6, nl * 128 / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  return 0;
+}

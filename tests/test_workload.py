@@ -47,3 +47,13 @@ def test_mlp_init_layout():
     assert np.max(np.abs(W0)) <= 1 / np.sqrt(32)
     b1 = p[-4:]
     assert abs(np.log1p(np.exp(b1[0])) - 1.2) < 1e-6 and np.all(b1[1:] == 0)
+
+
+def test_tiled_pixel_order_is_a_permutation():
+    for img in (64, 256, 800):
+        pix = np.arange(img * img)
+        r, c = wl.pixel_of(pix, img)
+        assert len(set((r * img + c).tolist())) == img * img
+        assert r.min() == 0 and r.max() == img - 1 and c.max() == img - 1
+    r, c = wl.pixel_of(np.arange(32), 256)     # first warp = 8x4 block
+    assert set(r.tolist()) == {0, 1, 2, 3} and set(c.tolist()) == set(range(8))

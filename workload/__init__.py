@@ -12,8 +12,9 @@ Recipe:
   shard or subset of a tensor reproduces exactly the same numbers.
 * Cameras: V views on a Fibonacci sphere of radius 4 looking at the origin,
   up = +z (fallback +y), pinhole with 30 deg field of view, one ray per pixel
-  centre (u+0.5, v+0.5), unit directions, raster order within a view, views in
-  index order. (Rays: PAPER.md P:234 "M rays ... R+1 points per ray";
+  centre (u+0.5, v+0.5), unit directions, views in index order; within a view
+  rays come in 16x8-pixel tiles of four 8x4 blocks (`pixel_of`), the batching a
+  renderer uses so that neighbouring rays sit in the same warp / CTA. (Rays: PAPER.md P:234 "M rays ... R+1 points per ray";
   pixel centres as SPEC.md S:193.)
 * near/far: per-ray slab intersection with the cube [-1+1e-4, 1-1e-4]^3, so
   every sample of a hitting ray lies in the grid's domain (the paper's
@@ -206,6 +207,26 @@ def _camera_basis(c: np.ndarray):
     return right, down, fwd
 
 
+TILE_W, TILE_H = 16, 8
+
+
+def pixel_of(pix: np.ndarray, img: int):
+    """Ray order within a view: 16x8-pixel tiles in raster order of tiles; inside a
+    tile, four 8x4 blocks (2 x 2) of 32 pixels, each block in raster order. So every
+    128 consecutive rays form a compact 16x8 patch and every 32 an 8x4 patch
+    (images whose side is not a multiple of 16 fall back to plain raster order)."""
+    pix = np.asarray(pix, dtype=np.int64)
+    if img % TILE_W or img % TILE_H:
+        return pix // img, pix % img
+    t, u = pix // (TILE_W * TILE_H), pix % (TILE_W * TILE_H)
+    tiles_x = img // TILE_W
+    tx, ty = t % tiles_x, t // tiles_x
+    w, l = u // 32, u % 32
+    col = tx * TILE_W + (w % 2) * 8 + l % 8
+    row = ty * TILE_H + (w // 2) * 4 + l // 8
+    return row, col
+
+
 def make_rays(cfg: Config, idx: Optional[np.ndarray] = None, start: int = 0,
               count: Optional[int] = None, fov_deg: float = 30.0, margin: float = 1e-4):
     """Rays for global ray indices `idx` (or the contiguous range [start, start+count)).
@@ -220,8 +241,9 @@ def make_rays(cfg: Config, idx: Optional[np.ndarray] = None, start: int = 0,
     npix = cfg.img * cfg.img
     view = idx // npix
     pix = idx % npix
-    row = (pix // cfg.img).astype(np.float64)
-    col = (pix % cfg.img).astype(np.float64)
+    row, col = pixel_of(pix, cfg.img)
+    row = row.astype(np.float64)
+    col = col.astype(np.float64)
     f = cfg.img / (2.0 * math.tan(math.radians(fov_deg) / 2.0))
     cx = cy = cfg.img / 2.0
     cams = camera_positions(cfg.views)
