@@ -470,7 +470,9 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       write_taps<KIND, K>(taps + gt * S::NPL, x, a.dims);
       __syncwarp();
       LP_PT(0)
+#ifndef LP_ABL_NOGATHER
       coop_gather<KIND, K, S::HC, 3>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane);
+#endif
       LP_PT(1)
       tc::fence_async_smem();
       tc::fence_before_sync();
@@ -581,7 +583,9 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       }
       tc::fence_before_sync();
       __syncwarp();
+#ifndef LP_ABL_NOSCATTER   // ablation hooks (timing experiments only; results are wrong when set)
       coop_scatter<KIND, K>(gplanes, taps, a.dims, dhs, wg * 32, lane);
+#endif
       __syncwarp();
       LP_PT(6)
     }
