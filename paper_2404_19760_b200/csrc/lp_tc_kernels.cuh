@@ -31,7 +31,7 @@
 #include "lp_tc.cuh"
 
 #ifndef LP_GATHER_UNROLL
-#define LP_GATHER_UNROLL 2
+#define LP_GATHER_UNROLL 1
 #endif
 
 #ifdef LP_PHASES
@@ -137,9 +137,14 @@ __device__ __forceinline__ void record_corners(const float4 rec, int p, const Gr
 
 // Warp-cooperative gather of the warp's 32 rays: lane = (ray RPI-subgroup, chunk).
 // Writes h into rows [row0, row0 + 32) of the H tile (NP bf16 pieces).
-template <int KIND, int K, int C, int NP>
+// With SCATTER, each iteration also issues the grid-gradient reductions of the
+// previous march step for the same lane slot (records `ptaps`, dh rows `dhs`):
+// the L2 reductions of step q+1 overlap the corner loads of step q (B6 || F3).
+template <int KIND, int K, int C, int NP, bool SCATTER = false>
 __device__ __forceinline__ void coop_gather(const float* const* planes, const float4* taps, const GridDims& g,
-                                            uint8_t* Htile, uint32_t piece_stride, int row0, int lane) {
+                                            uint8_t* Htile, uint32_t piece_stride, int row0, int lane,
+                                            float* const* gplanes = nullptr, const float4* ptaps = nullptr,
+                                            const float* dhs = nullptr) {
   constexpr int KC = K / 4, RPI = 32 / KC, NPL = KIND == 0 ? 3 : 1;
   const int ch = lane % KC, sub = lane / KC;
 #pragma unroll kGatherUnroll
@@ -155,6 +160,20 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
       float4 v[Corners<KIND, K>::N];
 #pragma unroll
       for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) v[cc] = __ldg(reinterpret_cast<const float4*>(pl + c.off[cc]));
+      if constexpr (SCATTER) {
+        const float4 prec = ptaps[row * NPL + p];
+        if (__float_as_int(prec.x) >= 0) {
+          const float4 d = *reinterpret_cast<const float4*>(dhs + row * (K + 4) + 4 * ch);
+          Corners<KIND, K> pc;
+          record_corners<KIND, K>(prec, p, g, pc);
+          float* gpl = gplanes[p] + 4 * ch;
+#pragma unroll
+          for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) {
+            const float w = pc.w[cc];
+            atomicAdd(reinterpret_cast<float4*>(gpl + pc.off[cc]), make_float4(w * d.x, w * d.y, w * d.z, w * d.w));
+          }
+        }
+      }
 #pragma unroll
       for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) {
         acc[0] = fmaf(c.w[cc], v[cc].x, acc[0]);
@@ -406,6 +425,10 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   uint8_t* A1t = gsm + L::A1;
   uint8_t* DOt = gsm + L::DO;
   float* dhs = reinterpret_cast<float*>(gsm + L::D1);
+  // tap records of the previous step (its scatter is fused into the next gather): A1 tile,
+  // free between the MMA2 completion and the next epilogue
+  float4* ptaps = reinterpret_cast<float4*>(gsm + L::A1);
+  bool pending = false;
   float4* taps = reinterpret_cast<float4*>(gsm + L::TAPS);
 
   for (uint32_t i = threadIdx.x * 16; i < L::BAR; i += blockDim.x * 16)
@@ -471,7 +494,11 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       __syncwarp();
       LP_PT(0)
 #ifndef LP_ABL_NOGATHER
-      coop_gather<KIND, K, S::HC, 3>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane);
+      if (pending)   // warp-uniform
+        coop_gather<KIND, K, S::HC, 3, true>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, gplanes, ptaps, dhs);
+      else
+        coop_gather<KIND, K, S::HC, 3>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane);
+      pending = false;
 #endif
       LP_PT(1)
       tc::fence_async_smem();
@@ -582,13 +609,20 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
               make_float4(dh[4 * k4], dh[4 * k4 + 1], dh[4 * k4 + 2], dh[4 * k4 + 3]);
       }
       tc::fence_before_sync();
-      __syncwarp();
+      // keep this step's tap records for its scatter, fused into the next gather
+#pragma unroll
+      for (int pp = 0; pp < S::NPL; ++pp) ptaps[gt * S::NPL + pp] = taps[gt * S::NPL + pp];
 #ifndef LP_ABL_NOSCATTER   // ablation hooks (timing experiments only; results are wrong when set)
-      coop_scatter<KIND, K>(gplanes, taps, a.dims, dhs, wg * 32, lane);
+      pending = true;
 #endif
       __syncwarp();
       LP_PT(6)
     }
+  }
+  if (pending) {   // the last step's scatter
+    __syncwarp();
+    coop_scatter<KIND, K>(gplanes, ptaps, a.dims, dhs, wg * 32, lane);
+    __syncwarp();
   }
   LP_PT_FLUSH(1)
 
