@@ -35,7 +35,13 @@ lp_status launch(KernelT kernel, LaunchShape& shape, size_t smem, int threads, i
   if (M == 0) return LP_OK;
   const int64_t tiles = (M + 127) / 128;
   const int64_t need = (tiles + groups - 1) / groups;
-  const int grid = (int)(need < shape.ctas ? need : shape.ctas);
+  int ctas = shape.ctas;
+  static const int cap = [] {   // LP_MAX_CTAS: cap the persistent grid (experiments only)
+    const char* e = getenv("LP_MAX_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  if (cap > 0 && cap < ctas) ctas = cap;
+  const int grid = (int)(need < ctas ? need : ctas);
 
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
