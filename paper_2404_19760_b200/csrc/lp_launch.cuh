@@ -5,7 +5,7 @@
 #include <mutex>
 
 #include "lp_internal.h"
-#include "lp_tc_kernels.cuh"
+#include "lp_tc2_kernels.cuh"
 
 namespace lpi {
 
@@ -66,9 +66,9 @@ lp_status launch(KernelT kernel, LaunchShape& shape, size_t smem, int threads, i
   return cuda_check(cudaGetLastError(), "kernel launch");
 }
 
-// Kernel variant: tensor-core kernels (K1tc/K2tc) for one-hidden-layer MLPs,
-// FFMA kernels (K1/K2) for two hidden layers. LP_KERNELS=fma forces the FFMA
-// kernels (A/B measurements only).
+// Kernel variant: tensor-core kernels K1tc/K2tc (one hidden layer) and K1tc2/K2tc2
+// (two hidden layers of width 64); FFMA kernels K1/K2 otherwise. LP_KERNELS=fma
+// forces the FFMA kernels (A/B measurements only).
 inline bool force_fma() {
   static const bool f = [] {
     const char* e = getenv("LP_KERNELS");
@@ -78,13 +78,17 @@ inline bool force_fma() {
 }
 
 #ifndef LP_FWD_GROUPS
-#define LP_FWD_GROUPS 2
+#define LP_FWD_GROUPS 4
+#endif
+#ifndef LP_FWD2_GROUPS
+#define LP_FWD2_GROUPS 2
 #endif
 #ifndef LP_BWD_GROUPS
 #define LP_BWD_GROUPS 2
 #endif
 constexpr int kFwdGroups = LP_FWD_GROUPS;
 constexpr int kBwdGroups = LP_BWD_GROUPS;
+constexpr int kFwd2Groups = LP_FWD2_GROUPS;
 
 template <int KIND, int K, int HID, int NH>
 lp_status run_fwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
@@ -93,6 +97,14 @@ lp_status run_fwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
       static LaunchShape shape;
       constexpr int G = kFwdGroups;
       return launch(lp::lp_fwd_tc_kernel<KIND, K, HID, G>, shape, lp::FwdTcSmem<KIND, K, HID, G>::BYTES, 128 * G, G,
+                    a.M, a, w, s);
+    }
+  }
+  if constexpr (NH == 2 && HID == 64 && K >= 8) {
+    if (!force_fma()) {
+      static LaunchShape shape;
+      constexpr int G = kFwd2Groups;
+      return launch(lp::lp_fwd_tc2_kernel<KIND, K, HID, G>, shape, lp::Fwd2Smem<KIND, K, HID, G>::BYTES, 256 * G, G,
                     a.M, a, w, s);
     }
   }
@@ -107,6 +119,13 @@ lp_status run_bwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
       constexpr int G = kBwdGroups;
       return launch(lp::lp_bwd_tc_kernel<KIND, K, HID, G>, shape, lp::BwdTcSmem<KIND, K, HID, G>::BYTES, 128 * G, G,
                     a.M, a, w, s);
+    }
+  }
+  if constexpr (NH == 2 && HID == 64 && K >= 8) {
+    if (!force_fma()) {
+      static LaunchShape shape;
+      return launch(lp::lp_bwd_tc2_kernel<KIND, K, HID>, shape, lp::Bwd2Smem<KIND, K, HID>::BYTES, 256, 1, a.M, a, w,
+                    s);
     }
   }
   static LaunchShape shape;

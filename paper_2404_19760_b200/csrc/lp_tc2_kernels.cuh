@@ -1,0 +1,600 @@
+// lp_tc2_kernels.cuh -- tensor-core (tcgen05) ray march for two-hidden-layer MLPs
+// (the paper's own field MLP: 3 linear layers of width 64): K1tc2 (forward,
+// Eq. 1) and K2tc2 (backward, Eq. 3).
+//
+// Same tile scheme as lp_tc_kernels.cuh (a group owns 128 rays, marched step by
+// step; the cooperative gather fills a bf16-piece H tile; one elected thread
+// issues tcgen05.mma into TMEM), with two threads per ray: the group has 256
+// threads, thread (half, row) handles hidden units [half*HID/2, (half+1)*HID/2)
+// of its ray's sample in every epilogue, so the per-thread dependency chains are
+// half as long and twice as many warps hide the gather/MMA latencies. The two
+// halves exchange the 4 partial output-layer sums through shared memory and
+// then both hold the (identical) per-ray EA state. Per step:
+//   forward   gather H | Z1 = H W0^T | a1 -> A1 tile | Z2 = A1 W1^T | a2, o, heads, EA
+//   backward  gather H (+ scatter of step q+1) | Z1 | a1 -> A1 | Z2 | a2, o, heads, Eq. 3,
+//             delta2 -> D2, a2 -> A2, dL/do -> DO |
+//             dA1 = D2 W1, dW1|db1 += D2^T [A1|1], dWo += A2^T DO | delta1 -> D1 |
+//             dH = D1 W0, dW0|db0 += D1^T [H|1] | dH -> fp32 staging (scattered next step)
+// Precision as in lp_tc.cuh: forward-type contractions (Z1, Z2) on 3 bf16 pieces
+// with 6 piece products (fp32-class), gradient contractions on 2 pieces with 3
+// products.
+#pragma once
+
+#include "lp_tc_kernels.cuh"
+
+namespace lp {
+
+template <int HID>
+struct Tc2Params {  // fp32 copies used on CUDA cores
+  static constexpr int B0 = 0;                // [HID]
+  static constexpr int B1 = HID;              // [HID]
+  static constexpr int WOT = 2 * HID;         // [HID][4]
+  static constexpr int BO = WOT + 4 * HID;    // [4]
+  static constexpr int N = round4(BO + 4);
+};
+
+template <int KIND, int K, int HID>
+struct Tc2Shape : TcShape<KIND, K, HID> {
+  using S = TcShape<KIND, K, HID>;
+  static constexpr int HH = HID / 2;                           // hidden units per half-thread
+  static constexpr int HC1 = HID + 8;                          // A1 tile columns (+ ones column, bwd)
+  static constexpr uint32_t W1_PIECE = HID * HID * 2;
+  static constexpr uint32_t W0P = 0;                           // W0 [HID][KP], 3 pieces
+  static constexpr uint32_t W1P = W0P + 3 * S::W0_PIECE;       // W1 [HID][HID], 3 pieces
+  static constexpr uint32_t FP = W1P + 3 * W1_PIECE;
+  static constexpr uint32_t GRP = (FP + Tc2Params<HID>::N * 4 + 127) & ~127u;
+  static_assert(HID == 64, "two-hidden-layer tensor-core kernels: hidden width 64");
+  static_assert(K / 4 >= 2, "the two halves split the cooperative gather");
+};
+
+template <int K, int HID, int KP>
+__device__ __forceinline__ void stage_tc2_weights(uint8_t* w0p, uint8_t* w1p, float* fp, const float* __restrict__ g) {
+  using P = PackedParams<K, HID, 2>;
+  using F = Tc2Params<HID>;
+  for (int i = threadIdx.x; i < HID * K + HID * HID; i += blockDim.x) {
+    const bool l0 = i < HID * K;
+    const int j = l0 ? i : i - HID * K;
+    const int C = l0 ? K : HID, CP = l0 ? KP : HID;
+    const int r = j / C, c = j % C;
+    float v = g[(l0 ? P::W0 : P::W1) + j];
+    uint8_t* base = l0 ? w0p : w1p;
+    const uint32_t ps = (uint32_t)(HID * CP * 2);
+#pragma unroll
+    for (int pc = 0; pc < 3; ++pc) {
+      __nv_bfloat16 b = __float2bfloat16_rn(v);
+      *reinterpret_cast<__nv_bfloat16*>(base + pc * ps + tc::cm_off(r, c, CP)) = b;
+      v -= __bfloat162float(b);
+    }
+  }
+  for (int i = threadIdx.x; i < HID; i += blockDim.x) {
+    fp[F::B0 + i] = g[P::B0 + i];
+    fp[F::B1 + i] = g[P::B1 + i];
+  }
+  for (int i = threadIdx.x; i < 4 * HID; i += blockDim.x) {
+    const int r = i / HID, c = i % HID;
+    fp[F::WOT + c * 4 + r] = g[P::WO + i];
+  }
+  if (threadIdx.x < 4) fp[F::BO + threadIdx.x] = g[P::BO + threadIdx.x];
+}
+
+// 6 piece products of a 3-piece x 3-piece K-major contraction (forward-type)
+__device__ __forceinline__ void mma_split6(uint32_t d, uint32_t a, uint32_t a_piece, int CA, uint32_t b,
+                                           uint32_t b_piece, int CB, int nks, uint32_t idesc) {
+  constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
+  uint32_t acc = 0;
+  for (int ks = 0; ks < nks; ++ks)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      tc::mma_bf16(d, tc::desc_kmajor(a + PA[c] * a_piece, CA, ks), tc::desc_kmajor(b + PB[c] * b_piece, CB, ks),
+                   idesc, acc);
+      acc = 1;
+    }
+}
+
+// ================================================================= K1tc2 forward
+template <int KIND, int K, int HID, int G>
+struct Fwd2Smem : Tc2Shape<KIND, K, HID> {
+  using T = Tc2Shape<KIND, K, HID>;
+  static constexpr uint32_t A_PIECE = 128 * HID * 2;
+  static constexpr uint32_t X = 0;   // H tile (3 x H_PIECE), overlaid by the A1 tile (3 x A_PIECE)
+  static constexpr uint32_t XSZ = 3 * (T::H_PIECE > A_PIECE ? T::H_PIECE : A_PIECE);
+  static constexpr uint32_t TAPS = X + XSZ;            // [2 halves][128][NPL]
+  static constexpr uint32_t XO = TAPS + 2 * T::TAPS;   // [2 halves][128] float4 partial outputs
+  static constexpr uint32_t GSIZE = (XO + 2 * 128 * 16 + 127) & ~127u;
+  static constexpr uint32_t BAR = T::GRP + G * GSIZE;
+  static constexpr uint32_t BYTES = BAR + 8 * G + 16;
+  static constexpr uint32_t TMEM_COLS = G * 128 <= 128 ? 128 : G * 128 <= 256 ? 256 : 512;
+};
+
+template <int KIND, int K, int HID, int G>
+__global__ void __launch_bounds__(256 * G, 1) lp_fwd_tc2_kernel(const KernelArgs a) {
+  using L = Fwd2Smem<KIND, K, HID, G>;
+  using F = Tc2Params<HID>;
+  constexpr int HH = L::HH, KP = L::KP, NPL = L::NPL, KC = K / 4;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* w0p = smem + L::W0P;
+  uint8_t* w1p = smem + L::W1P;
+  float* fp = reinterpret_cast<float*>(smem + L::FP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 8 * G);
+
+  const int g = threadIdx.x >> 8, gt = threadIdx.x & 255, hf = gt >> 7, rt = gt & 127;
+  const int wq = (gt >> 5) & 3, lane = gt & 31;
+  uint8_t* gsm = smem + L::GRP + g * L::GSIZE;
+  uint8_t* X = gsm + L::X;
+  float4* taps = reinterpret_cast<float4*>(gsm + L::TAPS) + hf * 128 * NPL;
+  float4* xo = reinterpret_cast<float4*>(gsm + L::XO);
+
+  for (uint32_t i = threadIdx.x * 16; i < L::BAR; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  stage_tc2_weights<K, HID, KP>(w0p, w1p, fp, a.params);
+  if (threadIdx.x < G) tc::mbar_init(&bars[threadIdx.x], 1);
+  if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
+  tc::fence_async_smem();
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tZ1 = *tslot + (uint32_t)(g * 128), tZ2 = tZ1 + 64;
+  const uint32_t tl = ((uint32_t)(wq * 32) << 16) + (uint32_t)(hf * HH);
+  const int it0 = hf * (KC / 2), it1 = hf ? KC : KC / 2;
+
+  const int R = a.S - 1;
+  const float* planes[3] = {a.grid[0], a.grid[1], a.grid[2]};
+  float bg[kC];
+#pragma unroll
+  for (int c = 0; c < kC; ++c) bg[c] = a.bg ? __ldg(a.bg + c) : 0.0f;
+  const uint32_t idesc = tc::idesc_bf16(128, HID, 0, 0);
+  const uint32_t x_addr = tc::smem_u32(X), w0_addr = tc::smem_u32(w0p), w1_addr = tc::smem_u32(w1p);
+  uint32_t phase = 0;
+  const float* b0 = fp + F::B0 + hf * HH;
+  const float* b1 = fp + F::B1 + hf * HH;
+  const float4* wot = reinterpret_cast<const float4*>(fp + F::WOT) + hf * HH;
+
+  const int64_t ntiles = (a.M + 127) / 128;
+  for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
+    const int64_t r0 = tile * 128 + rt;
+    const bool valid = r0 < a.M;
+    const int64_t r = valid ? r0 : a.M - 1;
+    const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
+    float tau = 0.0f, tau_e = 0.0f;
+    float v[kC] = {0.0f, 0.0f, 0.0f};
+    for (int j = 0; j <= R; ++j) {
+      double x[3];
+      ray_point(ray, j, x);                                                // F2
+      write_taps<KIND, K>(taps + rt * NPL, x, a.dims);                     // F3 (cells)
+      __syncwarp();
+      coop_gather<KIND, K, KP, 3>(planes, taps, a.dims, X, L::H_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
+                                  it0, it1);                               // F3 (gather)
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      tc::named_bar(1 + g, 256);
+      if (gt == 0) {                                                       // F4: Z1 = H W0^T
+        tc::fence_after_sync();
+        mma_split6(tZ1, x_addr, L::H_PIECE, KP, w0_addr, L::W0_PIECE, KP, KP / 16, idesc);
+        tc::mma_commit(&bars[g]);
+      }
+      tc::mbar_wait(&bars[g], phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+      {                                                                    // a1 = relu(z1 + b0) -> A1 tile
+        float z[HH];
+        tc::tmem_ld<HH>(tZ1 + tl, z);
+#pragma unroll
+        for (int c = 0; c < HH / 8; ++c) {
+          float a1[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a1[u] = fmaxf(z[8 * c + u] + b0[8 * c + u], 0.0f);
+          tc::store8<3>(X, L::A_PIECE, rt, hf * HH + 8 * c, HID, a1);
+        }
+      }
+      tc::fence_before_sync();
+      tc::fence_async_smem();
+      tc::named_bar(1 + g, 256);
+      if (gt == 0) {                                                       // Z2 = A1 W1^T
+        tc::fence_after_sync();
+        mma_split6(tZ2, x_addr, L::A_PIECE, HID, w1_addr, L::W1_PIECE, HID, HID / 16, idesc);
+        tc::mma_commit(&bars[g]);
+      }
+      tc::mbar_wait(&bars[g], phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+      {                                                                    // a2, partial output layer
+        float z[HH];
+        tc::tmem_ld<HH>(tZ2 + tl, z);
+        float4 part = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+        for (int i = 0; i < HH; ++i) {
+          const float a2 = fmaxf(z[i] + b1[i], 0.0f);
+          const float4 w = wot[i];
+          part.x = fmaf(w.x, a2, part.x);
+          part.y = fmaf(w.y, a2, part.y);
+          part.z = fmaf(w.z, a2, part.z);
+          part.w = fmaf(w.w, a2, part.w);
+        }
+        xo[hf * 128 + rt] = part;
+      }
+      tc::fence_before_sync();
+      tc::named_bar(1 + g, 256);
+      const float4 p0 = xo[rt], p1 = xo[128 + rt];
+      float o[kOut];
+      o[0] = fp[F::BO + 0] + p0.x + p1.x;
+      o[1] = fp[F::BO + 1] + p0.y + p1.y;
+      o[2] = fp[F::BO + 2] + p0.z + p1.z;
+      o[3] = fp[F::BO + 3] + p0.w + p1.w;
+      const float ds = (float)ray.delta * softplus_f(o[0]);               // F5
+      if (j > 0) {                                                         // F6
+        const float w = expf(-(tau + tau_e)) * (-expm1f(-ds));
+#pragma unroll
+        for (int c = 0; c < kC; ++c) v[c] = fmaf(w, sigmoid_f(o[1 + c]), v[c]);
+      }
+      two_sum_add(tau, tau_e, ds);
+    }
+    if (valid && hf == 0) {                                                // F7
+      const float tauR = tau + tau_e;
+      const float TR = expf(-tauR);
+#pragma unroll
+      for (int c = 0; c < kC; ++c) a.out[3 * r + c] = fmaf(TR, bg[c], v[c]);
+      a.tau[r] = tauR;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(*tslot, L::TMEM_COLS);
+  }
+}
+
+// ================================================================= K2tc2 backward
+template <int KIND, int K, int HID>
+struct Bwd2Smem : Tc2Shape<KIND, K, HID> {
+  using T = Tc2Shape<KIND, K, HID>;
+  static constexpr uint32_t A1_PIECE = 128 * T::HC1 * 2;
+  static constexpr uint32_t DP = 128 * HID * 2;
+  static constexpr uint32_t H = T::GRP;                          // [128][HC] x 3 (ones column at KP)
+  static constexpr uint32_t A1 = H + 3 * T::HB_PIECE;            // [128][HC1] x 3 (ones column at HID); piece 2: ptaps
+  static constexpr uint32_t D = A1 + 3 * A1_PIECE;               // D2, then D1, then fp32 dH staging
+  static constexpr uint32_t A2 = D + 2 * DP;                     // [128][HID] x 2
+  static constexpr uint32_t DO = A2 + 2 * DP;                    // [128][8] x 2
+  static constexpr uint32_t TAPS = DO + 2 * T::DO_PIECE;         // [2 halves][128][NPL]
+  static constexpr uint32_t XO = TAPS + 2 * T::TAPS;             // [2 halves][128] float4
+  static constexpr uint32_t BAR = (XO + 2 * 128 * 16 + 127) & ~127u;
+  static constexpr uint32_t BYTES = BAR + 16;
+  static constexpr uint32_t TMEM_COLS = 256;
+  static_assert(2 * DP >= 128 * (K + 4) * 4, "dH staging fits the D region");
+  static_assert(A1_PIECE >= 128 * T::NPL * 16, "tap records fit A1 piece 2");
+};
+
+// TMEM columns: S0 [0,64) Z1 then dA1; S1 [64,128) Z2 then dH; [dW0|db0] [128,168);
+// dWo [168,176); [dW1|db1] [176,248)
+template <int KIND, int K, int HID>
+__global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) {
+  using L = Bwd2Smem<KIND, K, HID>;
+  using F = Tc2Params<HID>;
+  using P = PackedParams<K, HID, 2>;
+  constexpr int HH = L::HH, KP = L::KP, HC = L::HC, HC1 = L::HC1, NPL = L::NPL, KC = K / 4;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* w0p = smem + L::W0P;
+  uint8_t* w1p = smem + L::W1P;
+  float* fp = reinterpret_cast<float*>(smem + L::FP);
+  uint8_t* Ht = smem + L::H;
+  uint8_t* A1t = smem + L::A1;
+  uint8_t* Dt = smem + L::D;
+  uint8_t* A2t = smem + L::A2;
+  uint8_t* DOt = smem + L::DO;
+  float* dhs = reinterpret_cast<float*>(smem + L::D);
+  // previous step's tap records: A1 piece 2 (used only by the Z2 MMA; piece 0 holds the ones column)
+  float4* ptaps = reinterpret_cast<float4*>(smem + L::A1 + 2 * L::A1_PIECE);
+  float4* xo = reinterpret_cast<float4*>(smem + L::XO);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 8);
+
+  const int gt = threadIdx.x, hf = gt >> 7, rt = gt & 127, wq = (gt >> 5) & 3, lane = gt & 31;
+  float4* taps = reinterpret_cast<float4*>(smem + L::TAPS) + hf * 128 * NPL;
+
+  for (uint32_t i = threadIdx.x * 16; i < L::BAR; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  stage_tc2_weights<K, HID, KP>(w0p, w1p, fp, a.params);
+  if (threadIdx.x == 0) tc::mbar_init(bar, 1);
+  if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
+  // ones columns (piece 0 only; never overwritten): H[:, KP] -> db0, A1[:, HID] -> db1
+  if (hf == 0) *reinterpret_cast<__nv_bfloat16*>(Ht + tc::cm_off(rt, KP, HC)) = __float2bfloat16_rn(1.0f);
+  else *reinterpret_cast<__nv_bfloat16*>(A1t + tc::cm_off(rt, HID, HC1)) = __float2bfloat16_rn(1.0f);
+  tc::fence_async_smem();
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *tslot;
+  const uint32_t tS0 = tbase, tS1 = tbase + 64, tW0 = tbase + 128, tWo = tbase + 168, tW1 = tbase + 176;
+  const uint32_t tq = (uint32_t)(wq * 32) << 16;
+  const int it0 = hf * (KC / 2), it1 = hf ? KC : KC / 2;
+
+  const int R = a.S - 1;
+  const float* planes[3] = {a.grid[0], a.grid[1], a.grid[2]};
+  float* gplanes[3] = {a.ggrid[0], a.ggrid[1], a.ggrid[2]};
+  float bg[kC];
+#pragma unroll
+  for (int c = 0; c < kC; ++c) bg[c] = a.bg ? __ldg(a.bg + c) : 0.0f;
+  const uint32_t id_z = tc::idesc_bf16(128, HID, 0, 0);
+  const uint32_t id_da1 = tc::idesc_bf16(128, HID, 0, 1);
+  const uint32_t id_dh = tc::idesc_bf16(128, KP, 0, 1);
+  const uint32_t id_w1 = tc::idesc_bf16(64, HC1, 1, 1);
+  const uint32_t id_w0 = tc::idesc_bf16(64, HC, 1, 1);
+  const uint32_t id_wo = tc::idesc_bf16(64, 8, 1, 1);
+  const uint32_t h_addr = tc::smem_u32(Ht), a1_addr = tc::smem_u32(A1t), d_addr = tc::smem_u32(Dt);
+  const uint32_t a2_addr = tc::smem_u32(A2t), do_addr = tc::smem_u32(DOt);
+  const uint32_t w0_addr = tc::smem_u32(w0p), w1_addr = tc::smem_u32(w1p);
+  constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
+  uint32_t phase = 0, wacc = 0, wacc0 = 0;   // weight-gradient accumulators initialised (issuing thread)
+  bool pending = false;
+  float dbo[kOut] = {0.0f, 0.0f, 0.0f, 0.0f};
+  const float* b0 = fp + F::B0 + hf * HH;
+  const float* b1 = fp + F::B1 + hf * HH;
+  const float4* wot = reinterpret_cast<const float4*>(fp + F::WOT) + hf * HH;
+
+  auto mma_done = [&]() {
+    tc::mbar_wait(bar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+  };
+  auto to_tensor_core = [&]() {   // this thread's smem tiles / TMEM reads -> the MMA issuer
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    tc::named_bar(1, 256);
+  };
+
+  const int64_t ntiles = (a.M + 127) / 128;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * 128 + rt;
+    const bool valid = r0 < a.M;
+    const int64_t r = valid ? r0 : a.M - 1;   // tail rows march a real ray with zero upstream
+    const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
+    float p[kC];
+#pragma unroll
+    for (int c = 0; c < kC; ++c) p[c] = valid ? __ldg(a.grad_out + 3 * r + c) : 0.0f;
+    const float gtau = (valid && a.grad_tau) ? __ldg(a.grad_tau + r) : 0.0f;
+    const float tauR = __ldg(a.tau + r);
+    float pbg = 0.0f;
+#pragma unroll
+    for (int c = 0; c < kC; ++c) pbg = fmaf(p[c], bg[c], pbg);
+    float G_ = expf(-tauR) * pbg;      // B1
+    float U = 0.0f, Ue = 0.0f;
+
+    for (int q = R; q >= 0; --q) {
+      // ---- B2: recompute sample q (taps, gather fused with step q+1's scatter, Z1, Z2)
+      double x[3];
+      ray_point(ray, q, x);
+      write_taps<KIND, K>(taps + rt * NPL, x, a.dims);
+      __syncwarp();
+      if (pending)   // warp-uniform
+        coop_gather<KIND, K, HC, 3, true>(planes, taps, a.dims, Ht, L::HB_PIECE, wq * 32, lane, gplanes, ptaps, dhs,
+                                          it0, it1);
+      else
+        coop_gather<KIND, K, HC, 3>(planes, taps, a.dims, Ht, L::HB_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
+                                    it0, it1);
+      pending = false;
+      to_tensor_core();
+      if (gt == 0) {
+        tc::fence_after_sync();
+        mma_split6(tS0, h_addr, L::HB_PIECE, HC, w0_addr, L::W0_PIECE, KP, KP / 16, id_z);
+        tc::mma_commit(bar);
+      }
+      mma_done();
+      uint32_t mask1 = 0;   // ReLU'(z1) of this half's hidden units
+      {
+        float z[HH];
+        tc::tmem_ld<HH>(tS0 + tq + hf * HH, z);
+#pragma unroll
+        for (int c = 0; c < HH / 8; ++c) {
+          float a1[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float zz = z[8 * c + u] + b0[8 * c + u];
+            mask1 |= (zz > 0.0f ? 1u : 0u) << (8 * c + u);
+            a1[u] = fmaxf(zz, 0.0f);
+          }
+          tc::store8<3>(A1t, L::A1_PIECE, rt, hf * HH + 8 * c, HC1, a1);
+        }
+      }
+      to_tensor_core();
+      if (gt == 0) {
+        tc::fence_after_sync();
+        mma_split6(tS1, a1_addr, L::A1_PIECE, HC1, w1_addr, L::W1_PIECE, HID, HID / 16, id_z);
+        tc::mma_commit(bar);
+      }
+      mma_done();
+      float a2[HH];
+      {
+        tc::tmem_ld<HH>(tS1 + tq + hf * HH, a2);
+        float4 part = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+        for (int i = 0; i < HH; ++i) {
+          a2[i] = fmaxf(a2[i] + b1[i], 0.0f);
+          const float4 w = wot[i];
+          part.x = fmaf(w.x, a2[i], part.x);
+          part.y = fmaf(w.y, a2[i], part.y);
+          part.z = fmaf(w.z, a2[i], part.z);
+          part.w = fmaf(w.w, a2[i], part.w);
+        }
+        xo[hf * 128 + rt] = part;
+      }
+      tc::fence_before_sync();
+      tc::named_bar(1, 256);
+      float o[kOut];
+      {
+        const float4 p0 = xo[rt], p1 = xo[128 + rt];
+        o[0] = fp[F::BO + 0] + p0.x + p1.x;
+        o[1] = fp[F::BO + 1] + p0.y + p1.y;
+        o[2] = fp[F::BO + 2] + p0.z + p1.z;
+        o[3] = fp[F::BO + 3] + p0.w + p1.w;
+      }
+      const float s_sig = sigmoid_f(o[0]);
+      const float ds = (float)ray.delta * softplus_f(o[0]);
+      float col[kC];
+#pragma unroll
+      for (int c = 0; c < kC; ++c) col[c] = sigmoid_f(o[1 + c]);
+      // ---- B3: Eq. 3, log-domain reverse update (R12); both halves hold the same state
+      const float tau_q = (tauR - U) - Ue;
+      two_sum_add(U, Ue, ds);
+      const float tau_qm1 = (tauR - U) - Ue;
+      float aq = 0.0f;
+#pragma unroll
+      for (int c = 0; c < kC; ++c) aq = fmaf(p[c], col[c], aq);
+      const float wq_ = q > 0 ? expf(-tau_qm1) * (-expm1f(-ds)) : 0.0f;
+      const float Tq_aq = q > 0 ? expf(-tau_q) * aq : 0.0f;
+      const float dsig = (float)ray.delta * (gtau - (G_ - Tq_aq));
+      G_ = fmaf(wq_, aq, G_);
+      // ---- B4: head VJP
+      float dout[8];
+      dout[0] = dsig * s_sig;
+#pragma unroll
+      for (int c = 0; c < kC; ++c) dout[1 + c] = wq_ * p[c] * col[c] * (1.0f - col[c]);
+#pragma unroll
+      for (int c = 4; c < 8; ++c) dout[c] = 0.0f;
+      // ---- B5: delta2 = ReLU'(z2) (Wo^T dout) -> D2, a2 -> A2, dout -> DO
+      if (hf == 0) {
+#pragma unroll
+        for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
+        tc::store8<2>(DOt, L::DO_PIECE, rt, 0, 8, dout);
+      }
+#pragma unroll
+      for (int c = 0; c < HH / 8; ++c) {
+        float d2[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float4 w = wot[8 * c + u];
+          float s = w.x * dout[0];
+          s = fmaf(w.y, dout[1], s);
+          s = fmaf(w.z, dout[2], s);
+          s = fmaf(w.w, dout[3], s);
+          d2[u] = a2[8 * c + u] > 0.0f ? s : 0.0f;
+        }
+        tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, HID, d2);
+        tc::store8<2>(A2t, L::DP, rt, hf * HH + 8 * c, HID, a2 + 8 * c);
+      }
+      to_tensor_core();
+      if (gt == 0) {
+        tc::fence_after_sync();
+        // dA1 = D2 W1   (B = W1 [out][in] viewed MN-major: MN = in, K = out)
+#pragma unroll
+        for (int ks = 0; ks < HID / 16; ++ks)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            tc::mma_bf16(tS0, tc::desc_kmajor(d_addr + QA[c] * L::DP, HID, ks),
+                         tc::desc_mnmajor(w1_addr + QB[c] * L::W1_PIECE, HID, ks), id_da1, (ks | c) != 0);
+        // dW1|db1 += D2^T [A1|1] ; dWo^T += A2^T DOUT   (K = the 128 samples of this step)
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            tc::mma_bf16(tW1, tc::desc_mnmajor(d_addr + QA[c] * L::DP, HID, ks),
+                         tc::desc_mnmajor(a1_addr + QB[c] * L::A1_PIECE, HC1, ks), id_w1, wacc);
+            tc::mma_bf16(tWo, tc::desc_mnmajor(a2_addr + QA[c] * L::DP, HID, ks),
+                         tc::desc_mnmajor(do_addr + QB[c] * L::DO_PIECE, 8, ks), id_wo, wacc);
+            wacc = 1;
+          }
+        tc::mma_commit(bar);
+      }
+      mma_done();
+      {   // delta1 = ReLU'(z1) dA1 -> D1 (over D2, consumed)
+        float da[HH];
+        tc::tmem_ld<HH>(tS0 + tq + hf * HH, da);
+#pragma unroll
+        for (int c = 0; c < HH / 8; ++c) {
+          float d1[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) d1[u] = (mask1 >> (8 * c + u)) & 1u ? da[8 * c + u] : 0.0f;
+          tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, HID, d1);
+        }
+      }
+      to_tensor_core();
+      if (gt == 0) {
+        tc::fence_after_sync();
+        // dH = D1 W0 ; dW0|db0 += D1^T [H|1]
+#pragma unroll
+        for (int ks = 0; ks < HID / 16; ++ks)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            tc::mma_bf16(tS1, tc::desc_kmajor(d_addr + QA[c] * L::DP, HID, ks),
+                         tc::desc_mnmajor(w0_addr + QB[c] * L::W0_PIECE, KP, ks), id_dh, (ks | c) != 0);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            tc::mma_bf16(tW0, tc::desc_mnmajor(d_addr + QA[c] * L::DP, HID, ks),
+                         tc::desc_mnmajor(h_addr + QB[c] * L::HB_PIECE, HC, ks), id_w0, wacc0);
+            wacc0 = 1;
+          }
+        tc::mma_commit(bar);
+      }
+      mma_done();
+      // ---- B6: this half's dH channels -> fp32 staging; scattered by the next step's gather
+      {
+        constexpr int HK = KP / 2;
+        float dh[HK];
+        tc::tmem_ld<HK>(tS1 + tq + hf * HK, dh);
+#pragma unroll
+        for (int k4 = 0; k4 < HK / 4; ++k4)
+          if (hf * HK + 4 * k4 < K)
+            *reinterpret_cast<float4*>(dhs + rt * (K + 4) + hf * HK + 4 * k4) =
+                make_float4(dh[4 * k4], dh[4 * k4 + 1], dh[4 * k4 + 2], dh[4 * k4 + 3]);
+      }
+      if (hf == 0) {
+#pragma unroll
+        for (int pp = 0; pp < NPL; ++pp) ptaps[rt * NPL + pp] = taps[rt * NPL + pp];
+      }
+      pending = true;
+      tc::fence_before_sync();
+      tc::named_bar(1, 256);
+    }
+  }
+  if (pending) coop_scatter<KIND, K>(gplanes, ptaps, a.dims, dhs, wq * 32, lane, it0, it1);
+
+  // ---- B7: flush the gradient partials (TMEM accumulators + register bias sums)
+  tc::fence_after_sync();
+  const bool had_tiles = (int64_t)blockIdx.x < ntiles;
+  const int row = 16 * wq + lane;   // M = 64 accumulator row i lives in TMEM lane (i/16)*32 + i%16
+  if (hf == 0) {
+    float w0row[HC], worow[8];
+    tc::tmem_ld<HC>(tW0 + tq, w0row);
+    tc::tmem_ld<8>(tWo + tq, worow);
+    if (had_tiles && lane < 16) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) atomicAdd(a.gparams + P::W0 + row * K + c, w0row[c]);
+#pragma unroll
+      for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + row, worow[rr]);
+      atomicAdd(a.gparams + P::B0 + row, w0row[KP]);   // ones column: db0
+    }
+#pragma unroll
+    for (int i = 0; i < kOut; ++i) {
+      float s = dbo[i];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      dbo[i] = s;
+    }
+    if (lane == 0 && had_tiles) {
+#pragma unroll
+      for (int i = 0; i < kOut; ++i) atomicAdd(a.gparams + P::BO + i, dbo[i]);
+    }
+  } else {
+    float w1row[HC1];
+    tc::tmem_ld<HC1>(tW1 + tq, w1row);
+    if (had_tiles && lane < 16) {
+#pragma unroll
+      for (int c = 0; c < HID; ++c) atomicAdd(a.gparams + P::W1 + row * HID + c, w1row[c]);
+      atomicAdd(a.gparams + P::B1 + row, w1row[HID]);   // ones column: db1
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(*tslot, L::TMEM_COLS);
+  }
+}
+
+}  // namespace lp

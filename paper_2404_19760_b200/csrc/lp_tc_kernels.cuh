@@ -140,15 +140,16 @@ __device__ __forceinline__ void record_corners(const float4 rec, int p, const Gr
 // With SCATTER, each iteration also issues the grid-gradient reductions of the
 // previous march step for the same lane slot (records `ptaps`, dh rows `dhs`):
 // the L2 reductions of step q+1 overlap the corner loads of step q (B6 || F3).
+// Iterations [it0, it1) of the KC = K/4 per warp (two warps may split one row block).
 template <int KIND, int K, int C, int NP, bool SCATTER = false>
 __device__ __forceinline__ void coop_gather(const float* const* planes, const float4* taps, const GridDims& g,
                                             uint8_t* Htile, uint32_t piece_stride, int row0, int lane,
                                             float* const* gplanes = nullptr, const float4* ptaps = nullptr,
-                                            const float* dhs = nullptr) {
+                                            const float* dhs = nullptr, int it0 = 0, int it1 = K / 4) {
   constexpr int KC = K / 4, RPI = 32 / KC, NPL = KIND == 0 ? 3 : 1;
   const int ch = lane % KC, sub = lane / KC;
 #pragma unroll kGatherUnroll
-  for (int it = 0; it < KC; ++it) {
+  for (int it = it0; it < it1; ++it) {
     const int row = row0 + it * RPI + sub;
     float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
@@ -190,11 +191,11 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
 // dh rows are fp32 in `dhs` ([128][K + 4]).
 template <int KIND, int K>
 __device__ __forceinline__ void coop_scatter(float* const* gplanes, const float4* taps, const GridDims& g,
-                                             const float* dhs, int row0, int lane) {
+                                             const float* dhs, int row0, int lane, int it0 = 0, int it1 = K / 4) {
   constexpr int KC = K / 4, RPI = 32 / KC, NPL = KIND == 0 ? 3 : 1;
   const int ch = lane % KC, sub = lane / KC;
 #pragma unroll 1
-  for (int it = 0; it < KC; ++it) {
+  for (int it = it0; it < it1; ++it) {
     const int row = row0 + it * RPI + sub;
     const float4 d = *reinterpret_cast<const float4*>(dhs + row * (K + 4) + 4 * ch);
 #pragma unroll
