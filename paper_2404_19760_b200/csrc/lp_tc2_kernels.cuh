@@ -12,8 +12,8 @@
 // then both hold the (identical) per-ray EA state. Per step:
 //   forward   gather H | Z1 = H W0^T | a1 -> A1 tile | Z2 = A1 W1^T | a2, o, heads, EA
 //   backward  gather H (+ scatter of step q+1) | Z1 | a1 -> A1 | Z2 | a2, o, heads, Eq. 3,
-//             delta2 -> D2, a2 -> A2, dL/do -> DO |
-//             dA1 = D2 W1, dW1|db1 += D2^T [A1|1], dWo += A2^T DO | delta1 -> D1 |
+//             [delta2 | a2] -> DA tile, dL/do -> A1 tile |
+//             dA1 = D2 W1, [dW1 db1 . ; . . dWo^T] += [D2 | A2]^T [A1 | 1 | DO] | delta1 -> D1 |
 //             dH = D1 W0, dW0|db0 += D1^T [H|1] | dH -> fp32 staging (scattered next step)
 // Precision as in lp_tc.cuh: forward-type contractions (Z1, Z2) on 3 bf16 pieces
 // with 6 piece products (fp32-class), gradient contractions on 2 pieces with 3
@@ -37,7 +37,7 @@ template <int KIND, int K, int HID>
 struct Tc2Shape : TcShape<KIND, K, HID> {
   using S = TcShape<KIND, K, HID>;
   static constexpr int HH = HID / 2;                           // hidden units per half-thread
-  static constexpr int HC1 = HID + 8;                          // A1 tile columns (+ ones column, bwd)
+  static constexpr int HC1 = HID + 16;                         // A1 tile columns (+ ones, dL/do: bwd)
   static constexpr uint32_t W1_PIECE = HID * HID * 2;
   static constexpr uint32_t W0P = 0;                           // W0 [HID][KP], 3 pieces
   static constexpr uint32_t W1P = W0P + 3 * S::W0_PIECE;       // W1 [HID][HID], 3 pieces
@@ -252,23 +252,21 @@ template <int KIND, int K, int HID>
 struct Bwd2Smem : Tc2Shape<KIND, K, HID> {
   using T = Tc2Shape<KIND, K, HID>;
   static constexpr uint32_t A1_PIECE = 128 * T::HC1 * 2;
-  static constexpr uint32_t DP = 128 * HID * 2;
+  static constexpr uint32_t DP = 128 * 2 * HID * 2;
   static constexpr uint32_t H = T::GRP;                          // [128][HC] x 3 (ones column at KP)
-  static constexpr uint32_t A1 = H + 3 * T::HB_PIECE;            // [128][HC1] x 3 (ones column at HID); piece 2: ptaps
-  static constexpr uint32_t D = A1 + 3 * A1_PIECE;               // D2, then D1, then fp32 dH staging
-  static constexpr uint32_t A2 = D + 2 * DP;                     // [128][HID] x 2
-  static constexpr uint32_t DO = A2 + 2 * DP;                    // [128][8] x 2
-  static constexpr uint32_t TAPS = DO + 2 * T::DO_PIECE;         // [2 halves][128][NPL]
+  static constexpr uint32_t A1 = H + 3 * T::HB_PIECE;            // [A1 | 1 | DO] [128][HC1] x 3; piece 2: ptaps
+  static constexpr uint32_t D = A1 + 3 * A1_PIECE;               // [D2 | A2] x 2, then D1, then fp32 dH
+  static constexpr uint32_t TAPS = D + 2 * DP;                   // [2 halves][128][NPL]
   static constexpr uint32_t XO = TAPS + 2 * T::TAPS;             // [2 halves][128] float4
   static constexpr uint32_t BAR = (XO + 2 * 128 * 16 + 127) & ~127u;
   static constexpr uint32_t BYTES = BAR + 16;
   static constexpr uint32_t TMEM_COLS = 256;
-  static_assert(2 * DP >= 128 * (K + 4) * 4, "dH staging fits the D region");
+  static_assert(DP >= 128 * (K + 4) * 4, "dH staging fits the D region");
   static_assert(A1_PIECE >= 128 * T::NPL * 16, "tap records fit A1 piece 2");
 };
 
-// TMEM columns: S0 [0,64) Z1 then dA1; S1 [64,128) Z2 then dH; [dW0|db0] [128,168);
-// dWo [168,176); [dW1|db1] [176,248)
+// TMEM columns: S0 [0,64) Z1 then dA1; S1 [64,128) Z2 then dH; W1 [128,208): M = 128
+// rows [D2 units | A2 units] x [A1 units | 1 | dout] (dW1, db1, dWo^T); [dW0|db0] [208,248)
 template <int KIND, int K, int HID>
 __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) {
   using L = Bwd2Smem<KIND, K, HID>;
@@ -282,8 +280,6 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
   uint8_t* Ht = smem + L::H;
   uint8_t* A1t = smem + L::A1;
   uint8_t* Dt = smem + L::D;
-  uint8_t* A2t = smem + L::A2;
-  uint8_t* DOt = smem + L::DO;
   float* dhs = reinterpret_cast<float*>(smem + L::D);
   // previous step's tap records: A1 piece 2 (used only by the Z2 MMA; piece 0 holds the ones column)
   float4* ptaps = reinterpret_cast<float4*>(smem + L::A1 + 2 * L::A1_PIECE);
@@ -309,7 +305,7 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = *tslot;
-  const uint32_t tS0 = tbase, tS1 = tbase + 64, tW0 = tbase + 128, tWo = tbase + 168, tW1 = tbase + 176;
+  const uint32_t tS0 = tbase, tS1 = tbase + 64, tW1 = tbase + 128, tW0 = tbase + 208;
   const uint32_t tq = (uint32_t)(wq * 32) << 16;
   const int it0 = hf * (KC / 2), it1 = hf ? KC : KC / 2;
 
@@ -322,11 +318,9 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
   const uint32_t id_z = tc::idesc_bf16(128, HID, 0, 0);
   const uint32_t id_da1 = tc::idesc_bf16(128, HID, 0, 1);
   const uint32_t id_dh = tc::idesc_bf16(128, KP, 0, 1);
-  const uint32_t id_w1 = tc::idesc_bf16(64, HC1, 1, 1);
-  const uint32_t id_w0 = tc::idesc_bf16(64, HC, 1, 1);
-  const uint32_t id_wo = tc::idesc_bf16(64, 8, 1, 1);
+  const uint32_t id_w1 = tc::idesc_bf16(128, HC1, 1, 1);
+  const uint32_t id_w0 = tc::idesc_bf16(64, KP + 8, 1, 1);
   const uint32_t h_addr = tc::smem_u32(Ht), a1_addr = tc::smem_u32(A1t), d_addr = tc::smem_u32(Dt);
-  const uint32_t a2_addr = tc::smem_u32(A2t), do_addr = tc::smem_u32(DOt);
   const uint32_t w0_addr = tc::smem_u32(w0p), w1_addr = tc::smem_u32(w1p);
   constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
   uint32_t phase = 0, wacc = 0, wacc0 = 0;   // weight-gradient accumulators initialised (issuing thread)
@@ -455,11 +449,11 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
       for (int c = 0; c < kC; ++c) dout[1 + c] = wq_ * p[c] * col[c] * (1.0f - col[c]);
 #pragma unroll
       for (int c = 4; c < 8; ++c) dout[c] = 0.0f;
-      // ---- B5: delta2 = ReLU'(z2) (Wo^T dout) -> D2, a2 -> A2, dout -> DO
+      // ---- B5: delta2 = ReLU'(z2) (Wo^T dout) -> D2, a2 -> A2, dout -> A1 tile columns [HID+8, HID+16)
       if (hf == 0) {
 #pragma unroll
         for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
-        tc::store8<2>(DOt, L::DO_PIECE, rt, 0, 8, dout);
+        tc::store8<2>(A1t, L::A1_PIECE, rt, HID + 8, HC1, dout);
       }
 #pragma unroll
       for (int c = 0; c < HH / 8; ++c) {
@@ -473,8 +467,8 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
           s = fmaf(w.w, dout[3], s);
           d2[u] = a2[8 * c + u] > 0.0f ? s : 0.0f;
         }
-        tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, HID, d2);
-        tc::store8<2>(A2t, L::DP, rt, hf * HH + 8 * c, HID, a2 + 8 * c);
+        tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, 2 * HID, d2);
+        tc::store8<2>(Dt, L::DP, rt, HID + hf * HH + 8 * c, 2 * HID, a2 + 8 * c);
       }
       to_tensor_core();
       if (gt == 0) {
@@ -484,17 +478,15 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
         for (int ks = 0; ks < HID / 16; ++ks)
 #pragma unroll
           for (int c = 0; c < 3; ++c)
-            tc::mma_bf16(tS0, tc::desc_kmajor(d_addr + QA[c] * L::DP, HID, ks),
+            tc::mma_bf16(tS0, tc::desc_kmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
                          tc::desc_mnmajor(w1_addr + QB[c] * L::W1_PIECE, HID, ks), id_da1, (ks | c) != 0);
-        // dW1|db1 += D2^T [A1|1] ; dWo^T += A2^T DOUT   (K = the 128 samples of this step)
+        // [dW1 db1 . ; . . dWo^T] += [D2 | A2]^T [A1 | 1 | DOUT]   (K = the 128 samples of this step)
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            tc::mma_bf16(tW1, tc::desc_mnmajor(d_addr + QA[c] * L::DP, HID, ks),
+            tc::mma_bf16(tW1, tc::desc_mnmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
                          tc::desc_mnmajor(a1_addr + QB[c] * L::A1_PIECE, HC1, ks), id_w1, wacc);
-            tc::mma_bf16(tWo, tc::desc_mnmajor(a2_addr + QA[c] * L::DP, HID, ks),
-                         tc::desc_mnmajor(do_addr + QB[c] * L::DO_PIECE, 8, ks), id_wo, wacc);
             wacc = 1;
           }
         tc::mma_commit(bar);
@@ -508,7 +500,7 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
           float d1[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) d1[u] = (mask1 >> (8 * c + u)) & 1u ? da[8 * c + u] : 0.0f;
-          tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, HID, d1);
+          tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, 2 * HID, d1);
         }
       }
       to_tensor_core();
@@ -519,13 +511,13 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
         for (int ks = 0; ks < HID / 16; ++ks)
 #pragma unroll
           for (int c = 0; c < 3; ++c)
-            tc::mma_bf16(tS1, tc::desc_kmajor(d_addr + QA[c] * L::DP, HID, ks),
+            tc::mma_bf16(tS1, tc::desc_kmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
                          tc::desc_mnmajor(w0_addr + QB[c] * L::W0_PIECE, KP, ks), id_dh, (ks | c) != 0);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            tc::mma_bf16(tW0, tc::desc_mnmajor(d_addr + QA[c] * L::DP, HID, ks),
+            tc::mma_bf16(tW0, tc::desc_mnmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
                          tc::desc_mnmajor(h_addr + QB[c] * L::HB_PIECE, HC, ks), id_w0, wacc0);
             wacc0 = 1;
           }
@@ -557,16 +549,14 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
   // ---- B7: flush the gradient partials (TMEM accumulators + register bias sums)
   tc::fence_after_sync();
   const bool had_tiles = (int64_t)blockIdx.x < ntiles;
-  const int row = 16 * wq + lane;   // M = 64 accumulator row i lives in TMEM lane (i/16)*32 + i%16
   if (hf == 0) {
-    float w0row[HC], worow[8];
-    tc::tmem_ld<HC>(tW0 + tq, w0row);
-    tc::tmem_ld<8>(tWo + tq, worow);
+    // M = 64 accumulator: row i lives in TMEM lane (i/16)*32 + i%16
+    const int row = 16 * wq + lane;
+    float w0row[KP + 8];
+    tc::tmem_ld<KP + 8>(tW0 + tq, w0row);
     if (had_tiles && lane < 16) {
 #pragma unroll
       for (int c = 0; c < K; ++c) atomicAdd(a.gparams + P::W0 + row * K + c, w0row[c]);
-#pragma unroll
-      for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + row, worow[rr]);
       atomicAdd(a.gparams + P::B0 + row, w0row[KP]);   // ones column: db0
     }
 #pragma unroll
@@ -581,12 +571,18 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
       for (int i = 0; i < kOut; ++i) atomicAdd(a.gparams + P::BO + i, dbo[i]);
     }
   } else {
+    // M = 128 accumulator: row i in TMEM lane i; rows < HID: D2 units (dW1, db1), rows >= HID: A2 units (dWo^T)
+    const int row = 32 * wq + lane;
     float w1row[HC1];
     tc::tmem_ld<HC1>(tW1 + tq, w1row);
-    if (had_tiles && lane < 16) {
+    if (had_tiles && row < HID) {
 #pragma unroll
       for (int c = 0; c < HID; ++c) atomicAdd(a.gparams + P::W1 + row * HID + c, w1row[c]);
       atomicAdd(a.gparams + P::B1 + row, w1row[HID]);   // ones column: db1
+    }
+    if (had_tiles && row >= HID) {
+#pragma unroll
+      for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + (row - HID), w1row[HID + 8 + rr]);
     }
   }
   tc::fence_before_sync();

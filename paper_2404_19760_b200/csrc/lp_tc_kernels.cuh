@@ -69,11 +69,13 @@ struct TcShape {
   // bytes
   static constexpr uint32_t W0_PIECE = HID * KP * 2;
   static constexpr uint32_t H_PIECE = TILE * KP * 2;
-  // backward H tile: channels + one 8-wide group whose first column is 1, so that
-  // the dW0 contraction D1^T [H | 1] also yields db0 = sum_s delta1 (no registers)
-  static constexpr int HC = KP + 8;
+  // backward H tile [H | 1 | DO]: channels, an 8-wide group whose first column is 1
+  // (so the weight-gradient contraction also yields db0 = sum_s delta1), and the
+  // 8-wide dL/do group: one MMA set [D1 | A1]^T [H | 1 | DO] gives dW0, db0 and dWo
+  static constexpr int HC = KP + 16;
   static constexpr uint32_t HB_PIECE = TILE * HC * 2;
   static constexpr uint32_t D_PIECE = TILE * HP * 2;
+  static constexpr uint32_t DA_PIECE = TILE * 2 * HP * 2;   // [D1 | A1] tile
   static constexpr uint32_t DO_PIECE = TILE * 8 * 2;
   static constexpr uint32_t TAPS = TILE * NPL * 16;
   static_assert(HID % 16 == 0 && HID <= 64, "hidden width");
@@ -394,19 +396,20 @@ struct BwdTcSmem {
   static constexpr uint32_t W0P = 0;
   static constexpr uint32_t FP = W0P + 3 * S::W0_PIECE;
   static constexpr uint32_t GRP = (FP + TcParams<K, HID>::N * 4 + 127) & ~127u;
-  static constexpr uint32_t H = 0;                             // 3 pieces
-  static constexpr uint32_t D1 = H + 3 * S::HB_PIECE;          // 2 pieces (reused as fp32 dH staging)
-  static constexpr uint32_t A1 = D1 + 2 * S::D_PIECE;          // 2 pieces
-  static constexpr uint32_t DO = A1 + 2 * S::D_PIECE;          // 2 pieces
-  static constexpr uint32_t TAPS = DO + 2 * S::DO_PIECE;
+  static constexpr uint32_t H = 0;                             // [H | 1 | DO], 3 pieces
+  static constexpr uint32_t DA = H + 3 * S::HB_PIECE;          // [D1 | A1], 2 pieces; after the
+                                                               // MMAs: fp32 dH staging + tap records
+  static constexpr uint32_t PTAPS = DA + S::DA_PIECE;
+  static constexpr uint32_t TAPS = DA + 2 * S::DA_PIECE;
   static constexpr uint32_t GSIZE = (TAPS + S::TAPS + 127) & ~127u;
   static constexpr uint32_t BAR = GRP + G * GSIZE;             // 2 mbarriers per group + tmem slot
   static constexpr uint32_t BYTES = BAR + 16 * G + 16;
   static constexpr uint32_t TMEM_COLS = G == 1 ? 256 : 512;
-  static_assert(2 * S::D_PIECE >= 128 * (K + 4) * 4, "dH staging fits the D1 region");
+  static_assert(S::DA_PIECE >= 128 * (K + 4) * 4 && S::DA_PIECE >= 128 * S::NPL * 16, "staging fits the DA tile");
 };
 
-// TMEM columns of a group (bwd): Z [0,64), dH [64,96), [dW0 | db0] [96,136), dWo [144,152)
+// TMEM columns of a group (bwd): Z [0,64), dH [64,96), W [96,96+HC): M = 128 rows
+// [D1 units | A1 units] x [channels | 1 | dout] -> dW0, db0 (rows < 64), dWo^T (rows >= 64)
 template <int KIND, int K, int HID, int G>
 __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs a) {
   using S = TcShape<KIND, K, HID>;
@@ -422,13 +425,11 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   const int g = threadIdx.x >> 7, gt = threadIdx.x & 127, wg = gt >> 5, lane = gt & 31;
   uint8_t* gsm = smem + L::GRP + g * L::GSIZE;
   uint8_t* Ht = gsm + L::H;
-  uint8_t* D1t = gsm + L::D1;
-  uint8_t* A1t = gsm + L::A1;
-  uint8_t* DOt = gsm + L::DO;
-  float* dhs = reinterpret_cast<float*>(gsm + L::D1);
-  // tap records of the previous step (its scatter is fused into the next gather): A1 tile,
-  // free between the MMA2 completion and the next epilogue
-  float4* ptaps = reinterpret_cast<float4*>(gsm + L::A1);
+  uint8_t* DAt = gsm + L::DA;
+  // fp32 dH rows and tap records of the previous step (its scatter is fused into the
+  // next gather): DA tile, free between the MMA2 completion and the next epilogue
+  float* dhs = reinterpret_cast<float*>(gsm + L::DA);
+  float4* ptaps = reinterpret_cast<float4*>(gsm + L::PTAPS);
   bool pending = false;
   float4* taps = reinterpret_cast<float4*>(gsm + L::TAPS);
 
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = *tslot + (uint32_t)(g * 256);
-  const uint32_t tZ = tbase, tDH = tbase + 64, tW0 = tbase + 96, tWo = tbase + 144;
+  const uint32_t tZ = tbase, tDH = tbase + 64, tW = tbase + 96;
   // ones column of the H tile (piece 0 = 1, pieces 1, 2 = 0; written once, never overwritten)
   *reinterpret_cast<__nv_bfloat16*>(Ht + tc::cm_off(gt, S::KP, S::HC)) = __float2bfloat16_rn(1.0f);
   tc::fence_async_smem();
@@ -460,10 +461,8 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   for (int c = 0; c < kC; ++c) bg[c] = a.bg ? __ldg(a.bg + c) : 0.0f;
   const uint32_t id_z = tc::idesc_bf16(128, HID, 0, 0);
   const uint32_t id_dh = tc::idesc_bf16(128, S::KP, 0, 1);
-  const uint32_t id_w0 = tc::idesc_bf16(64, S::HC, 1, 1);
-  const uint32_t id_wo = tc::idesc_bf16(64, 8, 1, 1);
-  const uint32_t h_addr = tc::smem_u32(Ht), w_addr = tc::smem_u32(w0p);
-  const uint32_t d1_addr = tc::smem_u32(D1t), a1_addr = tc::smem_u32(A1t), do_addr = tc::smem_u32(DOt);
+  const uint32_t id_w = tc::idesc_bf16(128, S::HC, 1, 1);
+  const uint32_t h_addr = tc::smem_u32(Ht), w_addr = tc::smem_u32(w0p), da_addr = tc::smem_u32(DAt);
   uint32_t phase = 0, wacc = 0;   // wacc: weight-gradient accumulators initialised (issuing thread)
   float dbo[kOut];
 #pragma unroll
@@ -555,7 +554,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
 #pragma unroll
       for (int c = 0; c < HID / 8; ++c) {
-        tc::store8<2>(A1t, S::D_PIECE, gt, 8 * c, S::HP, a1 + 8 * c);
+        tc::store8<2>(DAt, S::DA_PIECE, gt, S::HP + 8 * c, 2 * S::HP, a1 + 8 * c);
         float d1[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -566,9 +565,9 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
           sacc = fmaf(w.w, dout[3], sacc);
           d1[u] = a1[8 * c + u] > 0.0f ? sacc : 0.0f;
         }
-        tc::store8<2>(D1t, S::D_PIECE, gt, 8 * c, S::HP, d1);
+        tc::store8<2>(DAt, S::DA_PIECE, gt, 8 * c, 2 * S::HP, d1);
       }
-      tc::store8<2>(DOt, S::DO_PIECE, gt, 0, 8, dout);
+      tc::store8<2>(Ht, S::HB_PIECE, gt, S::KP + 8, S::HC, dout);
       LP_PT(4)
       tc::fence_async_smem();
       tc::fence_before_sync();
@@ -581,17 +580,15 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
         for (int ks = 0; ks < HID / 16; ++ks)
 #pragma unroll
           for (int c = 0; c < 3; ++c)
-            tc::mma_bf16(tDH, tc::desc_kmajor(d1_addr + QA[c] * S::D_PIECE, S::HP, ks),
+            tc::mma_bf16(tDH, tc::desc_kmajor(da_addr + QA[c] * S::DA_PIECE, 2 * S::HP, ks),
                          tc::desc_mnmajor(w_addr + QB[c] * S::W0_PIECE, S::KP, ks), id_dh, (ks | c) != 0);
-        // dW0 += D1^T H ; dWo^T += A1^T DOUT   (K = the 128 samples of this step)
+        // [dW0 | db0 | . ; . | dWo^T] += [D1 | A1]^T [H | 1 | DOUT]   (K = the 128 samples of this step)
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            tc::mma_bf16(tW0, tc::desc_mnmajor(d1_addr + QA[c] * S::D_PIECE, S::HP, ks),
-                         tc::desc_mnmajor(h_addr + QB[c] * S::HB_PIECE, S::HC, ks), id_w0, wacc);
-            tc::mma_bf16(tWo, tc::desc_mnmajor(a1_addr + QA[c] * S::D_PIECE, S::HP, ks),
-                         tc::desc_mnmajor(do_addr + QB[c] * S::DO_PIECE, 8, ks), id_wo, wacc);
+            tc::mma_bf16(tW, tc::desc_mnmajor(da_addr + QA[c] * S::DA_PIECE, 2 * S::HP, ks),
+                         tc::desc_mnmajor(h_addr + QB[c] * S::HB_PIECE, S::HC, ks), id_w, wacc);
             wacc = 1;
           }
         tc::mma_commit(bar_d);
@@ -631,17 +628,19 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   tc::fence_after_sync();
   const bool had_tiles = (int64_t)blockIdx.x * G + g < ntiles;
   {
-    // M = 64 accumulators: row i lives in TMEM lane (i/16)*32 + i%16 -> warp wg, lanes 0..15
-    float w0row[S::HC], worow[8];
-    tc::tmem_ld<S::HC>(tW0 + tlane, w0row);
-    tc::tmem_ld<8>(tWo + tlane, worow);
-    const int row = 16 * wg + lane;
-    if (had_tiles && lane < 16 && row < HID) {
+    // M = 128 accumulator: row i lives in TMEM lane i (warp i / 32); rows [0, HP) are
+    // hidden units of D1 (dW0, db0), rows [HP, 2 HP) hidden units of A1 (dWo^T)
+    float wrow[S::HC];
+    tc::tmem_ld<S::HC>(tW + tlane, wrow);
+    const int row = 32 * wg + lane;
+    if (had_tiles && row < HID) {
 #pragma unroll
-      for (int c = 0; c < K; ++c) atomicAdd(a.gparams + P::W0 + row * K + c, w0row[c]);
+      for (int c = 0; c < K; ++c) atomicAdd(a.gparams + P::W0 + row * K + c, wrow[c]);
+      atomicAdd(a.gparams + P::B0 + row, wrow[S::KP]);   // ones column: db0
+    }
+    if (had_tiles && row >= S::HP && row - S::HP < HID) {
 #pragma unroll
-      for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + row, worow[rr]);
-      atomicAdd(a.gparams + P::B0 + row, w0row[S::KP]);   // ones column: db0
+      for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + (row - S::HP), wrow[S::KP + 8 + rr]);
     }
   }
 #pragma unroll
