@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 1
+#define LP_ABI_VERSION 2
 #define LP_MAX_LAYERS 8
 
 typedef enum {
@@ -56,6 +56,15 @@ typedef enum {
 
 typedef enum { LP_GRID_TRIPLANE = 0, LP_GRID_VOXEL = 1 } lp_grid_kind;
 
+/* Scene contraction applied to every sample point before hashing (Supp. Eq.
+ * "contract"; reading R25):
+ *   CC(x) = 0.5 a x                                   ||x|| <= 1
+ *   CC(x) = 0.5 ((2 - a)(1 - 1/||x||) + a) x/||x||    otherwise,
+ * mapping an unbounded scene into (-1,1)^3 with the foreground [-1,1] at
+ * [-a/2, a/2]. PER_AXIS applies it to each coordinate with ||x|| -> |x_k|
+ * (the paper's choice); RADIAL uses the Euclidean norm. */
+typedef enum { LP_CONTRACT_NONE = 0, LP_CONTRACT_PER_AXIS = 1, LP_CONTRACT_RADIAL = 2 } lp_contraction;
+
 /* theta, the 3D hash structure. Channel-last, K contiguous floats
  * per grid vertex. Axis convention (reading R9): x <-> H, y <-> W, z <-> D;
  * the world cube [-1,1]^3 maps to vertex index space [0, N-1] per axis
@@ -65,12 +74,16 @@ typedef enum { LP_GRID_TRIPLANE = 0, LP_GRID_VOXEL = 1 } lp_grid_kind;
  *   voxel:    data[0] = [H][W][D][K]; data[1], data[2] unused (may be NULL);
  *             h = trilinear sample.
  * Requirements: H, W, D >= 2; every data[] pointer 16-byte aligned;
- * elements per plane/volume < 2^31. Compiled K values: 8, 16, 32. */
+ * elements per plane/volume < 2^31. Compiled K values: 8, 16, 32.
+ * contraction / contract_scale: see lp_contraction; scale a in (0, 2]
+ * (ignored for LP_CONTRACT_NONE). */
 typedef struct {
   int32_t kind;           /* lp_grid_kind */
   int32_t H, W, D;
   int32_t K;
   const float* data[3];
+  int32_t contraction;    /* lp_contraction */
+  float contract_scale;   /* a */
 } lp_grid;
 
 /* The tiny MLP g: n_layers Linear layers, ReLU between them,
@@ -99,21 +112,25 @@ typedef struct {
 /* Forward render (Eq. 1). bg: [C] or NULL (= zeros).
  * out: [M][C], overwritten with v_i + T_iR bg.
  * tau_out: [M], overwritten with tau_iR = sum_j Delta_i sigma(x_ij) = -ln T_iR,
- * the one per-ray scalar the backward needs. */
+ * the one per-ray scalar the backward needs.
+ * depth_out: [M] or NULL; if given, overwritten with the expected depth
+ * sum_{j=1..R} (T_{i,j-1} - T_ij) t_ij, t_ij = near_i + j Delta_i (the "depths"
+ * feature of P:234 rendered like a colour channel; reading R26; no background
+ * term; the opacity is 1 - exp(-tau_out)). */
 lp_status lp_render_forward(const lp_grid* grid, const lp_mlp* mlp, const lp_rays* rays, const float* bg,
-                            float* out, float* tau_out, void* stream);
+                            float* out, float* tau_out, float* depth_out, void* stream);
 
 /* Backward (Eq. 3 by reverse marching) of the loss
- *   L = sum_i <grad_out_i, out_i> + grad_tau_i * tau_i
+ *   L = sum_i <grad_out_i, out_i> + grad_tau_i * tau_i + grad_depth_i * depth_i
  * w.r.t. theta and the MLP parameters. tau: [M] from lp_render_forward with the
- * same inputs. grad_out: [M][C]. grad_tau: [M] or NULL (= zeros).
+ * same inputs. grad_out: [M][C]. grad_tau, grad_depth: [M] or NULL (= zeros).
  * grad_data: same shapes as grid->data (grad_data[1..2] unused for voxels);
  * grad_params: same packing as mlp->params. Both are ACCUMULATED (+=) with
  * fp32 atomics (summation order nondeterministic); the caller zeroes them.
  * No gradient is produced for rays, near/far or bg. */
 lp_status lp_render_backward(const lp_grid* grid, const lp_mlp* mlp, const lp_rays* rays, const float* bg,
                              const float* tau, const float* grad_out, const float* grad_tau,
-                             float* const grad_data[3], float* grad_params, void* stream);
+                             const float* grad_depth, float* const grad_data[3], float* grad_params, void* stream);
 
 /* End-to-end training step from HOST buffers (the e2e measurement path).
  * rays_host, bg_host, grad_out_host, grad_tau_host (may be NULL) are HOST

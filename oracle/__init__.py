@@ -54,17 +54,18 @@ def lib():
             L.lpo_mlp_forward.argtypes = [i32, P, P, i64, P, P]
             L.lpo_mlp_backward.argtypes = [i32, P, P, i64, P, P, P, P]
             L.lpo_render_forward.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
-                                             P, P, P, P, i32, P, P, P]
+                                             P, P, P, P, i32, P, P, P, P, i32, f64]
             L.lpo_render_backward.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
-                                              P, P, P, P, i32, P, P, P, P, P, P, P, i32]
+                                              P, P, P, P, i32, P, P, P, P, P, P, P, i32, P, i32, f64]
             L.lpo_trace.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, P, P, f64, f64, i32,
-                                    P, P, P, P, P]
+                                    P, P, P, P, P, i32, f64]
             L.lpo_render_min_preact.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
-                                                P, P, P, P, i32, P]
+                                                P, P, P, P, i32, P, i32, f64]
             L.lpo_render_relu_slack.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
-                                                P, P, P, P, i32, P, P, P, f64, P, P, P, P]
+                                                P, P, P, P, i32, P, P, P, f64, P, P, P, P, P, i32, f64]
+            L.lpo_contract.argtypes = [i32, f64, i64, P, P]
             for f in (L.lpo_render_relu_slack, L.lpo_render_min_preact, L.lpo_sample, L.lpo_splat, L.lpo_mlp_forward, L.lpo_mlp_backward,
-                      L.lpo_render_forward, L.lpo_render_backward, L.lpo_trace):
+                      L.lpo_render_forward, L.lpo_render_backward, L.lpo_trace, L.lpo_contract):
                 f.restype = ctypes.c_int
             _lib = L
     return _lib
@@ -79,10 +80,15 @@ def _p(a: Optional[np.ndarray]):
 
 
 class Field:
-    """theta (list of planes or one voxel volume, channel-last) + packed MLP."""
+    """theta (list of planes or one voxel volume, channel-last) + packed MLP,
+    plus the scene contraction applied to sample points (0 none, 1 per-axis,
+    2 radial; scale a) -- lp_oracle.cpp contract()."""
 
-    def __init__(self, kind: int, grid: Sequence[np.ndarray], widths: Sequence[int], params: np.ndarray):
+    def __init__(self, kind: int, grid: Sequence[np.ndarray], widths: Sequence[int], params: np.ndarray,
+                 contraction: int = 0, contract_a: float = 1.0):
         self.kind = int(kind)
+        self.contraction = int(contraction)
+        self.contract_a = float(contract_a)
         self.grid = [_d(g) for g in grid]
         if self.kind == TRIPLANE:
             assert len(self.grid) == 3
@@ -105,6 +111,18 @@ class Field:
 
     def _geom(self):
         return (self.kind, self.H, self.W, self.D, self.K)
+
+    def _scene(self):
+        return (self.contraction, self.contract_a)
+
+
+def contract(contraction: int, a: float, x: np.ndarray) -> np.ndarray:
+    """CC(x) (Supp. Eq. contract) for points x[n][3]."""
+    x = _d(x).reshape(-1, 3)
+    out = np.zeros_like(x)
+    rc = lib().lpo_contract(int(contraction), float(a), len(x), _p(x), _p(out))
+    assert rc == 0
+    return out
 
 
 def sample(field: Field, x: np.ndarray) -> np.ndarray:
@@ -159,26 +177,30 @@ class Rays:
 
 
 def render_forward(field: Field, rays: Rays, bg=None, r0: int = 0, r1: Optional[int] = None,
-                   out=None, tau=None):
+                   out=None, tau=None, depth=None, return_depth: bool = False):
+    """Returns (out [n][C], tau [n]) and, with return_depth / a depth buffer, depth [n]."""
     r1 = rays.n if r1 is None else r1
     if out is None:
         out = np.zeros((rays.n, field.C))
     if tau is None:
         tau = np.zeros(rays.n)
+    if return_depth and depth is None:
+        depth = np.zeros(rays.n)
     bgd = None if bg is None else _d(bg)
     rc = lib().lpo_render_forward(*field._geom(), *field._planes(), field.n_layers, _p(field.widths),
                                   _p(field.params), r0, r1, _p(rays.o), _p(rays.d), _p(rays.near),
-                                  _p(rays.far), rays.S, _p(bgd), _p(out), _p(tau))
+                                  _p(rays.far), rays.S, _p(bgd), _p(out), _p(tau), _p(depth), *field._scene())
     assert rc == 0
-    return out, tau
+    return (out, tau) if depth is None else (out, tau, depth)
 
 
 def render_backward(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, mode: int = 0,
-                    r0: int = 0, r1: Optional[int] = None, grads=None):
+                    r0: int = 0, r1: Optional[int] = None, grads=None, grad_depth=None):
     """Returns (grad_grid list, grad_params); accumulates into `grads` if given."""
     r1 = rays.n if r1 is None else r1
     go = _d(grad_out).reshape(rays.n, field.C)
     gt = None if grad_tau is None else _d(grad_tau).reshape(rays.n)
+    gd = None if grad_depth is None else _d(grad_depth).reshape(rays.n)
     bgd = None if bg is None else _d(bg)
     if grads is None:
         grads = ([np.zeros_like(a) for a in field.grid], np.zeros_like(field.params))
@@ -186,7 +208,8 @@ def render_backward(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, 
     gp = [_p(a) for a in gg] + [None] * (3 - len(gg))
     rc = lib().lpo_render_backward(*field._geom(), *field._planes(), field.n_layers, _p(field.widths),
                                    _p(field.params), r0, r1, _p(rays.o), _p(rays.d), _p(rays.near),
-                                   _p(rays.far), rays.S, _p(bgd), _p(go), _p(gt), *gp, _p(gpar), mode)
+                                   _p(rays.far), rays.S, _p(bgd), _p(go), _p(gt), *gp, _p(gpar), mode, _p(gd),
+                                   *field._scene())
     assert rc == 0
     return gg, gpar
 
@@ -196,19 +219,20 @@ def min_preact(field: Field, rays: Rays) -> np.ndarray:
     out = np.zeros(rays.n)
     rc = lib().lpo_render_min_preact(*field._geom(), *field._planes(), field.n_layers, _p(field.widths),
                                      _p(field.params), 0, rays.n, _p(rays.o), _p(rays.d), _p(rays.near),
-                                     _p(rays.far), rays.S, _p(out))
+                                     _p(rays.far), rays.S, _p(out), *field._scene())
     assert rc == 0
     return out
 
 
 def relu_slack(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, band: float = 2e-5,
-               r0: int = 0, r1: Optional[int] = None, out=None):
+               r0: int = 0, r1: Optional[int] = None, out=None, grad_depth=None):
     """Elementwise bound of how much the gradients may change when any ReLU
     decision with |z| < band * scale is taken the other way (lp_oracle.cpp
     mlp_slack). Returns (slack_grid list, slack_params)."""
     r1 = rays.n if r1 is None else r1
     go = _d(grad_out).reshape(rays.n, field.C)
     gt = None if grad_tau is None else _d(grad_tau).reshape(rays.n)
+    gd = None if grad_depth is None else _d(grad_depth).reshape(rays.n)
     bgd = None if bg is None else _d(bg)
     if out is None:
         out = ([np.zeros_like(a) for a in field.grid], np.zeros_like(field.params))
@@ -216,18 +240,20 @@ def relu_slack(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, band:
     ptrs = [_p(a) for a in sg] + [None] * (3 - len(sg))
     rc = lib().lpo_render_relu_slack(*field._geom(), *field._planes(), field.n_layers, _p(field.widths),
                                      _p(field.params), r0, r1, _p(rays.o), _p(rays.d), _p(rays.near),
-                                     _p(rays.far), rays.S, _p(bgd), _p(go), _p(gt), float(band), *ptrs, _p(sp))
+                                     _p(rays.far), rays.S, _p(bgd), _p(go), _p(gt), float(band), *ptrs, _p(sp),
+                                     _p(gd), *field._scene())
     assert rc == 0
     return sg, sp
 
 
 def relu_slack_threaded(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, band: float = 2e-5,
-                        threads: int = 1):
+                        threads: int = 1, grad_depth=None):
     bounds = np.linspace(0, rays.n, threads + 1).astype(np.int64)
     parts = [([np.zeros_like(a) for a in field.grid], np.zeros_like(field.params)) for _ in range(threads)]
     ts = [threading.Thread(target=relu_slack, kwargs=dict(field=field, rays=rays, grad_out=grad_out,
                                                           grad_tau=grad_tau, bg=bg, band=band, r0=int(bounds[i]),
-                                                          r1=int(bounds[i + 1]), out=parts[i]))
+                                                          r1=int(bounds[i + 1]), out=parts[i],
+                                                          grad_depth=grad_depth))
           for i in range(threads)]
     for t in ts:
         t.start()
@@ -244,33 +270,36 @@ def trace(field: Field, origin, direction, near: float, far: float, S: int):
     c = np.zeros((S, field.C))
     rc = lib().lpo_trace(*field._geom(), *field._planes(), field.n_layers, _p(field.widths),
                          _p(field.params), _p(o), _p(d), float(near), float(far), S, _p(sigma), _p(tau),
-                         _p(T), _p(w), _p(c))
+                         _p(T), _p(w), _p(c), *field._scene())
     assert rc == 0
     return sigma, tau, T, w, c
 
 
-def render_forward_threaded(field: Field, rays: Rays, bg=None, threads: int = 1):
+def render_forward_threaded(field: Field, rays: Rays, bg=None, threads: int = 1, return_depth: bool = False):
     """Forward over disjoint contiguous ray ranges on `threads` host threads
-    (ctypes releases the GIL). Used only for the timed cpu baseline."""
+    (ctypes releases the GIL)."""
     out = np.zeros((rays.n, field.C))
     tau = np.zeros(rays.n)
+    depth = np.zeros(rays.n) if return_depth else None
     bounds = np.linspace(0, rays.n, threads + 1).astype(np.int64)
     ts = [threading.Thread(target=render_forward, args=(field, rays, bg, int(bounds[i]), int(bounds[i + 1]),
-                                                        out, tau)) for i in range(threads)]
+                                                        out, tau, depth)) for i in range(threads)]
     for t in ts:
         t.start()
     for t in ts:
         t.join()
-    return out, tau
+    return (out, tau) if depth is None else (out, tau, depth)
 
 
-def render_backward_threaded(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, threads: int = 1):
+def render_backward_threaded(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, threads: int = 1,
+                             grad_depth=None):
     """Backward with per-thread private gradient buffers, summed in thread order."""
     bounds = np.linspace(0, rays.n, threads + 1).astype(np.int64)
     parts = [([np.zeros_like(a) for a in field.grid], np.zeros_like(field.params)) for _ in range(threads)]
     ts = [threading.Thread(target=render_backward,
                            kwargs=dict(field=field, rays=rays, grad_out=grad_out, grad_tau=grad_tau, bg=bg,
-                                       r0=int(bounds[i]), r1=int(bounds[i + 1]), grads=parts[i]))
+                                       r0=int(bounds[i]), r1=int(bounds[i + 1]), grads=parts[i],
+                                       grad_depth=grad_depth))
           for i in range(threads)]
     for t in ts:
         t.start()

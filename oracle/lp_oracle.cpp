@@ -29,6 +29,8 @@ struct Field {
   int n_layers;    // number of Linear layers
   const int* widths;   // n_layers + 1 entries
   const double* params;  // W_0[w1][w0], b_0[w1], W_1[w2][w1], b_1[w2], ...
+  int contraction;     // 0 none, 1 per-axis, 2 radial (see contract())
+  double contract_a;   // scale a
 };
 
 struct Tap {
@@ -36,6 +38,34 @@ struct Tap {
   int64_t cell;    // index of the K-vector within its plane / volume
   double w;
 };
+
+// Scene contraction (Supp. Eq. "contract"):
+//   CC(x) = 0.5 * a x                                    if ||x|| <= 1
+//   CC(x) = 0.5 * ((2 - a)(1 - 1/||x||) + a) (x/||x||)   if ||x|| > 1
+// "We convert X, Y, Z axes into contract coordinates independently":
+// mode 1 applies the formula to each coordinate with ||x|| = |x_k| (reading
+// R25); mode 2 is the displayed Euclidean form. The contracted point is what
+// the hashing scheme samples; Delta stays the world distance (reading R25).
+double contract_1d(double x, double a) {
+  double n = std::fabs(x);
+  if (n <= 1.0) return 0.5 * (a * x);
+  return 0.5 * (((2.0 - a) * (1.0 - 1.0 / n) + a) * (x / n));
+}
+
+void contract(const Field& F, double x[3]) {
+  if (F.contraction == 1) {
+    for (int k = 0; k < 3; ++k) x[k] = contract_1d(x[k], F.contract_a);
+  } else if (F.contraction == 2) {
+    double n = std::sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+    const double a = F.contract_a;
+    if (n <= 1.0) {
+      for (int k = 0; k < 3; ++k) x[k] = 0.5 * (a * x[k]);
+    } else {
+      double s = (2.0 - a) * (1.0 - 1.0 / n) + a;
+      for (int k = 0; k < 3; ++k) x[k] = 0.5 * (s * (x[k] / n));
+    }
+  }
+}
 
 // O1: hashing scheme h (P:202 trilinear on voxels; P:207-210 bilinear on the
 // (x,y), (y,z), (z,x) planes, summed). World cube [-1,1]^3 -> index space
@@ -171,6 +201,7 @@ struct RayTrace {
   double delta;
   std::vector<std::vector<Tap>> taps;
   std::vector<MlpTrace> mlp;
+  std::vector<double> t;                  // t_j = near + j Delta (ray parameter of sample j)
   std::vector<double> sigma, tau, T, w;   // tau_j = sum_{n<=j} Delta sigma_n, T_j = exp(-tau_j)
   std::vector<std::vector<double>> c;     // colours c_j (C each)
 };
@@ -189,6 +220,7 @@ void trace_ray(const Field& F, const double* o, const double* d, double nearv, d
   rt.delta = (span > 0.0 ? span : 0.0) / (double)R;
   rt.taps.assign(S, {});
   rt.mlp.assign(S, {});
+  rt.t.assign(S, 0.0);
   rt.sigma.assign(S, 0.0);
   rt.tau.assign(S, 0.0);
   rt.T.assign(S, 0.0);
@@ -198,7 +230,9 @@ void trace_ray(const Field& F, const double* o, const double* d, double nearv, d
   double tau_prev = 0.0;
   for (int j = 0; j < S; ++j) {
     double t = nearv + (double)j * rt.delta;
+    rt.t[j] = t;
     double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+    contract(F, x);
     sample_taps(F, x, rt.taps[j]);
     gather(F, rt.taps[j], h.data());
     mlp_forward(F, h.data(), rt.mlp[j]);
@@ -213,7 +247,11 @@ void trace_ray(const Field& F, const double* o, const double* d, double nearv, d
   }
 }
 
-void finish_forward(const Field& F, const RayTrace& rt, const double* bg, double* out, double* tau_out) {
+// out = sum_{j>=1} w_j c_j + T_R bg; tau_out = tau_R; depth (optional, reading
+// R26: the "depths" feature of P:234 composited like a colour, no background
+// term) = sum_{j>=1} w_j t_j.
+void finish_forward(const Field& F, const RayTrace& rt, const double* bg, double* out, double* tau_out,
+                    double* depth_out) {
   const int C = F.widths[F.n_layers] - 1;
   const int R = rt.S - 1;
   for (int k = 0; k < C; ++k) {
@@ -222,12 +260,19 @@ void finish_forward(const Field& F, const RayTrace& rt, const double* bg, double
     out[k] = v + rt.T[R] * (bg ? bg[k] : 0.0);
   }
   *tau_out = rt.tau[R];
+  if (depth_out) {
+    double dep = 0.0;
+    for (int j = 1; j <= R; ++j) dep += rt.w[j] * rt.t[j];
+    *depth_out = dep;
+  }
 }
 
 void mlp_slack(const Field& F, const MlpTrace& tr, const double* dout, double band, double* slack_params,
                double* dh_slack);
 
-// O5 / O7: backward for one ray. Loss convention L = p.out + g_tau * tau_R.
+// O5 / O7: backward for one ray. Loss convention L = p.out + g_tau * tau_R
+// (+ g_depth * depth: the depth is one more composited channel whose per-sample
+// value t_j has no parameter dependence, so it only enters through a_j).
 // mode 0: Eq. 3 via suffix sums over the stored w_j a_j:
 //   dL/dsigma_q = -Delta (G_q - [q>=1] T_q a_q) + Delta g_tau,
 //   G_q = sum_{j>q} w_j a_j + T_R (p.bg),
@@ -235,7 +280,8 @@ void mlp_slack(const Field& F, const MlpTrace& tr, const double* dout, double ba
 // mode 1: literal derivative of Eq. 1 (O(S^2)):
 //   dout/dsigma_q = sum_{j>=1} (dT_{j-1}/dsigma_q - dT_j/dsigma_q) c_j + dT_R/dsigma_q bg,
 //   dT_j/dsigma_q = -Delta T_j [q <= j], T_{-1} = 1 (constant).
-void backward_ray(const Field& F, const RayTrace& rt, const double* bg, const double* p, double gtau, int mode,
+void backward_ray(const Field& F, const RayTrace& rt, const double* bg, const double* p, double gtau, double gdep,
+                  int mode,
                   double* const* grad_planes, double* grad_params, double band = 0.0,
                   double* const* slack_planes = nullptr, double* slack_params = nullptr) {
   const int C = F.widths[F.n_layers] - 1;
@@ -245,7 +291,7 @@ void backward_ray(const Field& F, const RayTrace& rt, const double* bg, const do
   for (int j = 0; j < S; ++j) {
     double s = 0.0;
     for (int k = 0; k < C; ++k) s += p[k] * rt.c[j][k];
-    a[j] = s;
+    a[j] = s + gdep * rt.t[j];
   }
   double b = 0.0;
   if (bg)
@@ -350,8 +396,11 @@ void mlp_slack(const Field& F, const MlpTrace& tr, const double* dout, double ba
 }
 
 Field make_field(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
-                 int n_layers, const int* widths, const double* params) {
+                 int n_layers, const int* widths, const double* params, int contraction = 0,
+                 double contract_a = 1.0) {
   Field F;
+  F.contraction = contraction;
+  F.contract_a = contract_a;
   F.kind = kind;
   F.H = H;
   F.W = W;
@@ -379,7 +428,19 @@ int check(int kind, int H, int W, int D, int K, int n_layers, const int* widths,
 
 extern "C" {
 
-int lpo_version(void) { return 1; }
+int lpo_version(void) { return 2; }
+
+// CC(x) for n points (contraction 1 = per-axis, 2 = radial), out[n][3].
+int lpo_contract(int contraction, double a, int64_t n, const double* x, double* out) {
+  if (contraction < 0 || contraction > 2) return 1;
+  Field F = make_field(0, 2, 2, 2, 1, nullptr, nullptr, nullptr, 0, nullptr, nullptr, contraction, a);
+  for (int64_t i = 0; i < n; ++i) {
+    double p[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};
+    contract(F, p);
+    for (int k = 0; k < 3; ++k) out[3 * i + k] = p[k];
+  }
+  return 0;
+}
 
 // h(x) for n points: h_out[n][K].
 int lpo_sample(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
@@ -438,14 +499,15 @@ int lpo_mlp_backward(int n_layers, const int* widths, const double* params, int6
 int lpo_render_forward(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
                        int n_layers, const int* widths, const double* params, int64_t r0, int64_t r1,
                        const double* origins, const double* dirs, const double* nearv, const double* farv, int S,
-                       const double* bg, double* out, double* tau_out) {
+                       const double* bg, double* out, double* tau_out, double* depth_out, int contraction,
+                       double contract_a) {
   if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
-  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params);
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a);
   const int C = widths[n_layers] - 1;
   RayTrace rt;
   for (int64_t r = r0; r < r1; ++r) {
     trace_ray(F, origins + 3 * r, dirs + 3 * r, nearv[r], farv[r], S, rt);
-    finish_forward(F, rt, bg, out + r * C, tau_out + r);
+    finish_forward(F, rt, bg, out + r * C, tau_out + r, depth_out ? depth_out + r : nullptr);
   }
   return 0;
 }
@@ -456,15 +518,17 @@ int lpo_render_backward(int kind, int H, int W, int D, int K, const double* p0, 
                         int n_layers, const int* widths, const double* params, int64_t r0, int64_t r1,
                         const double* origins, const double* dirs, const double* nearv, const double* farv, int S,
                         const double* bg, const double* grad_out, const double* grad_tau, double* g0, double* g1,
-                        double* g2, double* grad_params, int mode) {
+                        double* g2, double* grad_params, int mode, const double* grad_depth, int contraction,
+                        double contract_a) {
   if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
-  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params);
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a);
   const int C = widths[n_layers] - 1;
   double* g[3] = {g0, g1, g2};
   RayTrace rt;
   for (int64_t r = r0; r < r1; ++r) {
     trace_ray(F, origins + 3 * r, dirs + 3 * r, nearv[r], farv[r], S, rt);
-    backward_ray(F, rt, bg, grad_out + r * C, grad_tau ? grad_tau[r] : 0.0, mode, g, grad_params);
+    backward_ray(F, rt, bg, grad_out + r * C, grad_tau ? grad_tau[r] : 0.0, grad_depth ? grad_depth[r] : 0.0, mode,
+                 g, grad_params);
   }
   return 0;
 }
@@ -476,9 +540,9 @@ int lpo_render_relu_slack(int kind, int H, int W, int D, int K, const double* p0
                           int64_t r1, const double* origins, const double* dirs, const double* nearv,
                           const double* farv, int S, const double* bg, const double* grad_out,
                           const double* grad_tau, double band, double* s0, double* s1, double* s2,
-                          double* slack_params) {
+                          double* slack_params, const double* grad_depth, int contraction, double contract_a) {
   if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
-  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params);
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a);
   const int C = widths[n_layers] - 1;
   double* sg[3] = {s0, s1, s2};
   int64_t np = 0;
@@ -494,8 +558,8 @@ int lpo_render_relu_slack(int kind, int H, int W, int D, int K, const double* p0
   RayTrace rt;
   for (int64_t r = r0; r < r1; ++r) {
     trace_ray(F, origins + 3 * r, dirs + 3 * r, nearv[r], farv[r], S, rt);
-    backward_ray(F, rt, bg, grad_out + r * C, grad_tau ? grad_tau[r] : 0.0, 0, gptr, gp.data(), band, sg,
-                 slack_params);
+    backward_ray(F, rt, bg, grad_out + r * C, grad_tau ? grad_tau[r] : 0.0, grad_depth ? grad_depth[r] : 0.0, 0,
+                 gptr, gp.data(), band, sg, slack_params);
   }
   return 0;
 }
@@ -503,9 +567,10 @@ int lpo_render_relu_slack(int kind, int H, int W, int D, int K, const double* p0
 // Per-sample trace of one ray for invariant tests: sigma[S], tau[S], T[S], w[S], c[S][C].
 int lpo_trace(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
               int n_layers, const int* widths, const double* params, const double* origin, const double* dir,
-              double nearv, double farv, int S, double* sigma, double* tau, double* T, double* w, double* c) {
+              double nearv, double farv, int S, double* sigma, double* tau, double* T, double* w, double* c,
+              int contraction, double contract_a) {
   if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
-  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params);
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a);
   const int C = widths[n_layers] - 1;
   RayTrace rt;
   trace_ray(F, origin, dir, nearv, farv, S, rt);
@@ -528,9 +593,9 @@ int lpo_trace(int kind, int H, int W, int D, int K, const double* p0, const doub
 int lpo_render_min_preact(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
                           int n_layers, const int* widths, const double* params, int64_t r0, int64_t r1,
                           const double* origins, const double* dirs, const double* nearv, const double* farv, int S,
-                          double* min_rel) {
+                          double* min_rel, int contraction, double contract_a) {
   if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
-  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params);
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a);
   RayTrace rt;
   for (int64_t r = r0; r < r1; ++r) {
     trace_ray(F, origins + 3 * r, dirs + 3 * r, nearv[r], farv[r], S, rt);

@@ -14,6 +14,8 @@ LIB_PATH = os.environ.get("LP_LIB_PATH") or os.path.join(_HERE, "liblp_b200.so")
 
 LP_OK, LP_ERR_INVALID_ARG, LP_ERR_UNSUPPORTED, LP_ERR_MISALIGNED, LP_ERR_CUDA = range(5)
 LP_GRID_TRIPLANE, LP_GRID_VOXEL = 0, 1
+LP_CONTRACT_NONE, LP_CONTRACT_PER_AXIS, LP_CONTRACT_RADIAL = 0, 1, 2
+LP_ABI_VERSION = 2
 LP_MAX_LAYERS = 8
 _STATUS = {0: "LP_OK", 1: "LP_ERR_INVALID_ARG", 2: "LP_ERR_UNSUPPORTED", 3: "LP_ERR_MISALIGNED", 4: "LP_ERR_CUDA"}
 
@@ -24,7 +26,8 @@ EXPORTED = ("lp_render_forward", "lp_render_backward", "lp_fwd_bwd_host_workspac
 
 class LpGrid(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("H", ctypes.c_int32), ("W", ctypes.c_int32), ("D", ctypes.c_int32),
-                ("K", ctypes.c_int32), ("data", ctypes.c_void_p * 3)]
+                ("K", ctypes.c_int32), ("data", ctypes.c_void_p * 3), ("contraction", ctypes.c_int32),
+                ("contract_scale", ctypes.c_float)]
 
 
 class LpMlp(ctypes.Structure):
@@ -45,13 +48,13 @@ class LpError(RuntimeError):
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2404_19760_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2404_19760_b200/build.py` "
                           "(there is no CPU fallback)")
     L = ctypes.CDLL(LIB_PATH)
     P = ctypes.c_void_p
     gp, mp, rp = ctypes.POINTER(LpGrid), ctypes.POINTER(LpMlp), ctypes.POINTER(LpRays)
-    L.lp_render_forward.argtypes = [gp, mp, rp, P, P, P, P]
-    L.lp_render_backward.argtypes = [gp, mp, rp, P, P, P, P, ctypes.POINTER(ctypes.c_void_p), P, P]
+    L.lp_render_forward.argtypes = [gp, mp, rp, P, P, P, P, P]
+    L.lp_render_backward.argtypes = [gp, mp, rp, P, P, P, P, P, ctypes.POINTER(ctypes.c_void_p), P, P]
     L.lp_fwd_bwd_host_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int32]
     L.lp_fwd_bwd_host_workspace_bytes.restype = ctypes.c_size_t
     L.lp_render_fwd_bwd_host.argtypes = [gp, mp, rp, P, P, P, P, P, ctypes.POINTER(ctypes.c_void_p), P, P,
@@ -61,6 +64,8 @@ def _load():
     for f in (L.lp_render_forward, L.lp_render_backward, L.lp_render_fwd_bwd_host, L.lp_set_l2_persist,
               L.lp_abi_version):
         f.restype = ctypes.c_int
+    if L.lp_abi_version() != LP_ABI_VERSION:
+        raise ImportError(f"{LIB_PATH} has ABI {L.lp_abi_version()}, expected {LP_ABI_VERSION}: rebuild it")
     return L
 
 
@@ -72,9 +77,11 @@ def check(status: int):
         raise LpError(status, lib.lp_last_error().decode())
 
 
-def make_grid(kind: int, H: int, W: int, D: int, K: int, ptrs) -> LpGrid:
+def make_grid(kind: int, H: int, W: int, D: int, K: int, ptrs, contraction: int = 0,
+              contract_scale: float = 1.0) -> LpGrid:
     g = LpGrid()
     g.kind, g.H, g.W, g.D, g.K = kind, H, W, D, K
+    g.contraction, g.contract_scale = int(contraction), float(contract_scale)
     for i in range(3):
         g.data[i] = ptrs[i] if i < len(ptrs) else None
     return g

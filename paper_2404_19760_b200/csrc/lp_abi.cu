@@ -64,6 +64,10 @@ lp_status validate(const lp_grid* g, const lp_mlp* m, const lp_rays* r, Inst* in
   if (g->kind != LP_GRID_TRIPLANE && g->kind != LP_GRID_VOXEL) return fail(LP_ERR_INVALID_ARG, "bad grid kind %d", g->kind);
   if (g->H < 2 || g->W < 2 || g->D < 2) return fail(LP_ERR_INVALID_ARG, "grid dims must be >= 2 (got %d,%d,%d)", g->H, g->W, g->D);
   if (g->K < 1) return fail(LP_ERR_INVALID_ARG, "K must be >= 1");
+  if (g->contraction < LP_CONTRACT_NONE || g->contraction > LP_CONTRACT_RADIAL)
+    return fail(LP_ERR_INVALID_ARG, "bad contraction mode %d", g->contraction);
+  if (g->contraction != LP_CONTRACT_NONE && !(g->contract_scale > 0.0f && g->contract_scale <= 2.0f))
+    return fail(LP_ERR_INVALID_ARG, "contract_scale must be in (0, 2] (got %g)", (double)g->contract_scale);
   const int nplanes = g->kind == LP_GRID_TRIPLANE ? 3 : 1;
   for (int i = 0; i < nplanes; ++i) {
     if (!g->data[i]) return fail(LP_ERR_INVALID_ARG, "grid data[%d] is null", i);
@@ -161,6 +165,7 @@ lp::KernelArgs make_args(const lp_grid* g, const lp_mlp* m, const lp_rays* r, co
   a.M = r->n_rays;
   a.S = r->n_samples;
   a.bg = bg;
+  a.contract = lp::Contract{g->contraction, (double)g->contract_scale};
   return a;
 }
 
@@ -173,7 +178,7 @@ int lp_abi_version(void) { return LP_ABI_VERSION; }
 const char* lp_last_error(void) { return lpi::g_err.c_str(); }
 
 lp_status lp_render_forward(const lp_grid* grid, const lp_mlp* mlp, const lp_rays* rays, const float* bg, float* out,
-                            float* tau_out, void* stream) {
+                            float* tau_out, float* depth_out, void* stream) {
   Inst in;
   lp_status st = validate(grid, mlp, rays, &in);
   if (st != LP_OK) return st;
@@ -181,12 +186,13 @@ lp_status lp_render_forward(const lp_grid* grid, const lp_mlp* mlp, const lp_ray
   lp::KernelArgs a = make_args(grid, mlp, rays, bg);
   a.out = out;
   a.tau = tau_out;
+  a.depth = depth_out;
   return dispatch<true>(in, grid, a, static_cast<cudaStream_t>(stream));
 }
 
 lp_status lp_render_backward(const lp_grid* grid, const lp_mlp* mlp, const lp_rays* rays, const float* bg,
                              const float* tau, const float* grad_out, const float* grad_tau,
-                             float* const grad_data[3], float* grad_params, void* stream) {
+                             const float* grad_depth, float* const grad_data[3], float* grad_params, void* stream) {
   Inst in;
   lp_status st = validate(grid, mlp, rays, &in);
   if (st != LP_OK) return st;
@@ -203,6 +209,7 @@ lp_status lp_render_backward(const lp_grid* grid, const lp_mlp* mlp, const lp_ra
   a.tau = const_cast<float*>(tau);
   a.grad_out = grad_out;
   a.grad_tau = grad_tau;
+  a.grad_depth = grad_depth;
   return dispatch<false>(in, grid, a, static_cast<cudaStream_t>(stream));
 }
 
@@ -254,8 +261,8 @@ lp_status lp_render_fwd_bwd_host(const lp_grid* grid, const lp_mlp* mlp, const l
   dr.t_near = d_n;
   dr.t_far = d_f;
   const float* dbg = bg_host ? d_bg : nullptr;
-  if ((e = lp_render_forward(grid, mlp, &dr, dbg, d_out, d_tau, stream)) != LP_OK) return e;
-  if ((e = lp_render_backward(grid, mlp, &dr, dbg, d_tau, d_go, grad_tau_host ? d_gt : nullptr, grad_data,
+  if ((e = lp_render_forward(grid, mlp, &dr, dbg, d_out, d_tau, nullptr, stream)) != LP_OK) return e;
+  if ((e = lp_render_backward(grid, mlp, &dr, dbg, d_tau, d_go, grad_tau_host ? d_gt : nullptr, nullptr, grad_data,
                               grad_params, stream)) != LP_OK)
     return e;
   const auto D2H = cudaMemcpyDeviceToHost;

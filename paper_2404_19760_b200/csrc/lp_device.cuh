@@ -247,10 +247,59 @@ __device__ __forceinline__ RayIn load_ray(const float* __restrict__ orig, const 
   return ray;
 }
 
+__device__ __forceinline__ double ray_t(const RayIn& ray, int j) {
+  return __dadd_rn(ray.t0, __dmul_rn((double)j, ray.delta));
+}
+
 __device__ __forceinline__ void ray_point(const RayIn& ray, int j, double x[3]) {
-  const double t = __dadd_rn(ray.t0, __dmul_rn((double)j, ray.delta));
+  const double t = ray_t(ray, j);
 #pragma unroll
   for (int a = 0; a < 3; ++a) x[a] = __dadd_rn((double)ray.o[a], __dmul_rn(t, (double)ray.d[a]));
+}
+
+// ---------------------------------------------------------------- contraction
+// Supp. Eq. "contract", mapping an unbounded scene into the grid cube:
+//   CC(x) = 0.5 a x                                  if ||x|| <= 1
+//   CC(x) = 0.5 ((2 - a)(1 - 1/||x||) + a) x/||x||   otherwise,
+// foreground [-1,1] -> [-a/2, a/2]. mode 1: per axis, ||x|| -> |x_k|
+// ("convert X, Y, Z axes into contract coordinates independently", the
+// paper's choice; reading R25); mode 2: the displayed radial form. Applied to
+// the sample point before the hashing h (F2 -> F3); Delta stays the world
+// distance. fp64 with explicit rounding, in the oracle's operation order.
+struct Contract {
+  int mode;   // 0 none, 1 per-axis, 2 radial
+  double a;   // scale a in (0, 2]
+};
+
+__device__ __forceinline__ void contract_point(double x[3], const Contract& c) {
+  if (c.mode == 1) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double n = fabs(x[k]);
+      if (n <= 1.0) {
+        x[k] = __dmul_rn(0.5, __dmul_rn(c.a, x[k]));
+      } else {
+        const double s = __dadd_rn(__dmul_rn(__dsub_rn(2.0, c.a), __dsub_rn(1.0, __ddiv_rn(1.0, n))), c.a);
+        x[k] = __dmul_rn(0.5, __dmul_rn(s, __ddiv_rn(x[k], n)));
+      }
+    }
+  } else if (c.mode == 2) {
+    const double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1])), __dmul_rn(x[2], x[2])));
+    if (n <= 1.0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) x[k] = __dmul_rn(0.5, __dmul_rn(c.a, x[k]));
+    } else {
+      const double s = __dadd_rn(__dmul_rn(__dsub_rn(2.0, c.a), __dsub_rn(1.0, __ddiv_rn(1.0, n))), c.a);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) x[k] = __dmul_rn(0.5, __dmul_rn(s, __ddiv_rn(x[k], n)));
+    }
+  }
+}
+
+// F2 (+ optional contraction): the point the hashing scheme h samples for step j.
+__device__ __forceinline__ void sample_point(const RayIn& ray, int j, const Contract& c, double x[3]) {
+  ray_point(ray, j, x);
+  if (c.mode != 0) contract_point(x, c);
 }
 
 }  // namespace lp

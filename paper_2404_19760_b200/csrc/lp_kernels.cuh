@@ -34,6 +34,9 @@ struct KernelArgs {
   float* tau;            // fwd: out [M]; bwd: in [M]
   const float* grad_out; // bwd: [M][3]
   const float* grad_tau; // bwd: [M] or null
+  float* depth;          // fwd: [M] expected depth sum_j w_j t_j, or null
+  const float* grad_depth;  // bwd: [M] or null
+  Contract contract;     // sample-point contraction (mode 0 = none)
   unsigned long long* dbg;  // debug phase timers (LP_PHASES variant builds only), else null
 };
 
@@ -107,9 +110,10 @@ __global__ void __launch_bounds__(kThreads) lp_fwd_kernel(const KernelArgs a) {
     const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
     float tau = 0.0f, tau_e = 0.0f;  // tau_{j-1} as a compensated sum
     float v[kC] = {0.0f, 0.0f, 0.0f};
+    float dep = 0.0f;
     for (int j = 0; j <= R; ++j) {
       double x[3];
-      ray_point(ray, j, x);                 // F2
+      sample_point(ray, j, a.contract, x);  // F2
       Taps<KIND> tp;
       compute_taps<KIND, K>(x, a.dims, tp); // F3
       float h[K];
@@ -122,6 +126,7 @@ __global__ void __launch_bounds__(kThreads) lp_fwd_kernel(const KernelArgs a) {
         const float w = expf(-(tau + tau_e)) * (-expm1f(-ds));
 #pragma unroll
         for (int c = 0; c < kC; ++c) v[c] = fmaf(w, sigmoid_f(o[1 + c]), v[c]);
+        dep = fmaf(w, (float)ray_t(ray, j), dep);
       }
       two_sum_add(tau, tau_e, ds);
     }
@@ -130,6 +135,7 @@ __global__ void __launch_bounds__(kThreads) lp_fwd_kernel(const KernelArgs a) {
 #pragma unroll
     for (int c = 0; c < kC; ++c) a.out[3 * r + c] = fmaf(TR, bg[c], v[c]);  // F7
     a.tau[r] = tauR;
+    if (a.depth) a.depth[r] = dep;
   }
 }
 
@@ -212,6 +218,7 @@ __global__ void __launch_bounds__(kThreads, NH == 1 ? 2 : 1) lp_bwd_kernel(const
 #pragma unroll
     for (int c = 0; c < kC; ++c) p[c] = valid ? __ldg(a.grad_out + 3 * r + c) : 0.0f;
     const float gtau = (valid && a.grad_tau) ? __ldg(a.grad_tau + r) : 0.0f;
+    const float gdep = (valid && a.grad_depth) ? __ldg(a.grad_depth + r) : 0.0f;
     const float tauR = __ldg(a.tau + r);
     float pbg = 0.0f;
 #pragma unroll
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, NH == 1 ? 2 : 1) lp_bwd_kernel(const
     for (int q = R; q >= 0; --q) {
       // ---- B2: recompute sample q (F2-F5)
       double x[3];
-      ray_point(ray, q, x);
+      sample_point(ray, q, a.contract, x);
       Taps<KIND> tp;
       compute_taps<KIND, K>(x, a.dims, tp);
       float h[K];
@@ -243,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, NH == 1 ? 2 : 1) lp_bwd_kernel(const
       float aq = 0.0f;
 #pragma unroll
       for (int c = 0; c < kC; ++c) aq = fmaf(p[c], col[c], aq);
+      aq = fmaf(gdep, (float)ray_t(ray, q), aq);   // depth channel: "colour" t_q, no MLP gradient
       const float wq = q > 0 ? expf(-tau_qm1) * (-expm1f(-ds)) : 0.0f;
       const float Tq_aq = q > 0 ? expf(-tau_q) * aq : 0.0f;
       const float dsig = (float)ray.delta * (gtau - (G - Tq_aq));

@@ -160,9 +160,10 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tc2_kernel(const KernelArgs
     const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
     float tau = 0.0f, tau_e = 0.0f;
     float v[kC] = {0.0f, 0.0f, 0.0f};
+    float dep = 0.0f;
     for (int j = 0; j <= R; ++j) {
       double x[3];
-      ray_point(ray, j, x);                                                // F2
+      sample_point(ray, j, a.contract, x);                                                // F2
       write_taps<KIND, K>(taps + rt * NPL, x, a.dims);                     // F3 (cells)
       __syncwarp();
       coop_gather<KIND, K, KP, 3>(planes, taps, a.dims, X, L::H_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tc2_kernel(const KernelArgs
         const float w = expf(-(tau + tau_e)) * (-expm1f(-ds));
 #pragma unroll
         for (int c = 0; c < kC; ++c) v[c] = fmaf(w, sigmoid_f(o[1 + c]), v[c]);
+        dep = fmaf(w, (float)ray_t(ray, j), dep);
       }
       two_sum_add(tau, tau_e, ds);
     }
@@ -237,6 +239,7 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tc2_kernel(const KernelArgs
 #pragma unroll
       for (int c = 0; c < kC; ++c) a.out[3 * r + c] = fmaf(TR, bg[c], v[c]);
       a.tau[r] = tauR;
+      if (a.depth) a.depth[r] = dep;
     }
   }
   tc::fence_before_sync();
@@ -351,6 +354,7 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
 #pragma unroll
     for (int c = 0; c < kC; ++c) p[c] = valid ? __ldg(a.grad_out + 3 * r + c) : 0.0f;
     const float gtau = (valid && a.grad_tau) ? __ldg(a.grad_tau + r) : 0.0f;
+    const float gdep = (valid && a.grad_depth) ? __ldg(a.grad_depth + r) : 0.0f;
     const float tauR = __ldg(a.tau + r);
     float pbg = 0.0f;
 #pragma unroll
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
     for (int q = R; q >= 0; --q) {
       // ---- B2: recompute sample q (taps, gather fused with step q+1's scatter, Z1, Z2)
       double x[3];
-      ray_point(ray, q, x);
+      sample_point(ray, q, a.contract, x);
       write_taps<KIND, K>(taps + rt * NPL, x, a.dims);
       __syncwarp();
       if (pending)   // warp-uniform
@@ -438,6 +442,7 @@ __global__ void __launch_bounds__(256, 1) lp_bwd_tc2_kernel(const KernelArgs a) 
       float aq = 0.0f;
 #pragma unroll
       for (int c = 0; c < kC; ++c) aq = fmaf(p[c], col[c], aq);
+      aq = fmaf(gdep, (float)ray_t(ray, q), aq);   // depth channel: "colour" t_q, no MLP gradient
       const float wq_ = q > 0 ? expf(-tau_qm1) * (-expm1f(-ds)) : 0.0f;
       const float Tq_aq = q > 0 ? expf(-tau_q) * aq : 0.0f;
       const float dsig = (float)ray.delta * (gtau - (G_ - Tq_aq));

@@ -327,9 +327,10 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
     const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
     float tau = 0.0f, tau_e = 0.0f;
     float v[kC] = {0.0f, 0.0f, 0.0f};
+    float dep = 0.0f;
     for (int j = 0; j <= R; ++j) {
       double x[3];
-      ray_point(ray, j, x);                                        // F2
+      sample_point(ray, j, a.contract, x);                                        // F2
       write_taps<KIND, K>(taps + gt * S::NPL, x, a.dims);          // F3 (cells)
       __syncwarp();
       LP_PT(0)
@@ -368,6 +369,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
         const float w = expf(-(tau + tau_e)) * (-expm1f(-ds));
 #pragma unroll
         for (int c = 0; c < kC; ++c) v[c] = fmaf(w, sigmoid_f(o[1 + c]), v[c]);
+        dep = fmaf(w, (float)ray_t(ray, j), dep);
       }
       two_sum_add(tau, tau_e, ds);
       LP_PT(5)
@@ -378,6 +380,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
 #pragma unroll
       for (int c = 0; c < kC; ++c) a.out[3 * r + c] = fmaf(TR, bg[c], v[c]);
       a.tau[r] = tauR;
+      if (a.depth) a.depth[r] = dep;
     }
   }
   LP_PT_FLUSH(0)
@@ -479,6 +482,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
 #pragma unroll
     for (int c = 0; c < kC; ++c) p[c] = valid ? __ldg(a.grad_out + 3 * r + c) : 0.0f;
     const float gtau = (valid && a.grad_tau) ? __ldg(a.grad_tau + r) : 0.0f;
+    const float gdep = (valid && a.grad_depth) ? __ldg(a.grad_depth + r) : 0.0f;
     const float tauR = __ldg(a.tau + r);
     float pbg = 0.0f;
 #pragma unroll
@@ -489,7 +493,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
     for (int q = R; q >= 0; --q) {
       // ---- B2: recompute sample q: taps, cooperative gather, Z = H W0^T
       double x[3];
-      ray_point(ray, q, x);
+      sample_point(ray, q, a.contract, x);
       write_taps<KIND, K>(taps + gt * S::NPL, x, a.dims);
       __syncwarp();
       LP_PT(0)
@@ -538,6 +542,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       float aq = 0.0f;
 #pragma unroll
       for (int c = 0; c < kC; ++c) aq = fmaf(p[c], col[c], aq);
+      aq = fmaf(gdep, (float)ray_t(ray, q), aq);   // depth channel: "colour" t_q, no MLP gradient
       const float wq = q > 0 ? expf(-tau_qm1) * (-expm1f(-ds)) : 0.0f;
       const float Tq_aq = q > 0 ? expf(-tau_q) * aq : 0.0f;
       const float dsig = (float)ray.delta * (gtau - (G_ - Tq_aq));

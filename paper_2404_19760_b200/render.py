@@ -20,6 +20,9 @@ from . import _lib
 
 TRIPLANE = _lib.LP_GRID_TRIPLANE
 VOXEL = _lib.LP_GRID_VOXEL
+CONTRACT_NONE = _lib.LP_CONTRACT_NONE
+CONTRACT_PER_AXIS = _lib.LP_CONTRACT_PER_AXIS
+CONTRACT_RADIAL = _lib.LP_CONTRACT_RADIAL
 
 
 def _req(t: torch.Tensor, name: str, shape=None) -> torch.Tensor:
@@ -47,11 +50,14 @@ def _stream():
 @dataclass
 class Field:
     """theta (3 planes [H][W][K], [W][D][K], [D][H][K] or one volume [H][W][D][K])
-    plus the packed MLP parameters (include/lp.h)."""
+    plus the packed MLP parameters (include/lp.h). `contraction` / `contract_scale`
+    select the scene contraction of sample points (lp_contraction)."""
     kind: int
     planes: List[torch.Tensor]
     widths: Sequence[int]
     params: torch.Tensor
+    contraction: int = CONTRACT_NONE
+    contract_scale: float = 1.0
 
     def __post_init__(self):
         if self.kind == TRIPLANE:
@@ -79,7 +85,8 @@ class Field:
 
     def c_grid(self, planes=None) -> _lib.LpGrid:
         planes = self.planes if planes is None else planes
-        return _lib.make_grid(self.kind, self.H, self.W, self.D, self.K, [p.data_ptr() for p in planes])
+        return _lib.make_grid(self.kind, self.H, self.W, self.D, self.K, [p.data_ptr() for p in planes],
+                              self.contraction, self.contract_scale)
 
     def c_mlp(self, params=None) -> _lib.LpMlp:
         params = self.params if params is None else params
@@ -95,8 +102,10 @@ def _c_rays(origins, dirs, near, far, n_samples) -> _lib.LpRays:
     return _lib.make_rays(M, origins.data_ptr(), dirs.data_ptr(), near.data_ptr(), far.data_ptr(), int(n_samples))
 
 
-def render_forward(field: Field, origins, dirs, near, far, n_samples: int, bg=None, out=None, tau=None):
-    """Eq. 1 forward. Returns (out [M][C], tau [M])."""
+def render_forward(field: Field, origins, dirs, near, far, n_samples: int, bg=None, out=None, tau=None,
+                   depth=None, return_depth: bool = False):
+    """Eq. 1 forward. Returns (out [M][C], tau [M]), plus depth [M] (expected
+    depth sum_j w_j t_j) when return_depth or a `depth` buffer is given."""
     M = origins.shape[0]
     rays = _c_rays(origins, dirs, near, far, n_samples)
     if bg is not None:
@@ -105,14 +114,18 @@ def render_forward(field: Field, origins, dirs, near, far, n_samples: int, bg=No
     tau = torch.empty((M,), device=origins.device, dtype=torch.float32) if tau is None else tau
     _req(out, "out", (M, field.C))
     _req(tau, "tau", (M,))
+    if return_depth and depth is None:
+        depth = torch.empty((M,), device=origins.device, dtype=torch.float32)
+    if depth is not None:
+        _req(depth, "depth", (M,))
     g, m = field.c_grid(), field.c_mlp()
     _lib.check(_lib.lib.lp_render_forward(ctypes.byref(g), ctypes.byref(m), ctypes.byref(rays), _ptr(bg),
-                                          _ptr(out), _ptr(tau), _stream()))
-    return out, tau
+                                          _ptr(out), _ptr(tau), _ptr(depth), _stream()))
+    return (out, tau) if depth is None else (out, tau, depth)
 
 
 def render_backward(field: Field, origins, dirs, near, far, n_samples: int, tau, grad_out, grad_tau=None,
-                    bg=None, grad_planes=None, grad_params=None):
+                    bg=None, grad_planes=None, grad_params=None, grad_depth=None):
     """Eq. 3 backward. Accumulates into (and returns) grad_planes, grad_params."""
     M = origins.shape[0]
     rays = _c_rays(origins, dirs, near, far, n_samples)
@@ -120,6 +133,8 @@ def render_backward(field: Field, origins, dirs, near, far, n_samples: int, tau,
     _req(grad_out, "grad_out", (M, field.C))
     if grad_tau is not None:
         _req(grad_tau, "grad_tau", (M,))
+    if grad_depth is not None:
+        _req(grad_depth, "grad_depth", (M,))
     if bg is not None:
         _req(bg, "bg", (field.C,))
     if grad_planes is None:
@@ -132,39 +147,44 @@ def render_backward(field: Field, origins, dirs, near, far, n_samples: int, tau,
     g, m = field.c_grid(), field.c_mlp()
     gptr = _lib.ptr_array3([t.data_ptr() for t in grad_planes])
     _lib.check(_lib.lib.lp_render_backward(ctypes.byref(g), ctypes.byref(m), ctypes.byref(rays), _ptr(bg),
-                                           _ptr(tau), _ptr(grad_out), _ptr(grad_tau), gptr, _ptr(grad_params),
-                                           _stream()))
+                                           _ptr(tau), _ptr(grad_out), _ptr(grad_tau), _ptr(grad_depth), gptr,
+                                           _ptr(grad_params), _stream()))
     return grad_planes, grad_params
 
 
 class _RenderFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, kind, widths, n_samples, origins, dirs, near, far, bg, params, *planes):
-        field = Field(kind, list(planes), widths, params)
-        out, tau = render_forward(field, origins, dirs, near, far, n_samples, bg)
+    def forward(ctx, geom, n_samples, origins, dirs, near, far, bg, params, *planes):
+        kind, widths, contraction, cscale = geom
+        field = Field(kind, list(planes), widths, params, contraction, cscale)
+        out, tau, depth = render_forward(field, origins, dirs, near, far, n_samples, bg, return_depth=True)
         ctx.save_for_backward(origins, dirs, near, far, bg if bg is not None else torch.empty(0), params, tau,
                               *planes)
-        ctx.meta = (kind, widths, n_samples, bg is not None)
-        return out, tau
+        ctx.meta = (geom, n_samples, bg is not None)
+        return out, tau, depth
 
     @staticmethod
-    def backward(ctx, grad_out, grad_tau):
-        kind, widths, n_samples, has_bg = ctx.meta
+    def backward(ctx, grad_out, grad_tau, grad_depth):
+        (kind, widths, contraction, cscale), n_samples, has_bg = ctx.meta
         origins, dirs, near, far, bg, params, tau, *planes = ctx.saved_tensors
-        field = Field(kind, list(planes), widths, params)
+        field = Field(kind, list(planes), widths, params, contraction, cscale)
         go = grad_out.contiguous() if grad_out is not None else torch.zeros((origins.shape[0], field.C),
                                                                            device=origins.device)
         gt = grad_tau.contiguous() if grad_tau is not None else None
+        gd = grad_depth.contiguous() if grad_depth is not None else None
         gplanes, gparams = render_backward(field, origins, dirs, near, far, n_samples, tau, go, gt,
-                                           bg if has_bg else None)
-        return (None, None, None, None, None, None, None, None, gparams, *gplanes)
+                                           bg if has_bg else None, grad_depth=gd)
+        return (None, None, None, None, None, None, None, gparams, *gplanes)
 
 
-def render(field: Field, origins, dirs, near, far, n_samples: int, bg=None):
-    """Differentiable fused render: returns (out [M][C], tau [M]); gradients
-    flow to field.params and field.planes (not to rays, near/far or bg)."""
-    return _RenderFn.apply(field.kind, tuple(field.widths), int(n_samples), origins, dirs, near, far, bg,
-                           field.params, *field.planes)
+def render(field: Field, origins, dirs, near, far, n_samples: int, bg=None, return_depth: bool = False):
+    """Differentiable fused render: returns (out [M][C], tau [M]) -- and the
+    expected depth [M] with return_depth; gradients flow to field.params and
+    field.planes (not to rays, near/far or bg)."""
+    geom = (field.kind, tuple(field.widths), int(field.contraction), float(field.contract_scale))
+    out, tau, depth = _RenderFn.apply(geom, int(n_samples), origins, dirs, near, far, bg, field.params,
+                                      *field.planes)
+    return (out, tau, depth) if return_depth else (out, tau)
 
 
 def fwd_bwd_host(field: Field, origins_h, dirs_h, near_h, far_h, n_samples: int, grad_out_h, grad_tau_h=None,

@@ -17,7 +17,8 @@ def grid_np(cfg_name: str):
     return wl.make_grid(wl.get_config(cfg_name))
 
 
-def problem_np(cfg_name: str, idx=None, n: int = 2048, sigma_bias=None, with_gtau=True, zero_bg=False):
+def problem_np(cfg_name: str, idx=None, n: int = 2048, sigma_bias=None, with_gtau=True, zero_bg=False,
+               with_gdepth=False):
     cfg = wl.get_config(cfg_name)
     if idx is None:
         idx = wl.subset_indices(cfg, n)
@@ -26,7 +27,8 @@ def problem_np(cfg_name: str, idx=None, n: int = 2048, sigma_bias=None, with_gta
     return dict(
         cfg=cfg, idx=idx, grid=grid_np(cfg_name), params=wl.make_mlp(cfg.widths, sigma_bias=sigma_bias),
         o=o, d=d, near=near, far=far, bg=wl.make_bg(cfg.C, zero=zero_bg), go=wl.make_grad_out(idx, cfg.C),
-        gt=wl.make_grad_tau(idx) if with_gtau else None)
+        gt=wl.make_grad_tau(idx) if with_gtau else None,
+        gd=wl.make_grad_tau(idx, seed=6) if with_gdepth else None)
 
 
 def to_cuda(pb, device="cuda"):
@@ -34,15 +36,16 @@ def to_cuda(pb, device="cuda"):
     import paper_2404_19760_b200 as lpb
     cfg = pb["cfg"]
     T = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(device)
-    field = lpb.Field(cfg.kind, [T(g) for g in pb["grid"]], cfg.widths, T(pb["params"]))
+    field = lpb.Field(cfg.kind, [T(g) for g in pb["grid"]], cfg.widths, T(pb["params"]), cfg.contraction,
+                      cfg.contract_a)
     return field, dict(o=T(pb["o"]), d=T(pb["d"]), near=T(pb["near"]), far=T(pb["far"]), bg=T(pb["bg"]),
-                       go=T(pb["go"]), gt=T(pb["gt"]))
+                       go=T(pb["go"]), gt=T(pb["gt"]), gd=T(pb.get("gd")))
 
 
 def oracle_field(pb):
     import oracle
     cfg = pb["cfg"]
-    return oracle.Field(cfg.kind, pb["grid"], cfg.widths, pb["params"])
+    return oracle.Field(cfg.kind, pb["grid"], cfg.widths, pb["params"], cfg.contraction, cfg.contract_a)
 
 
 def oracle_rays(pb):
@@ -60,15 +63,19 @@ def oracle_rays(pb):
 RELU_BAND = 2e-5
 
 
-def oracle_reference(pb, grad=True, threads=8):
-    """Oracle forward (+ backward and ReLU slack) on a problem."""
+def oracle_reference(pb, grad=True, threads=8, depth=False):
+    """Oracle forward (+ backward and ReLU slack) on a problem; with depth, also the
+    expected depth and the grad_depth term (pb["gd"])."""
     import oracle
     F, R = oracle_field(pb), oracle_rays(pb)
-    out, tau = oracle.render_forward_threaded(F, R, pb["bg"], threads=threads)
-    res = dict(out=out, tau=tau)
+    res = dict(zip(("out", "tau", "depth"), oracle.render_forward_threaded(F, R, pb["bg"], threads=threads,
+                                                                          return_depth=depth)))
     if grad:
-        gg, gp = oracle.render_backward_threaded(F, R, pb["go"], pb["gt"], pb["bg"], threads=threads)
-        sg, sp = oracle.relu_slack_threaded(F, R, pb["go"], pb["gt"], pb["bg"], band=RELU_BAND, threads=threads)
+        gd = pb.get("gd")
+        gg, gp = oracle.render_backward_threaded(F, R, pb["go"], pb["gt"], pb["bg"], threads=threads,
+                                                 grad_depth=gd)
+        sg, sp = oracle.relu_slack_threaded(F, R, pb["go"], pb["gt"], pb["bg"], band=RELU_BAND, threads=threads,
+                                            grad_depth=gd)
         res.update(gplanes=gg, gparams=gp, splanes=sg, sparams=sp)
     return res
 
@@ -77,6 +84,8 @@ def parity_errors(g, r):
     """Parity errors of a GPU result against oracle_reference()."""
     from tests.helpers import rel_inf, rel_inf_slack
     errs = dict(out=rel_inf(g["out"], r["out"]), tau=rel_inf(g["tau"], r["tau"]))
+    if "depth" in g and "depth" in r:
+        errs["depth"] = rel_inf(g["depth"], r["depth"])
     if "gplanes" in g and "gplanes" in r:
         for i, (a, b, s) in enumerate(zip(g["gplanes"], r["gplanes"], r["splanes"])):
             errs[f"gplane{i}"] = rel_inf_slack(a, b, s)

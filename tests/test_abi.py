@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol(L):
     for name in declared:
         assert hasattr(L.lib, name), name
     assert set(declared) == set(L.EXPORTED)
-    assert L.lib.lp_abi_version() == 1
+    assert L.lib.lp_abi_version() == L.LP_ABI_VERSION == 2
 
 
 def _args(L, K=8, widths=(8, 16, 4), kind=0, ptr=0x1000, S=8, n=4):
@@ -38,12 +38,12 @@ def _args(L, K=8, widths=(8, 16, 4), kind=0, ptr=0x1000, S=8, n=4):
 
 def _fwd(L, g, m, r):
     p = ctypes.c_void_p(0x2000)
-    return L.lib.lp_render_forward(ctypes.byref(g), ctypes.byref(m), ctypes.byref(r), None, p, p, None)
+    return L.lib.lp_render_forward(ctypes.byref(g), ctypes.byref(m), ctypes.byref(r), None, p, p, None, None)
 
 
 def test_validation_errors(L):
     g, m, r = _args(L)
-    assert L.lib.lp_render_forward(None, ctypes.byref(m), ctypes.byref(r), None, None, None, None) == L.LP_ERR_INVALID_ARG
+    assert L.lib.lp_render_forward(None, ctypes.byref(m), ctypes.byref(r), None, None, None, None, None) == L.LP_ERR_INVALID_ARG
     assert "null" in L.lib.lp_last_error().decode()
     g, m, r = _args(L, S=1)
     assert _fwd(L, g, m, r) == L.LP_ERR_INVALID_ARG
@@ -58,6 +58,11 @@ def test_validation_errors(L):
     g, m, r = _args(L, widths=(8, 16, 32, 4))      # 3 layers with mismatched hidden widths
     assert _fwd(L, g, m, r) == L.LP_ERR_UNSUPPORTED
     assert L.lib.lp_set_l2_persist(ctypes.c_float(2.0)) == L.LP_ERR_INVALID_ARG
+    g, m, r = _args(L)
+    g.contraction = 3                              # unknown contraction mode
+    assert _fwd(L, g, m, r) == L.LP_ERR_INVALID_ARG
+    g.contraction, g.contract_scale = L.LP_CONTRACT_PER_AXIS, 2.5   # scale a outside (0, 2]
+    assert _fwd(L, g, m, r) == L.LP_ERR_INVALID_ARG and "contract_scale" in L.lib.lp_last_error().decode()
 
 
 def test_workspace_size(L):

@@ -28,14 +28,15 @@ def torch_cuda():
     return torch
 
 
-def _gpu_fwd_bwd(torch, pb, grad=True):
+def _gpu_fwd_bwd(torch, pb, grad=True, depth=False):
     import paper_2404_19760_b200 as lpb
     field, t = to_cuda(pb)
-    out, tau = lpb.render_forward(field, t["o"], t["d"], t["near"], t["far"], pb["cfg"].S, t["bg"])
-    res = dict(out=out.cpu().numpy(), tau=tau.cpu().numpy())
+    res = lpb.render_forward(field, t["o"], t["d"], t["near"], t["far"], pb["cfg"].S, t["bg"], return_depth=depth)
+    tau = res[1]
+    res = {k: v.cpu().numpy() for k, v in zip(("out", "tau", "depth"), res)}
     if grad:
         gpl, gpar = lpb.render_backward(field, t["o"], t["d"], t["near"], t["far"], pb["cfg"].S, tau, t["go"],
-                                        t["gt"], t["bg"])
+                                        t["gt"], t["bg"], grad_depth=t["gd"])
         res["gplanes"] = [g.cpu().numpy() for g in gpl]
         res["gparams"] = gpar.cpu().numpy()
     torch.cuda.synchronize()
@@ -53,6 +54,7 @@ def _compare(g, r, grad=True):
 def _assert(errs):
     print(errs)
     assert errs["out"] < TOL_IMG and errs["tau"] < TOL_IMG, errs
+    assert errs.get("depth", 0.0) < TOL_IMG, errs
     for k, v in errs.items():
         if k.startswith("g"):   # raw_* are reported, not asserted
             assert v < TOL_GRAD, errs
@@ -63,6 +65,29 @@ def test_parity_subset(torch_cuda, cfg, n):
     """F1-F7 and B1-B7 on every config: forward images/tau and all gradients."""
     pb = problem_np(cfg, n=n)
     _assert(_compare(_gpu_fwd_bwd(torch_cuda, pb), _oracle_fwd_bwd(pb)))
+
+
+# SURVEY 8(f) rows 3 and 4: scene contraction (P:768-776) and the expected-depth
+# output with its upstream gradient, on every kernel family: "cu" (the paper's
+# unbounded renderer setting, 3-layer MLP -> K1tc2/K2tc2), c1 / c4 (one hidden
+# layer -> K1tc/K2tc, triplane) and c2 (voxel).
+NEXT_CASES = [("cu", 256, {}), ("c1", 1024, dict(contraction=2, contract_a=1.5, near_far=(0.05, 9.0))),
+              ("c2", 256, dict(contraction=1, contract_a=0.7)), ("c4", 512, {}), ("c4p", 256, {})]
+
+
+@pytest.mark.parametrize("cfg,n,over", NEXT_CASES)
+def test_parity_depth_and_contraction(torch_cuda, cfg, n, over):
+    import dataclasses
+    pb = problem_np(cfg, n=n, with_gdepth=True)
+    if over:
+        pb["cfg"] = dataclasses.replace(pb["cfg"], **over)
+        if "near_far" in over:
+            pb["near"] = np.full_like(pb["near"], over["near_far"][0])
+            pb["far"] = np.full_like(pb["far"], over["near_far"][1])
+    g = _gpu_fwd_bwd(torch_cuda, pb, depth=True)
+    r = oracle_reference(pb, depth=True)
+    assert np.max(np.abs(r["depth"])) > 0.1
+    _assert(_compare(g, r))
 
 
 @pytest.mark.parametrize("sigma_bias,label", [(-30.0, "empty"), (60.0, "opaque"), (2.5, "dense")])
@@ -196,5 +221,27 @@ def test_autograd_render(torch_cuda):
     loss.backward()
     r = _oracle_fwd_bwd(pb)
     g = dict(out=out.detach().cpu().numpy(), tau=tau.detach().cpu().numpy(),
+             gplanes=[p.grad.cpu().numpy() for p in field.planes], gparams=field.params.grad.cpu().numpy())
+    _assert(_compare(g, r))
+
+
+def test_autograd_render_depth_contracted(torch_cuda):
+    """render(..., return_depth=True) on a contracted field: the depth output and its
+    upstream gradient flow through the autograd Function."""
+    import dataclasses
+
+    import paper_2404_19760_b200 as lpb
+    pb = problem_np("c1", n=2048, with_gdepth=True)
+    pb["cfg"] = dataclasses.replace(pb["cfg"], contraction=1, contract_a=1.2)
+    pb["far"] = pb["far"] * 3.0
+    field, t = to_cuda(pb)
+    field.params.requires_grad_(True)
+    for p in field.planes:
+        p.requires_grad_(True)
+    out, tau, depth = lpb.render(field, t["o"], t["d"], t["near"], t["far"], pb["cfg"].S, t["bg"], return_depth=True)
+    loss = (out * t["go"]).sum() + (tau * t["gt"]).sum() + (depth * t["gd"]).sum()
+    loss.backward()
+    r = oracle_reference(pb, depth=True)
+    g = dict(out=out.detach().cpu().numpy(), tau=tau.detach().cpu().numpy(), depth=depth.detach().cpu().numpy(),
              gplanes=[p.grad.cpu().numpy() for p in field.planes], gparams=field.params.grad.cpu().numpy())
     _assert(_compare(g, r))

@@ -19,6 +19,8 @@ Recipe:
 * near/far: per-ray slab intersection with the cube [-1+1e-4, 1-1e-4]^3, so
   every sample of a hitting ray lies in the grid's domain (the paper's
   contracted setting). Misses get near = far = 0 (Delta = 0).
+  Unbounded configs (near_far set, e.g. "cu") use one constant [near, far] for
+  every ray and let the scene contraction map the samples into the cube.
 * Grid theta: i.i.d. U(-0.5, 0.5), seed 0, per element index.
 * MLP: W_l ~ U(+-1/sqrt(d_{l-1})) seed 1 (S:160); hidden/colour biases 0;
   sigma bias softplus^-1(1.2) unless overridden.
@@ -87,6 +89,9 @@ class Config:
     img: int                  # square image side
     S: int                    # samples per ray = R + 1
     note: str = ""
+    contraction: int = 0      # scene contraction of sample points (0 none, 1 per-axis, 2 radial)
+    contract_a: float = 1.0   # contraction scale a
+    near_far: Optional[tuple] = None   # constant (near, far) for every ray (unbounded scenes)
 
     @property
     def n_rays(self) -> int:
@@ -130,6 +135,13 @@ CONFIGS = {
                   "c3 with the paper's 3-layer width-64 MLP"),
     "c4p": Config("c4p", TRIPLANE, 256, 32, (32, 64, 64, 4), 128, 256, 128,
                   "c4 with the paper's 3-layer width-64 MLP"),
+    # The paper's renderer setting for unbounded scenes: 160x160 triplanes,
+    # 3-layer width-64 MLP, 384 points per ray, 256x256 renders, contracted coordinates
+    # (per-axis, a = 1); rays run from near the camera to far behind the object.
+    "cu": Config("cu", TRIPLANE, 160, 32, (32, 64, 64, 4), 16, 256, 384,
+                 "unbounded scene: triplane 3x160x160 C=32, 3-layer MLP, 16 views at 256x256, "
+                 "384 samples/ray, per-axis contraction a=1", contraction=1, contract_a=1.0,
+                 near_far=(0.05, 12.0)),
 }
 
 
@@ -254,6 +266,10 @@ def make_rays(cfg: Config, idx: Optional[np.ndarray] = None, start: int = 0,
     d = xc[:, None] * B[:, 0] + yc[:, None] * B[:, 1] + B[:, 2]
     d /= np.linalg.norm(d, axis=1, keepdims=True)
     o = cams[view]
+    if cfg.near_far is not None:
+        near32 = np.full(len(idx), cfg.near_far[0], dtype=np.float32)
+        far32 = np.full(len(idx), cfg.near_far[1], dtype=np.float32)
+        return (o.astype(np.float32), d.astype(np.float32), near32, far32)
     # slab intersection with [-b, b]^3
     b = 1.0 - margin
     with np.errstate(divide="ignore", invalid="ignore"):
