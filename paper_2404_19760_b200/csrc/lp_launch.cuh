@@ -80,6 +80,9 @@ inline bool force_fma() {
 #ifndef LP_FWD_GROUPS
 #define LP_FWD_GROUPS 4
 #endif
+#ifndef LP_BWD_T
+#define LP_BWD_T 1
+#endif
 #ifndef LP_FWD2_GROUPS
 #define LP_FWD2_GROUPS 2
 #endif
@@ -116,9 +119,9 @@ lp_status run_bwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
   if constexpr (NH == 1) {
     if (!force_fma()) {
       static LaunchShape shape;
-      constexpr int G = kBwdGroups;
-      return launch(lp::lp_bwd_tc_kernel<KIND, K, HID, G>, shape, lp::BwdTcSmem<KIND, K, HID, G>::BYTES, 128 * G, G,
-                    a.M, a, w, s);
+      constexpr int G = kBwdGroups, T = LP_BWD_T;
+      return launch(lp::lp_bwd_tc_kernel<KIND, K, HID, G, T>, shape, lp::BwdTcSmem<KIND, K, HID, G, T>::BYTES,
+                    128 * T * G, G, a.M, a, w, s);
     }
   }
   if constexpr (NH == 2 && HID == 64 && K >= 8) {

@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
 }
 
 // ================================================================= K2tc backward
-template <int KIND, int K, int HID, int G>
+template <int KIND, int K, int HID, int G, int T>
 struct BwdTcSmem {
   using S = TcShape<KIND, K, HID>;
   static constexpr uint32_t W0P = 0;
@@ -403,8 +403,9 @@ struct BwdTcSmem {
   static constexpr uint32_t DA = H + 3 * S::HB_PIECE;          // [D1 | A1], 2 pieces; after the
                                                                // MMAs: fp32 dH staging + tap records
   static constexpr uint32_t PTAPS = DA + S::DA_PIECE;
-  static constexpr uint32_t TAPS = DA + 2 * S::DA_PIECE;
-  static constexpr uint32_t GSIZE = (TAPS + S::TAPS + 127) & ~127u;
+  static constexpr uint32_t TAPS = DA + 2 * S::DA_PIECE;      // [T halves][128][NPL]
+  static constexpr uint32_t XO = TAPS + T * S::TAPS;           // T = 2: [2][128] float4 partial outputs
+  static constexpr uint32_t GSIZE = (XO + (T == 2 ? 2 * 128 * 16 : 0) + 127) & ~127u;
   static constexpr uint32_t BAR = GRP + G * GSIZE;             // 2 mbarriers per group + tmem slot
   static constexpr uint32_t BYTES = BAR + 16 * G + 16;
   static constexpr uint32_t TMEM_COLS = G == 1 ? 256 : 512;
@@ -413,10 +414,17 @@ struct BwdTcSmem {
 
 // TMEM columns of a group (bwd): Z [0,64), dH [64,96), W [96,96+HC): M = 128 rows
 // [D1 units | A1 units] x [channels | 1 | dout] -> dW0, db0 (rows < 64), dWo^T (rows >= 64)
-template <int KIND, int K, int HID, int G>
-__global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs a) {
+// T threads per ray (1 or 2): with T = 2 thread (half, row) takes hidden units
+// [half*HID/2, (half+1)*HID/2) of every epilogue and half of the gather
+// iterations, as in lp_tc2_kernels.cuh; the halves exchange their partial
+// output-layer sums through shared memory.
+template <int KIND, int K, int HID, int G, int T>
+__global__ void __launch_bounds__(128 * T * G, 1) lp_bwd_tc_kernel(const KernelArgs a) {
   using S = TcShape<KIND, K, HID>;
-  using L = BwdTcSmem<KIND, K, HID, G>;
+  using L = BwdTcSmem<KIND, K, HID, G, T>;
+  constexpr int GT = 128 * T, HH = HID / T, KC = K / 4;
+  static_assert(T == 1 || T == 2, "threads per ray");
+  static_assert(HH % 8 == 0 && KC % T == 0, "per-half split");
   using F = TcParams<K, HID>;
   using P = PackedParams<K, HID, 1>;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -425,16 +433,19 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 16 * G);
 
-  const int g = threadIdx.x >> 7, gt = threadIdx.x & 127, wg = gt >> 5, lane = gt & 31;
+  const int g = threadIdx.x / GT, gt = threadIdx.x % GT, hf = gt >> 7, rt = gt & 127;
+  const int wg = (gt >> 5) & 3, lane = gt & 31;
+  const int it0 = hf * (KC / T), it1 = it0 + KC / T;
   uint8_t* gsm = smem + L::GRP + g * L::GSIZE;
   uint8_t* Ht = gsm + L::H;
   uint8_t* DAt = gsm + L::DA;
+  float4* xo = reinterpret_cast<float4*>(gsm + L::XO);
   // fp32 dH rows and tap records of the previous step (its scatter is fused into the
   // next gather): DA tile, free between the MMA2 completion and the next epilogue
   float* dhs = reinterpret_cast<float*>(gsm + L::DA);
   float4* ptaps = reinterpret_cast<float4*>(gsm + L::PTAPS);
   bool pending = false;
-  float4* taps = reinterpret_cast<float4*>(gsm + L::TAPS);
+  float4* taps = reinterpret_cast<float4*>(gsm + L::TAPS) + hf * 128 * S::NPL;
 
   for (uint32_t i = threadIdx.x * 16; i < L::BAR; i += blockDim.x * 16)
     *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
@@ -450,7 +461,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   const uint32_t tbase = *tslot + (uint32_t)(g * 256);
   const uint32_t tZ = tbase, tDH = tbase + 64, tW = tbase + 96;
   // ones column of the H tile (piece 0 = 1, pieces 1, 2 = 0; written once, never overwritten)
-  *reinterpret_cast<__nv_bfloat16*>(Ht + tc::cm_off(gt, S::KP, S::HC)) = __float2bfloat16_rn(1.0f);
+  if (hf == 0) *reinterpret_cast<__nv_bfloat16*>(Ht + tc::cm_off(rt, S::KP, S::HC)) = __float2bfloat16_rn(1.0f);
   tc::fence_async_smem();
   const uint32_t tlane = (uint32_t)(wg * 32) << 16;
   uint64_t* bar_z = &bars[2 * g];
@@ -474,7 +485,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
 
   const int64_t ntiles = (a.M + 127) / 128;
   for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
-    const int64_t r0 = tile * 128 + gt;
+    const int64_t r0 = tile * 128 + rt;
     const bool valid = r0 < a.M;
     const int64_t r = valid ? r0 : a.M - 1;   // tail rows march a real ray with zero upstream
     const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
@@ -494,20 +505,22 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       // ---- B2: recompute sample q: taps, cooperative gather, Z = H W0^T
       double x[3];
       sample_point(ray, q, a.contract, x);
-      write_taps<KIND, K>(taps + gt * S::NPL, x, a.dims);
+      write_taps<KIND, K>(taps + rt * S::NPL, x, a.dims);
       __syncwarp();
       LP_PT(0)
 #ifndef LP_ABL_NOGATHER
       if (pending)   // warp-uniform
-        coop_gather<KIND, K, S::HC, 3, true>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, gplanes, ptaps, dhs);
+        coop_gather<KIND, K, S::HC, 3, true>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, gplanes, ptaps, dhs,
+                                             it0, it1);
       else
-        coop_gather<KIND, K, S::HC, 3>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane);
+        coop_gather<KIND, K, S::HC, 3>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, nullptr, nullptr,
+                                       nullptr, it0, it1);
       pending = false;
 #endif
       LP_PT(1)
       tc::fence_async_smem();
       tc::fence_before_sync();
-      tc::named_bar(1 + g, 128);
+      tc::named_bar(1 + g, GT);
       LP_PT(2)
       if (gt == 0) {
         tc::fence_after_sync();
@@ -526,10 +539,31 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       tc::mbar_wait(bar_z, phase);
       LP_PT(3)
       tc::fence_after_sync();
-      float a1[HID];
-      tc::tmem_ld<HID>(tZ + tlane, a1);
+      float a1[HH];
+      tc::tmem_ld<HH>(tZ + tlane + (uint32_t)(hf * HH), a1);
       float o[kOut];
-      tc_head_layer<HID>(fp + F::B0, fp + F::WOT, fp + F::BO, a1, o);   // a1 = relu(z + b0)
+      if constexpr (T == 1) {
+        tc_head_layer<HID>(fp + F::B0, fp + F::WOT, fp + F::BO, a1, o);   // a1 = relu(z + b0)
+      } else {   // this half's units: a1 = relu(z + b0), partial output layer, exchange
+        float4 part = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+        for (int i = 0; i < HH; ++i) {
+          a1[i] = fmaxf(a1[i] + fp[F::B0 + hf * HH + i], 0.0f);
+          const float4 w = reinterpret_cast<const float4*>(fp + F::WOT)[hf * HH + i];
+          part.x = fmaf(w.x, a1[i], part.x);
+          part.y = fmaf(w.y, a1[i], part.y);
+          part.z = fmaf(w.z, a1[i], part.z);
+          part.w = fmaf(w.w, a1[i], part.w);
+        }
+        xo[hf * 128 + rt] = part;
+        tc::fence_before_sync();
+        tc::named_bar(1 + g, GT);
+        const float4 p0 = xo[rt], p1 = xo[128 + rt];
+        o[0] = fp[F::BO + 0] + p0.x + p1.x;
+        o[1] = fp[F::BO + 1] + p0.y + p1.y;
+        o[2] = fp[F::BO + 2] + p0.z + p1.z;
+        o[3] = fp[F::BO + 3] + p0.w + p1.w;
+      }
       const float s_sig = sigmoid_f(o[0]);
       const float ds = (float)ray.delta * softplus_f(o[0]);
       float col[kC];
@@ -555,28 +589,30 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
 #pragma unroll
       for (int c = 4; c < 8; ++c) dout[c] = 0.0f;
       // ---- B5: per 8-unit chunk: stage a1, delta1 = ReLU'(z) (Wo^T dout), stage delta1
+      if (hf == 0) {
 #pragma unroll
-      for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
+        for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
+        tc::store8<2>(Ht, S::HB_PIECE, rt, S::KP + 8, S::HC, dout);
+      }
 #pragma unroll
-      for (int c = 0; c < HID / 8; ++c) {
-        tc::store8<2>(DAt, S::DA_PIECE, gt, S::HP + 8 * c, 2 * S::HP, a1 + 8 * c);
+      for (int c = 0; c < HH / 8; ++c) {
+        tc::store8<2>(DAt, S::DA_PIECE, rt, S::HP + hf * HH + 8 * c, 2 * S::HP, a1 + 8 * c);
         float d1[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const float4 w = reinterpret_cast<const float4*>(fp + F::WOT)[8 * c + u];
+          const float4 w = reinterpret_cast<const float4*>(fp + F::WOT)[hf * HH + 8 * c + u];
           float sacc = w.x * dout[0];
           sacc = fmaf(w.y, dout[1], sacc);
           sacc = fmaf(w.z, dout[2], sacc);
           sacc = fmaf(w.w, dout[3], sacc);
           d1[u] = a1[8 * c + u] > 0.0f ? sacc : 0.0f;
         }
-        tc::store8<2>(DAt, S::DA_PIECE, gt, 8 * c, 2 * S::HP, d1);
+        tc::store8<2>(DAt, S::DA_PIECE, rt, hf * HH + 8 * c, 2 * S::HP, d1);
       }
-      tc::store8<2>(Ht, S::HB_PIECE, gt, S::KP + 8, S::HC, dout);
       LP_PT(4)
       tc::fence_async_smem();
       tc::fence_before_sync();
-      tc::named_bar(1 + g, 128);
+      tc::named_bar(1 + g, GT);
       if (gt == 0) {
         tc::fence_after_sync();
         constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
@@ -604,27 +640,32 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
       tc::fence_after_sync();
       // ---- B6: dH row -> fp32 staging -> cooperative scatter
       {
-        float dh[S::KP];
-        tc::tmem_ld<S::KP>(tDH + tlane, dh);
+        constexpr int HK = S::KP / T;   // this thread's dH columns
+        float dh[HK];
+        tc::tmem_ld<HK>(tDH + tlane + (uint32_t)(hf * HK), dh);
 #pragma unroll
-        for (int k4 = 0; k4 < K / 4; ++k4)
-          *reinterpret_cast<float4*>(dhs + gt * (K + 4) + 4 * k4) =
-              make_float4(dh[4 * k4], dh[4 * k4 + 1], dh[4 * k4 + 2], dh[4 * k4 + 3]);
+        for (int k4 = 0; k4 < HK / 4; ++k4)
+          if (hf * HK + 4 * k4 < K)
+            *reinterpret_cast<float4*>(dhs + rt * (K + 4) + hf * HK + 4 * k4) =
+                make_float4(dh[4 * k4], dh[4 * k4 + 1], dh[4 * k4 + 2], dh[4 * k4 + 3]);
       }
       tc::fence_before_sync();
       // keep this step's tap records for its scatter, fused into the next gather
+      if (hf == 0) {
 #pragma unroll
-      for (int pp = 0; pp < S::NPL; ++pp) ptaps[gt * S::NPL + pp] = taps[gt * S::NPL + pp];
+        for (int pp = 0; pp < S::NPL; ++pp) ptaps[rt * S::NPL + pp] = taps[rt * S::NPL + pp];
+      }
 #ifndef LP_ABL_NOSCATTER   // ablation hooks (timing experiments only; results are wrong when set)
       pending = true;
 #endif
-      __syncwarp();
+      if constexpr (T == 1) __syncwarp();
+      else tc::named_bar(1 + g, GT);   // the other half's warps read these rows
       LP_PT(6)
     }
   }
   if (pending) {   // the last step's scatter
     __syncwarp();
-    coop_scatter<KIND, K>(gplanes, ptaps, a.dims, dhs, wg * 32, lane);
+    coop_scatter<KIND, K>(gplanes, ptaps, a.dims, dhs, wg * 32, lane, it0, it1);
     __syncwarp();
   }
   LP_PT_FLUSH(1)
@@ -632,7 +673,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
   // ---- B7: flush this group's gradient partials (TMEM accumulators + register bias sums)
   tc::fence_after_sync();
   const bool had_tiles = (int64_t)blockIdx.x * G + g < ntiles;
-  {
+  if (hf == 0) {
     // M = 128 accumulator: row i lives in TMEM lane i (warp i / 32); rows [0, HP) are
     // hidden units of D1 (dW0, db0), rows [HP, 2 HP) hidden units of A1 (dWo^T)
     float wrow[S::HC];
@@ -647,17 +688,17 @@ __global__ void __launch_bounds__(128 * G, 1) lp_bwd_tc_kernel(const KernelArgs 
 #pragma unroll
       for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + (row - S::HP), wrow[S::KP + 8 + rr]);
     }
-  }
 #pragma unroll
-  for (int i = 0; i < kOut; ++i) {
-    float s = dbo[i];
+    for (int i = 0; i < kOut; ++i) {
+      float s = dbo[i];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    dbo[i] = s;
-  }
-  if (lane == 0 && had_tiles) {
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      dbo[i] = s;
+    }
+    if (lane == 0 && had_tiles) {
 #pragma unroll
-    for (int i = 0; i < kOut; ++i) atomicAdd(a.gparams + P::BO + i, dbo[i]);
+      for (int i = 0; i < kOut; ++i) atomicAdd(a.gparams + P::BO + i, dbo[i]);
+    }
   }
   tc::fence_before_sync();
   __syncthreads();
