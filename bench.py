@@ -157,7 +157,7 @@ def cpu_oracle_rate(cfg, target_s: float, threads: int):
     from tests.gpu_problem import grid_np
     grid = grid_np(cfg.name)
     params = wl.make_mlp(cfg.widths)
-    F = oracle.Field(cfg.kind, grid, cfg.widths, params)
+    F = oracle.Field(cfg.kind, grid, cfg.widths, params, cfg.contraction, cfg.contract_a)
     n = max(threads, 8)
     total_rays, total_t = 0, 0.0
     idx_all = wl.subset_indices(cfg, 1 << 16)
@@ -249,7 +249,7 @@ def run_ours(args):
     grid = wl.make_grid(cfg)
     params = torch.from_numpy(wl.make_mlp(cfg.widths)).to(dev)
     planes = [torch.from_numpy(g).to(dev) for g in grid]
-    field = lpb.Field(cfg.kind, planes, cfg.widths, params)
+    field = lpb.Field(cfg.kind, planes, cfg.widths, params, cfg.contraction, cfg.contract_a)
     grads = FlatGrads([p.shape for p in planes] + [params.shape], device=dev)
     flat = grads.flat
     gplanes, gparams = grads.views[:-1], grads.views[-1]
