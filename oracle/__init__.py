@@ -64,8 +64,14 @@ def lib():
             L.lpo_render_relu_slack.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
                                                 P, P, P, P, i32, P, P, P, f64, P, P, P, P, P, i32, f64]
             L.lpo_contract.argtypes = [i32, f64, i64, P, P]
+            L.lpo_splat_rays.argtypes = [i32, i32, i32, i32, i32, i64, i64, P, P, P, P, i32, P, P, P, P, P, P, P,
+                                         i32, f64]
+            L.lpo_splat_normalize.argtypes = [i64, i32, P, P, P]
+            L.lpo_splat_rays_backward.argtypes = [i32, i32, i32, i32, i32, i64, i64, P, P, P, P, i32, P, P, P,
+                                                  P, P, P, P, i32, f64]
             for f in (L.lpo_render_relu_slack, L.lpo_render_min_preact, L.lpo_sample, L.lpo_splat, L.lpo_mlp_forward, L.lpo_mlp_backward,
-                      L.lpo_render_forward, L.lpo_render_backward, L.lpo_trace, L.lpo_contract):
+                      L.lpo_render_forward, L.lpo_render_backward, L.lpo_trace, L.lpo_contract,
+                      L.lpo_splat_rays, L.lpo_splat_normalize, L.lpo_splat_rays_backward):
                 f.restype = ctypes.c_int
             _lib = L
     return _lib
@@ -308,3 +314,91 @@ def render_backward_threaded(field: Field, rays: Rays, grad_out, grad_tau=None, 
     gg = [sum(p[0][k] for p in parts) for k in range(len(field.grid))]
     gp = sum(p[1] for p in parts)
     return gg, gp
+
+
+# ---------------------------------------------------------------- Splatter
+class GridSpec:
+    """Shape of a splat target: kind, (H, W, D), K channels, scene contraction."""
+
+    def __init__(self, kind: int, dims, K: int, contraction: int = 0, contract_a: float = 1.0):
+        self.kind, self.K = int(kind), int(K)
+        self.H, self.W, self.D = (int(v) for v in dims)
+        self.contraction, self.contract_a = int(contraction), float(contract_a)
+
+    def shapes(self, K=None):
+        K = self.K if K is None else K
+        H, W, D = self.H, self.W, self.D
+        return [(H, W, K), (W, D, K), (D, H, K)] if self.kind == TRIPLANE else [(H, W, D, K)]
+
+    def _geom(self, K=None):
+        return (self.kind, self.H, self.W, self.D, self.K if K is None else K)
+
+
+def _ptr3(arrs):
+    return [_p(a) for a in arrs] + [None] * (3 - len(arrs))
+
+
+def splat_rays(spec: GridSpec, rays: Rays, features, r0: int = 0, r1: Optional[int] = None, acc=None):
+    """Unnormalised splat of the rays' features and of the weights: returns
+    (theta list, theta_weight list), accumulating into `acc` if given."""
+    r1 = rays.n if r1 is None else r1
+    v = _d(features).reshape(rays.n, spec.K)
+    if acc is None:
+        acc = ([np.zeros(s) for s in spec.shapes()], [np.zeros(s) for s in spec.shapes(1)])
+    th, wt = acc
+    rc = lib().lpo_splat_rays(*spec._geom(), r0, r1, _p(rays.o), _p(rays.d), _p(rays.near), _p(rays.far),
+                              rays.S, _p(v), *_ptr3(th), *_ptr3(wt), spec.contraction, spec.contract_a)
+    assert rc == 0
+    return th, wt
+
+
+def splat_normalize(theta, theta_weight):
+    out = []
+    for t, w in zip(theta, theta_weight):
+        o = np.zeros_like(t)
+        rc = lib().lpo_splat_normalize(int(w.size), int(t.shape[-1]), _p(_d(t)), _p(_d(w)), _p(o))
+        assert rc == 0
+        out.append(o)
+    return out
+
+
+def splat_forward(spec: GridSpec, rays: Rays, features, threads: int = 1):
+    """Splatter forward: (normalised theta, theta, theta_weight)."""
+    bounds = np.linspace(0, rays.n, threads + 1).astype(np.int64)
+    parts = [([np.zeros(s) for s in spec.shapes()], [np.zeros(s) for s in spec.shapes(1)]) for _ in range(threads)]
+    ts = [threading.Thread(target=splat_rays, args=(spec, rays, features, int(bounds[i]), int(bounds[i + 1]),
+                                                    parts[i])) for i in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    th = [sum(p[0][k] for p in parts) for k in range(len(parts[0][0]))]
+    wt = [sum(p[1][k] for p in parts) for k in range(len(parts[0][1]))]
+    return splat_normalize(th, wt), th, wt
+
+
+def splat_backward(spec: GridSpec, rays: Rays, grad_out, theta_weight, r0: int = 0, r1: Optional[int] = None,
+                   out=None):
+    """dL/d(features) [n][K] of the normalised splat (theta_weight treated as constant)."""
+    r1 = rays.n if r1 is None else r1
+    g = [_d(a) for a in grad_out]
+    w = [_d(a) for a in theta_weight]
+    if out is None:
+        out = np.zeros((rays.n, spec.K))
+    rc = lib().lpo_splat_rays_backward(*spec._geom(), r0, r1, _p(rays.o), _p(rays.d), _p(rays.near),
+                                       _p(rays.far), rays.S, *_ptr3(g), *_ptr3(w), _p(out), spec.contraction,
+                                       spec.contract_a)
+    assert rc == 0
+    return out
+
+
+def splat_backward_threaded(spec: GridSpec, rays: Rays, grad_out, theta_weight, threads: int = 1):
+    out = np.zeros((rays.n, spec.K))
+    bounds = np.linspace(0, rays.n, threads + 1).astype(np.int64)
+    ts = [threading.Thread(target=splat_backward, args=(spec, rays, grad_out, theta_weight, int(bounds[i]),
+                                                        int(bounds[i + 1]), out)) for i in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return out

@@ -564,6 +564,91 @@ int lpo_render_relu_slack(int kind, int H, int W, int D, int K, const double* p0
   return 0;
 }
 
+// ---------------------------------------------------------------- Splatter
+// Each pixel ray i expands into the same R+1 equispaced points as the renderer
+// ("R+1 equispaced 3D points", points inheriting the pixel's feature v_i)
+// and pushes v_i into theta with the sampling weights of h ("the splatting
+// weights are the same as the sampling weights used in rendering"),
+// while a second pass pushes the scalar 1 into theta_weight. The
+// result is theta / theta_weight, 0 where no weight landed (reading
+// R27). The MLP g_s of Eq. 2 is disabled, as in the paper's benchmark.
+// Accumulates theta_acc[cells][K] and weight_acc[cells][1] (+=) for rays [r0, r1).
+int lpo_splat_rays(int kind, int H, int W, int D, int K, int64_t r0, int64_t r1, const double* origins,
+                   const double* dirs, const double* nearv, const double* farv, int S, const double* features,
+                   double* t0, double* t1, double* t2, double* w0, double* w1, double* w2, int contraction,
+                   double contract_a) {
+  int wd[2] = {K, 2};
+  if (check(kind, H, W, D, K, 1, wd, S)) return 1;
+  Field F = make_field(kind, H, W, D, K, nullptr, nullptr, nullptr, 0, nullptr, nullptr, contraction, contract_a);
+  Field F1 = make_field(kind, H, W, D, 1, nullptr, nullptr, nullptr, 0, nullptr, nullptr, contraction, contract_a);
+  double* tg[3] = {t0, t1, t2};
+  double* wg[3] = {w0, w1, w2};
+  const double one = 1.0;
+  const int R = S - 1;
+  std::vector<Tap> taps;
+  for (int64_t r = r0; r < r1; ++r) {
+    const double* o = origins + 3 * r;
+    const double* d = dirs + 3 * r;
+    double span = farv[r] - nearv[r];
+    double delta = (span > 0.0 ? span : 0.0) / (double)R;
+    for (int j = 0; j < S; ++j) {
+      double t = nearv[r] + (double)j * delta;
+      double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+      contract(F, x);
+      sample_taps(F, x, taps);
+      scatter(F, taps, features + r * K, tg);     // pass 1: the pixel feature
+      scatter(F1, taps, &one, wg);                // pass 2: the scalar 1 (MLPs off)
+    }
+  }
+  return 0;
+}
+
+// theta / theta_weight per cell (0 where theta_weight == 0), n cells of K channels.
+int lpo_splat_normalize(int64_t n, int K, const double* theta, const double* weight, double* out) {
+  for (int64_t c = 0; c < n; ++c)
+    for (int k = 0; k < K; ++k) out[c * K + k] = weight[c] > 0.0 ? theta[c * K + k] / weight[c] : 0.0;
+  return 0;
+}
+
+// Backward of the normalised splat w.r.t. the features of rays [r0, r1):
+// theta_weight is geometry only and treated as a constant ("manually cache
+// theta_weight to normalize gradients"), so with g' = grad_out / theta_weight
+// (0 where theta_weight == 0), dL/dv_i = sum_j h_{g'}(x_ij), the renderer's
+// gather ("mirrors"). grad_features[M][K] is overwritten for those rays.
+int lpo_splat_rays_backward(int kind, int H, int W, int D, int K, int64_t r0, int64_t r1, const double* origins,
+                            const double* dirs, const double* nearv, const double* farv, int S, const double* g0,
+                            const double* g1, const double* g2, const double* w0, const double* w1,
+                            const double* w2, double* grad_features, int contraction, double contract_a) {
+  int wd[2] = {K, 2};
+  if (check(kind, H, W, D, K, 1, wd, S)) return 1;
+  Field F = make_field(kind, H, W, D, K, nullptr, nullptr, nullptr, 0, nullptr, nullptr, contraction, contract_a);
+  const double* gg[3] = {g0, g1, g2};
+  const double* wg[3] = {w0, w1, w2};
+  const int R = S - 1;
+  std::vector<Tap> taps;
+  for (int64_t r = r0; r < r1; ++r) {
+    const double* o = origins + 3 * r;
+    const double* d = dirs + 3 * r;
+    double span = farv[r] - nearv[r];
+    double delta = (span > 0.0 ? span : 0.0) / (double)R;
+    double* gv = grad_features + r * K;
+    for (int k = 0; k < K; ++k) gv[k] = 0.0;
+    for (int j = 0; j < S; ++j) {
+      double t = nearv[r] + (double)j * delta;
+      double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+      contract(F, x);
+      sample_taps(F, x, taps);
+      for (const Tap& tp : taps) {
+        double wc = wg[tp.plane][tp.cell];
+        if (!(wc > 0.0)) continue;
+        const double* g = gg[tp.plane] + tp.cell * K;
+        for (int k = 0; k < K; ++k) gv[k] += tp.w * (g[k] / wc);
+      }
+    }
+  }
+  return 0;
+}
+
 // Per-sample trace of one ray for invariant tests: sigma[S], tau[S], T[S], w[S], c[S][C].
 int lpo_trace(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
               int n_layers, const int* widths, const double* params, const double* origin, const double* dir,

@@ -1,0 +1,135 @@
+"""Pins for the oracle's Splatter:
+
+* the unnormalised splat is the exact adjoint of the rays' gather, where the
+  gather is built from oracle.sample (itself pinned against scipy's
+  map_coordinates in test_oracle_pins.py) on the explicit point list;
+* partition of unity: theta_weight collects exactly one unit of weight per
+  in-cube sample and plane;
+* constant features splat to that constant on every touched cell and exactly 0
+  elsewhere ("averages the information splatted at identical positions");
+* a vertex-coincident sample puts v on that vertex (SPEC's worked example);
+* the backward is the exact transpose of the (linear) normalised splat:
+  finite differences and the adjoint identity.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workload as wl
+from tests.helpers import rel_inf, tiny_rays
+
+
+def _spec(kind, K=3, contraction=0):
+    dims = (4, 5, 6) if kind == wl.TRIPLANE else (3, 4, 5)
+    return oracle.GridSpec(kind, dims, K, contraction, 0.8)
+
+
+def _points(rays):
+    pts, owner = [], []
+    for i in range(rays.n):
+        span = max(rays.far[i] - rays.near[i], 0.0)
+        dl = span / (rays.S - 1)
+        for j in range(rays.S):
+            t = rays.near[i] + j * dl
+            pts.append(rays.o[i] + t * rays.d[i])
+            owner.append(i)
+    return np.array(pts), np.array(owner)
+
+
+def _gather_rays(spec, rays, g):
+    """sum_j h_g(x_ij) per ray from oracle.sample on the explicit point list."""
+    F = oracle.Field(spec.kind, g, (spec.K, 2), np.zeros(spec.K * 2 + 2))   # grid only; sample() has no MLP
+    x, owner = _points(rays)
+    if spec.contraction:
+        x = oracle.contract(spec.contraction, spec.contract_a, x)
+    h = oracle.sample(F, x)
+    out = np.zeros((rays.n, spec.K))
+    np.add.at(out, owner, h)
+    return out
+
+
+@pytest.mark.parametrize("kind,contraction", [(wl.TRIPLANE, 0), (wl.VOXEL, 0), (wl.TRIPLANE, 1), (wl.VOXEL, 2)])
+def test_splat_is_adjoint_of_the_rays_gather(kind, contraction):
+    spec = _spec(kind, contraction=contraction)
+    o, d, near, far = tiny_rays(6)
+    rays = oracle.Rays(o, d, near, far * (2.5 if contraction else 1.0), 9)
+    v = wl.counter_uniform(80, np.arange(6 * spec.K, dtype=np.uint64), -1, 1).reshape(6, spec.K)
+    th, wt = oracle.splat_rays(spec, rays, v)
+    g = [wl.counter_uniform(81 + i, np.arange(int(np.prod(s)), dtype=np.uint64), -1, 1).reshape(s).astype(np.float64)
+         for i, s in enumerate(spec.shapes())]
+    lhs = sum(float(np.sum(a * b)) for a, b in zip(th, g))
+    rhs = float(np.sum(v * _gather_rays(spec, rays, g)))
+    assert abs(lhs - rhs) < 1e-12 * max(1.0, abs(lhs))
+    assert abs(lhs) > 1e-3
+
+
+@pytest.mark.parametrize("kind", [wl.TRIPLANE, wl.VOXEL])
+def test_splat_weights_partition_of_unity(kind):
+    spec = _spec(kind)
+    o, d, near, far = tiny_rays(6)
+    rays = oracle.Rays(o, d, near, far, 11)
+    th, wt = oracle.splat_rays(spec, rays, np.ones((6, spec.K)))
+    x, _ = _points(rays)
+    inside = int(np.sum(np.all(np.abs(x) <= 1.0, axis=1)))
+    assert 0 < inside < len(x)                     # some samples leave the cube and splat nothing
+    for w in wt:
+        assert abs(float(np.sum(w)) - inside) < 1e-12
+        assert np.all(w >= 0)
+
+
+@pytest.mark.parametrize("kind", [wl.TRIPLANE, wl.VOXEL])
+def test_constant_features_normalise_to_the_constant(kind):
+    spec = _spec(kind)
+    o, d, near, far = tiny_rays(6)
+    rays = oracle.Rays(o, d, near, far, 13)
+    c = np.array([0.25, -1.5, 3.0])
+    out, th, wt = oracle.splat_forward(spec, rays, np.tile(c, (6, 1)))
+    for a, w in zip(out, wt):
+        touched = w[..., 0] > 0
+        assert touched.any() and (~touched).any()
+        assert np.max(np.abs(a[touched] - c)) < 1e-13
+        assert np.all(a[~touched] == 0.0)
+
+
+def test_vertex_coincident_sample():
+    """One ray whose samples sit on voxel vertices: each vertex gets v exactly."""
+    spec = oracle.GridSpec(wl.VOXEL, (5, 5, 5), 2)
+    # vertices at x = -1, -0.5, 0, 0.5, 1 along the x axis, y = z = 0
+    rays = oracle.Rays(np.array([[-1.0, 0.0, 0.0]]), np.array([[1.0, 0.0, 0.0]]), [0.0], [2.0], 5)
+    v = np.array([[0.7, -0.2]])
+    out, th, wt = oracle.splat_forward(spec, rays, v)
+    for i in range(5):
+        assert abs(wt[0][i, 2, 2, 0] - 1.0) < 1e-15
+        assert np.max(np.abs(out[0][i, 2, 2] - v[0])) < 1e-15
+    assert abs(float(np.sum(wt[0])) - 5.0) < 1e-15
+    # backward: grad_features = sum over the ray's samples of grad_out / weight at those vertices
+    g = [np.zeros((5, 5, 5, 2))]
+    g[0][1, 2, 2] = [1.0, 2.0]
+    gv = oracle.splat_backward(spec, rays, g, wt)
+    assert np.max(np.abs(gv[0] - np.array([1.0, 2.0]))) < 1e-15
+
+
+@pytest.mark.parametrize("kind,contraction", [(wl.TRIPLANE, 0), (wl.VOXEL, 1)])
+def test_splat_backward_matches_finite_differences(kind, contraction):
+    spec = _spec(kind, contraction=contraction)
+    o, d, near, far = tiny_rays(5)
+    rays = oracle.Rays(o, d, near, far * (2.0 if contraction else 1.0), 7)
+    v = wl.counter_uniform(90, np.arange(5 * spec.K, dtype=np.uint64), -1, 1).reshape(5, spec.K).astype(np.float64)
+    g = [wl.counter_uniform(91 + i, np.arange(int(np.prod(s)), dtype=np.uint64), -1, 1).reshape(s).astype(np.float64)
+         for i, s in enumerate(spec.shapes())]
+
+    def loss(vv):
+        out, _, _ = oracle.splat_forward(spec, rays, vv)
+        return sum(float(np.sum(a * b)) for a, b in zip(out, g))
+
+    _, _, wt = oracle.splat_forward(spec, rays, v)
+    gv = oracle.splat_backward(spec, rays, g, wt)
+    fd = np.zeros_like(v)
+    eps = 1e-6
+    for idx in np.ndindex(*v.shape):
+        vp, vm = v.copy(), v.copy()
+        vp[idx] += eps
+        vm[idx] -= eps
+        fd[idx] = (loss(vp) - loss(vm)) / (2 * eps)
+    assert np.max(np.abs(fd)) > 1e-2
+    assert rel_inf(gv, fd) < 1e-8
