@@ -195,14 +195,18 @@ def run_reference(args):
     cores = host_cores()
     per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
     rates = []
+    splat = cfg.op == "splat"
+    if splat:
+        cores = 1
     for i in range(args.warmup + args.steps):
-        rate, nrays, t = cpu_oracle_rate(cfg, per_step if i >= args.warmup else min(per_step, 2.0), cores)
+        tgt = per_step if i >= args.warmup else min(per_step, 2.0)
+        rate, nrays, t = cpu_splat_rate(cfg, tgt) if splat else cpu_oracle_rate(cfg, tgt, cores)
         if i >= args.warmup:
             rates.append((rate, nrays, t))
     value = sum(r[1] for r in rates) / sum(r[2] for r in rates)
     ms = 1000.0 * cfg.n_rays / value / args.gpus
     line = {
-        "impl": "reference", "metric": "rays/s fwd+bwd", "value": value, "unit": "rays/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": "rays/s splat fwd+bwd" if splat else "rays/s fwd+bwd", "value": value, "unit": "rays/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(cfg, args.gpus),
@@ -372,13 +376,15 @@ def run_ours(args):
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     alu_peak = fp32_peak_tflops(sm_max)
     traffic = ncu_traffic(cfg.name)
+    kname = (("lp_fwd_tc2_kernel (K1tc2)", "lp_bwd_tc2_kernel (K2tc2, backward)") if len(cfg.widths) == 4 else
+             ("lp_fwd_tc_kernel (K1tc)", "lp_bwd_tc_kernel (K2tc, backward)"))
     line = {
         "metric": "rays/s fwd+bwd", "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(cfg, world),
         "breakdown_ms": {"fwd": t_fwd, "bwd": t_bwd, "allreduce": t_ar},
         "peak_bytes_per_ray": bytes_per_ray,
-        "roofline": {"bound": "l2_atomic", "kernel": "lp_bwd_tc_kernel (K2tc, backward)",
+        "roofline": {"bound": "l2_atomic", "kernel": kname[1],
                      "achieved": achieved_red, "peak": L2_RED_GBS, "unit": "GB/s",
                      "frac": achieved_red / L2_RED_GBS,
                      "traffic": (traffic * M / traffic_rays(cfg.name)) if traffic else None,
@@ -389,7 +395,7 @@ def run_ours(args):
                              "peak_tflops": alu_peak,
                              "peak_source": f"FP32 FFMA {N_SM} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz "
                                             f"(sm_max_mhz {peak_src}); algorithmic {bwd_f} FLOP/sample"},
-                     "fwd_kernel": {"kernel": "lp_fwd_tc_kernel (K1tc)",
+                     "fwd_kernel": {"kernel": kname[0],
                                     "achieved_tflops": fwd_f * samples / (t_fwd / 1000.0) / 1e12,
                                     "alu_frac": fwd_f * samples / (t_fwd / 1000.0) / 1e12 / alu_peak}},
         "clocks": clk_sum,
@@ -408,6 +414,147 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------ the Splatter
+def cpu_splat_rate(cfg, target_s: float):
+    """The oracle's Splatter fwd (+normalise) + bwd on a bounded ray sample, 1 host thread
+    (its splat keeps full fp64 grids per thread)."""
+    import oracle
+    spec = oracle.GridSpec(cfg.kind, (cfg.res,) * 3, cfg.K, cfg.contraction, cfg.contract_a)
+    gout = wl.make_grid_grad(spec.shapes())
+    idx_all = wl.subset_indices(cfg, 1 << 14)
+    n, total_rays, total_t, pos = 256, 0, 0.0, 0
+    while total_t < target_s:
+        idx = idx_all[pos:pos + n]
+        pos = (pos + n) % len(idx_all)
+        R = oracle.Rays(*wl.make_rays(cfg, idx), cfg.S)
+        v = wl.make_features(idx, cfg.K)
+        t0 = time.perf_counter()
+        out, th, wt = oracle.splat_forward(spec, R, v)
+        oracle.splat_backward(spec, R, gout, wt)
+        total_t += time.perf_counter() - t0
+        total_rays += len(idx)
+    return total_rays / total_t, total_rays, total_t
+
+
+def run_splat(args):
+    """Splatter step: zero theta/theta_weight, splat forward (both passes), normalise,
+    backward w.r.t. the features against a resident synthetic grid gradient."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_19760_b200 as lpb
+    from paper_2404_19760_b200.dist import shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = wl.get_config(args.config)
+    lo, hi = shard_range(cfg.n_rays, rank, world)
+    M, S = hi - lo, cfg.S
+    grid = lpb.SplatGrid(cfg.kind, (cfg.res,) * 3, cfg.K, cfg.contraction, cfg.contract_a)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    o, d, near, far = (T(a) for a in wl.make_rays(cfg, start=lo, count=M))
+    feats = T(wl.make_features(np.arange(lo, hi), cfg.K))
+    gout = [T(g) for g in wl.make_grid_grad(grid.shapes())]
+    theta, weight = grid.zeros(dev), grid.zeros(dev, 1)
+    gf = torch.empty((M, cfg.K), device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        for t in theta + weight:
+            t.zero_()
+        if ev:
+            ev[0].record(stream)
+        lpb.splat_forward(grid, o, d, near, far, S, feats, theta, weight)
+        if world > 1:   # the splat of a sharded view batch is a sum over ranks (one all-reduce)
+            for t in theta + weight:
+                dist.all_reduce(t)
+        if ev:
+            ev[1].record(stream)
+        lpb.splat_normalize(grid, theta, weight, out=theta)
+        if ev:
+            ev[2].record(stream)
+        lpb.splat_backward(grid, o, d, near, far, S, gout, weight, gf)
+        if ev:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    tt = torch.tensor([start.elapsed_time(stop)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item()) / args.steps
+    t_f = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    t_n = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    t_b = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+
+    e2e = None
+    if not args.no_e2e:   # inputs from pinned host memory every step, a checksum of the result back
+        pin = lambda t: t.cpu().pin_memory()
+        hs = [pin(t) for t in (o, d, near, far, feats)]
+        for i in range(args.warmup + args.steps):
+            if i == args.warmup:
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+            for dst, src in zip((o, d, near, far, feats), hs):
+                dst.copy_(src, non_blocking=True)
+            step()
+            float(gf[0, 0].item())
+        e2e_ms = (time.perf_counter() - t0) * 1000.0 / args.steps
+        e2e = {"value": cfg.n_rays / (e2e_ms / 1000.0), "unit": "rays/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(M * (32 + 4 * cfg.K)), "d2h_bytes_per_step": 4,
+               "api": "paper_2404_19760_b200.splat_forward / splat_normalize / splat_backward (C ABI)"}
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    corners = 12 if cfg.kind == wl.TRIPLANE else 8
+    red_b = corners * (cfg.K * 4 + 4)          # feature + weight reductions per sample
+    ach = red_b * M * S / (t_f / 1000.0) / 1e9
+    line = {
+        "metric": "rays/s splat fwd+bwd", "value": cfg.n_rays / (ms / 1000.0), "unit": "rays/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.note}", "rays": cfg.n_rays, "samples_per_ray": S,
+                   "grid": "triplane" if cfg.kind == wl.TRIPLANE else "voxel", "grid_res": cfg.res, "K": cfg.K,
+                   "parallelism": f"dp{world} (rays sharded, grid all-reduce)",
+                   "l2": "theta + theta_weight (grid-sized, L2-resident for s2, not for s1) re-zeroed every step"},
+        "breakdown_ms": {"splat_fwd": t_f, "normalize": t_n, "splat_bwd": t_b},
+        "roofline": {"bound": "l2_atomic", "kernel": "lp_splat_fwd_kernel", "achieved": ach, "peak": L2_RED_GBS,
+                     "unit": "GB/s", "frac": ach / L2_RED_GBS, "traffic": None,
+                     "algorithmic": f"{red_b} B of fp32 reductions per sample (corners x (K + 1) x 4)",
+                     "peak_source": "measured: scripts/red_bench.cu, profiles/r1_red_bench.txt"},
+        "clocks": clk.summary(), "gpu_launches": (3 if cfg.kind == wl.TRIPLANE else 1) + 2,
+    }
+    line["gpu_launches"] *= args.steps
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline and world == 1:
+        rate, nrays, t = cpu_splat_rate(cfg, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": "rays/s", "cores": 1, "kind": "oracle",
+                                "sample": f"{nrays} rays of {cfg.name} (x{S} points) splat fwd+bwd, fp64 oracle, "
+                                          f"{t:.1f} s on 1 host thread"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def traffic_rays(cfg_name):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     return json.load(open(p))[cfg_name]["rays"]
@@ -417,6 +564,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif wl.get_config(args.config).op == "splat":
+        run_splat(args)
     else:
         run_ours(args)
 

@@ -145,6 +145,36 @@ lp_status lp_render_fwd_bwd_host(const lp_grid* grid, const lp_mlp* mlp, const l
                                  float* out_host, float* tau_host, float* const grad_data[3], float* grad_params,
                                  void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------- Splatter
+ * The dual of the renderer: M pixel rays, each
+ * expanded into the renderer's R+1 equispaced points x_ij (same lp_rays
+ * convention and contraction), every point inheriting the pixel feature v_i
+ * (P:263). theta[c] += sum_ij w_c(x_ij) v_i with the sampling weights of h
+ * ("the same as the sampling weights used in rendering"), and in a
+ * second pass with the MLPs off theta_weight[c] += sum_ij w_c(x_ij)
+ * (P:746-750); the result is theta / theta_weight. g_s of Eq. 2 is not
+ * applied (the paper's benchmark disables it). grid->data is unused
+ * (may be NULL); grid->K = feature channels (compiled: 8, 16, 32).
+ * Layouts: theta / out / grad_out as grid->data (channel-last, 16-byte aligned);
+ * theta_weight with the same planes and one channel ([H][W], [W][D], [D][H] or
+ * [H][W][D]); features / grad_features [M][K] (16-byte aligned).
+ * Forward: ACCUMULATES (+=, fp32 atomics) into theta and theta_weight; the
+ * caller zeroes them. */
+lp_status lp_splat_forward(const lp_grid* grid, const lp_rays* rays, const float* features, float* const theta[3],
+                           float* const theta_weight[3], void* stream);
+
+/* out = theta / theta_weight per cell, exactly 0 where theta_weight == 0
+ * (reading R27). out may alias theta. */
+lp_status lp_splat_normalize(const lp_grid* grid, const float* const theta[3], const float* const theta_weight[3],
+                             float* const out[3], void* stream);
+
+/* Backward of the normalised splat w.r.t. the features, theta_weight treated
+ * as a constant cached from the forward:
+ *   grad_features_i = sum_j h_{g'}(x_ij),  g' = grad_out / theta_weight (0 where 0),
+ * the renderer's gather ("mirrors"). grad_features [M][K] is OVERWRITTEN. */
+lp_status lp_splat_backward(const lp_grid* grid, const lp_rays* rays, const float* const grad_out[3],
+                            const float* const theta_weight[3], float* grad_features, void* stream);
+
 /* Optional: keep theta resident in L2 for kernels launched by this library on
  * the calling thread's current device (access-policy window on each launch,
  * hit ratio in (0,1]; 0 disables). Sets cudaLimitPersistingL2CacheSize. */

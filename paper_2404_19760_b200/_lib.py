@@ -21,7 +21,8 @@ _STATUS = {0: "LP_OK", 1: "LP_ERR_INVALID_ARG", 2: "LP_ERR_UNSUPPORTED", 3: "LP_
 
 # Every symbol include/lp.h declares (tests check the library exports them all).
 EXPORTED = ("lp_render_forward", "lp_render_backward", "lp_fwd_bwd_host_workspace_bytes",
-            "lp_render_fwd_bwd_host", "lp_set_l2_persist", "lp_last_error", "lp_abi_version")
+            "lp_render_fwd_bwd_host", "lp_splat_forward", "lp_splat_normalize", "lp_splat_backward",
+            "lp_set_l2_persist", "lp_last_error", "lp_abi_version")
 
 
 class LpGrid(ctypes.Structure):
@@ -59,10 +60,14 @@ def _load():
     L.lp_fwd_bwd_host_workspace_bytes.restype = ctypes.c_size_t
     L.lp_render_fwd_bwd_host.argtypes = [gp, mp, rp, P, P, P, P, P, ctypes.POINTER(ctypes.c_void_p), P, P,
                                          ctypes.c_size_t, P]
+    P3 = ctypes.POINTER(ctypes.c_void_p)
+    L.lp_splat_forward.argtypes = [gp, rp, P, P3, P3, P]
+    L.lp_splat_normalize.argtypes = [gp, P3, P3, P3, P]
+    L.lp_splat_backward.argtypes = [gp, rp, P3, P3, P, P]
     L.lp_set_l2_persist.argtypes = [ctypes.c_float]
     L.lp_last_error.restype = ctypes.c_char_p
     for f in (L.lp_render_forward, L.lp_render_backward, L.lp_render_fwd_bwd_host, L.lp_set_l2_persist,
-              L.lp_abi_version):
+              L.lp_abi_version, L.lp_splat_forward, L.lp_splat_normalize, L.lp_splat_backward):
         f.restype = ctypes.c_int
     if L.lp_abi_version() != LP_ABI_VERSION:
         raise ImportError(f"{LIB_PATH} has ABI {L.lp_abi_version()}, expected {LP_ABI_VERSION}: rebuild it")

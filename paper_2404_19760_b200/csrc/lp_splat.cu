@@ -1,0 +1,182 @@
+// lp_splat.cu -- C ABI of the Splatter (include/lp.h lp_splat_*): validation,
+// instance dispatch and persistent launches of lp_splat_kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "../../include/lp.h"
+#include "lp_internal.h"
+#include "lp_splat_kernels.cuh"
+
+namespace {
+using namespace lpi;
+
+struct Shape {
+  std::once_flag once;
+  int blocks = 0;
+  cudaError_t err = cudaSuccess;
+};
+
+template <typename KernelT>
+lp_status launch_persistent(KernelT kernel, Shape& sh, int threads, int64_t work_blocks, const lp::SplatArgs& a,
+                            cudaStream_t s) {
+  std::call_once(sh.once, [&] {
+    int dev = 0, sms = 0, occ = 0;
+    sh.err = cudaGetDevice(&dev);
+    if (sh.err == cudaSuccess) sh.err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sh.err == cudaSuccess) sh.err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0);
+    if (sh.err == cudaSuccess && occ < 1) sh.err = cudaErrorInvalidConfiguration;
+    sh.blocks = sms * occ;
+  });
+  if (sh.err != cudaSuccess) return cuda_check(sh.err, "splat kernel setup");
+  if (work_blocks <= 0) return LP_OK;
+  const int grid = (int)(work_blocks < sh.blocks ? work_blocks : sh.blocks);
+  kernel<<<grid, threads, 0, s>>>(a);
+  return cuda_check(cudaGetLastError(), "splat kernel launch");
+}
+
+template <bool FWD, int KIND, int K>
+lp_status run(const lp::SplatArgs& a, cudaStream_t s) {
+  static Shape sh;
+  constexpr int WARPS = lp::kSplatThreads / 32;
+  const int64_t blocks = ((a.M + 31) / 32 + WARPS - 1) / WARPS;
+  if constexpr (FWD) return launch_persistent(lp::lp_splat_fwd_kernel<KIND, K>, sh, lp::kSplatThreads, blocks, a, s);
+  else return launch_persistent(lp::lp_splat_bwd_kernel<KIND, K>, sh, lp::kSplatThreads, blocks, a, s);
+}
+
+template <bool FWD>
+lp_status dispatch(const lp_grid* g, const lp::SplatArgs& a, cudaStream_t s) {
+  const bool tri = g->kind == LP_GRID_TRIPLANE;
+  switch (g->K) {
+    case 8: return tri ? run<FWD, 0, 8>(a, s) : run<FWD, 1, 8>(a, s);
+    case 16: return tri ? run<FWD, 0, 16>(a, s) : run<FWD, 1, 16>(a, s);
+    default: return tri ? run<FWD, 0, 32>(a, s) : run<FWD, 1, 32>(a, s);
+  }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int64_t plane_cells(const lp_grid* g, int i) {
+  if (g->kind == LP_GRID_VOXEL) return (int64_t)g->H * g->W * g->D;
+  return i == 0 ? (int64_t)g->H * g->W : i == 1 ? (int64_t)g->W * g->D : (int64_t)g->D * g->H;
+}
+
+lp_status validate(const lp_grid* g, const lp_rays* r) {
+  if (!g) return fail(LP_ERR_INVALID_ARG, "null grid descriptor");
+  if (g->kind != LP_GRID_TRIPLANE && g->kind != LP_GRID_VOXEL) return fail(LP_ERR_INVALID_ARG, "bad grid kind %d", g->kind);
+  if (g->H < 2 || g->W < 2 || g->D < 2) return fail(LP_ERR_INVALID_ARG, "grid dims must be >= 2");
+  if (g->K != 8 && g->K != 16 && g->K != 32) return fail(LP_ERR_UNSUPPORTED, "splat: K must be 8, 16 or 32 (got %d)", g->K);
+  if (g->contraction < LP_CONTRACT_NONE || g->contraction > LP_CONTRACT_RADIAL)
+    return fail(LP_ERR_INVALID_ARG, "bad contraction mode %d", g->contraction);
+  if (g->contraction != LP_CONTRACT_NONE && !(g->contract_scale > 0.0f && g->contract_scale <= 2.0f))
+    return fail(LP_ERR_INVALID_ARG, "contract_scale must be in (0, 2]");
+  const int np = g->kind == LP_GRID_TRIPLANE ? 3 : 1;
+  for (int i = 0; i < np; ++i)
+    if (plane_cells(g, i) * g->K >= (1LL << 31)) return fail(LP_ERR_UNSUPPORTED, "grid plane/volume has >= 2^31 elements");
+  if (r) {
+    if (r->n_rays < 0) return fail(LP_ERR_INVALID_ARG, "n_rays < 0");
+    if (r->n_samples < 2) return fail(LP_ERR_INVALID_ARG, "n_samples must be >= 2");
+    if (r->n_rays > 0 && (!r->origins || !r->dirs || !r->t_near || !r->t_far))
+      return fail(LP_ERR_INVALID_ARG, "null ray array");
+  }
+  return LP_OK;
+}
+
+template <typename PtrT>
+lp_status check_planes(const lp_grid* g, PtrT const* p, const char* name) {
+  if (!p) return fail(LP_ERR_INVALID_ARG, "%s is null", name);
+  const int np = g->kind == LP_GRID_TRIPLANE ? 3 : 1;
+  for (int i = 0; i < np; ++i) {
+    if (!p[i]) return fail(LP_ERR_INVALID_ARG, "%s[%d] is null", name, i);
+    if (!aligned16(p[i])) return fail(LP_ERR_MISALIGNED, "%s[%d] not 16-byte aligned", name, i);
+  }
+  return LP_OK;
+}
+
+template <typename PtrT>
+lp_status check_weights(const lp_grid* g, PtrT const* p, const char* name) {
+  if (!p) return fail(LP_ERR_INVALID_ARG, "%s is null", name);
+  const int np = g->kind == LP_GRID_TRIPLANE ? 3 : 1;
+  for (int i = 0; i < np; ++i)
+    if (!p[i]) return fail(LP_ERR_INVALID_ARG, "%s[%d] is null", name, i);
+  return LP_OK;
+}
+
+lp::SplatArgs make_args(const lp_grid* g, const lp_rays* r) {
+  lp::SplatArgs a{};
+  a.dims = lp::GridDims{g->H, g->W, g->D};
+  a.contract = lp::Contract{g->contraction, (double)g->contract_scale};
+  a.orig = r->origins;
+  a.dir = r->dirs;
+  a.tnear = r->t_near;
+  a.tfar = r->t_far;
+  a.M = r->n_rays;
+  a.S = r->n_samples;
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+lp_status lp_splat_forward(const lp_grid* grid, const lp_rays* rays, const float* features, float* const theta[3],
+                           float* const theta_weight[3], void* stream) {
+  lp_status st = validate(grid, rays);
+  if (st != LP_OK) return st;
+  if (!rays) return fail(LP_ERR_INVALID_ARG, "null rays descriptor");
+  if ((st = check_planes(grid, theta, "theta")) != LP_OK) return st;
+  if ((st = check_weights(grid, theta_weight, "theta_weight")) != LP_OK) return st;
+  if (rays->n_rays > 0 && !features) return fail(LP_ERR_INVALID_ARG, "null features");
+  if (rays->n_rays > 0 && !aligned16(features)) return fail(LP_ERR_MISALIGNED, "features not 16-byte aligned");
+  lp::SplatArgs a = make_args(grid, rays);
+  const int np = grid->kind == LP_GRID_TRIPLANE ? 3 : 1;
+  for (int i = 0; i < 3; ++i) {
+    a.theta[i] = i < np ? theta[i] : nullptr;
+    a.weight[i] = i < np ? theta_weight[i] : nullptr;
+  }
+  a.feat = features;
+  return dispatch<true>(grid, a, static_cast<cudaStream_t>(stream));
+}
+
+lp_status lp_splat_normalize(const lp_grid* grid, const float* const theta[3], const float* const theta_weight[3],
+                             float* const out[3], void* stream) {
+  lp_status st = validate(grid, nullptr);
+  if (st != LP_OK) return st;
+  if ((st = check_planes(grid, theta, "theta")) != LP_OK) return st;
+  if ((st = check_weights(grid, theta_weight, "theta_weight")) != LP_OK) return st;
+  if ((st = check_planes(grid, out, "out")) != LP_OK) return st;
+  const int np = grid->kind == LP_GRID_TRIPLANE ? 3 : 1;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < np; ++i) {
+    const int64_t cells = plane_cells(grid, i);
+    const int64_t n4 = cells * grid->K / 4;
+    const int blocks = (int)((n4 + 255) / 256 < 148 * 16 ? (n4 + 255) / 256 : 148 * 16);
+    if (blocks == 0) continue;
+    if (grid->K == 8) lp::lp_splat_normalize_kernel<8><<<blocks, 256, 0, s>>>(theta[i], theta_weight[i], out[i], cells);
+    else if (grid->K == 16) lp::lp_splat_normalize_kernel<16><<<blocks, 256, 0, s>>>(theta[i], theta_weight[i], out[i], cells);
+    else lp::lp_splat_normalize_kernel<32><<<blocks, 256, 0, s>>>(theta[i], theta_weight[i], out[i], cells);
+    if ((st = cuda_check(cudaGetLastError(), "splat normalize launch")) != LP_OK) return st;
+  }
+  return LP_OK;
+}
+
+lp_status lp_splat_backward(const lp_grid* grid, const lp_rays* rays, const float* const grad_out[3],
+                            const float* const theta_weight[3], float* grad_features, void* stream) {
+  lp_status st = validate(grid, rays);
+  if (st != LP_OK) return st;
+  if (!rays) return fail(LP_ERR_INVALID_ARG, "null rays descriptor");
+  if ((st = check_planes(grid, grad_out, "grad_out")) != LP_OK) return st;
+  if ((st = check_weights(grid, theta_weight, "theta_weight")) != LP_OK) return st;
+  if (rays->n_rays > 0 && !grad_features) return fail(LP_ERR_INVALID_ARG, "null grad_features");
+  if (rays->n_rays > 0 && !aligned16(grad_features)) return fail(LP_ERR_MISALIGNED, "grad_features not 16-byte aligned");
+  lp::SplatArgs a = make_args(grid, rays);
+  const int np = grid->kind == LP_GRID_TRIPLANE ? 3 : 1;
+  for (int i = 0; i < 3; ++i) {
+    a.gout[i] = i < np ? grad_out[i] : nullptr;
+    a.weight[i] = i < np ? const_cast<float*>(theta_weight[i]) : nullptr;
+  }
+  a.gfeat = grad_features;
+  return dispatch<false>(grid, a, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+"""PyTorch-facing API of the Splatter (include/lp.h lp_splat_*; marshalling only).
+
+    grid = SplatGrid(VOXEL, (160, 160, 160), K=32)
+    planes = splat(grid, origins, dirs, near, far, n_samples, features)   # autograd-aware
+
+Pixel rays expand into the renderer's R+1 equispaced points, each inheriting
+the pixel's feature; features are pushed into theta with the sampling
+weights of h and the scalar 1 into theta_weight; the result is
+theta / theta_weight. The backward w.r.t. the features mirrors the
+renderer's gather with theta_weight cached.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import List, Optional, Tuple
+
+import torch
+
+from . import _lib
+from .render import CONTRACT_NONE, TRIPLANE, VOXEL, _c_rays, _ptr, _req, _stream
+
+
+@dataclass
+class SplatGrid:
+    """Shape of the splat target: kind, (H, W, D), K channels, contraction."""
+    kind: int
+    dims: Tuple[int, int, int]
+    K: int
+    contraction: int = CONTRACT_NONE
+    contract_scale: float = 1.0
+
+    def shapes(self, K: Optional[int] = None) -> List[tuple]:
+        K = self.K if K is None else K
+        H, W, D = self.dims
+        if self.kind == TRIPLANE:
+            return [(H, W, K), (W, D, K), (D, H, K)]
+        if self.kind == VOXEL:
+            return [(H, W, D, K)]
+        raise ValueError(f"bad kind {self.kind}")
+
+    def c_grid(self) -> _lib.LpGrid:
+        H, W, D = self.dims
+        return _lib.make_grid(self.kind, H, W, D, self.K, [], self.contraction, self.contract_scale)
+
+    def zeros(self, device, K: Optional[int] = None) -> List[torch.Tensor]:
+        return [torch.zeros(s, device=device, dtype=torch.float32) for s in self.shapes(K)]
+
+
+def _planes(grid: SplatGrid, ts, name, K=None):
+    shapes = grid.shapes(K)
+    if len(ts) != len(shapes):
+        raise ValueError(f"{name}: expected {len(shapes)} tensors")
+    for i, (t, s) in enumerate(zip(ts, shapes)):
+        _req(t, f"{name}[{i}]", s)
+    return _lib.ptr_array3([t.data_ptr() for t in ts])
+
+
+def splat_forward(grid: SplatGrid, origins, dirs, near, far, n_samples: int, features, theta=None, weight=None):
+    """Accumulate the unnormalised splat: returns (theta planes, theta_weight planes)."""
+    M = origins.shape[0]
+    rays = _c_rays(origins, dirs, near, far, n_samples)
+    _req(features, "features", (M, grid.K))
+    theta = grid.zeros(origins.device) if theta is None else theta
+    weight = grid.zeros(origins.device, 1) if weight is None else weight
+    g = grid.c_grid()
+    _lib.check(_lib.lib.lp_splat_forward(ctypes.byref(g), ctypes.byref(rays), _ptr(features),
+                                         _planes(grid, theta, "theta"), _planes(grid, weight, "weight", 1),
+                                         _stream()))
+    return theta, weight
+
+
+def splat_normalize(grid: SplatGrid, theta, weight, out=None):
+    """theta / theta_weight per cell (0 where no weight landed)."""
+    out = [torch.empty_like(t) for t in theta] if out is None else out
+    g = grid.c_grid()
+    _lib.check(_lib.lib.lp_splat_normalize(ctypes.byref(g), _planes(grid, theta, "theta"),
+                                           _planes(grid, weight, "weight", 1), _planes(grid, out, "out"),
+                                           _stream()))
+    return out
+
+
+def splat_backward(grid: SplatGrid, origins, dirs, near, far, n_samples: int, grad_out, weight,
+                   grad_features=None):
+    """dL/d(features) of the normalised splat, theta_weight cached from the forward."""
+    M = origins.shape[0]
+    rays = _c_rays(origins, dirs, near, far, n_samples)
+    gf = torch.empty((M, grid.K), device=origins.device, dtype=torch.float32) if grad_features is None \
+        else grad_features
+    _req(gf, "grad_features", (M, grid.K))
+    g = grid.c_grid()
+    _lib.check(_lib.lib.lp_splat_backward(ctypes.byref(g), ctypes.byref(rays), _planes(grid, grad_out, "grad_out"),
+                                          _planes(grid, weight, "weight", 1), _ptr(gf), _stream()))
+    return gf
+
+
+class _SplatFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, geom, n_samples, origins, dirs, near, far, features):
+        grid = SplatGrid(*geom)
+        theta, weight = splat_forward(grid, origins, dirs, near, far, n_samples, features)
+        out = splat_normalize(grid, theta, weight, out=theta)   # in place: theta itself is not kept
+        ctx.save_for_backward(origins, dirs, near, far, *weight)
+        ctx.meta = (geom, n_samples)
+        return tuple(out)
+
+    @staticmethod
+    def backward(ctx, *grad_out):
+        geom, n_samples = ctx.meta
+        origins, dirs, near, far, *weight = ctx.saved_tensors
+        grid = SplatGrid(*geom)
+        go = [g.contiguous() if g is not None else torch.zeros(s, device=origins.device)
+              for g, s in zip(grad_out, grid.shapes())]
+        gf = splat_backward(grid, origins, dirs, near, far, n_samples, go, weight)
+        return (None, None, None, None, None, None, gf)
+
+
+def splat(grid: SplatGrid, origins, dirs, near, far, n_samples: int, features) -> List[torch.Tensor]:
+    """Differentiable Splatter: returns the normalised planes (theta / theta_weight);
+    gradients flow to `features` (the saved state is theta_weight only)."""
+    geom = (grid.kind, tuple(grid.dims), grid.K, grid.contraction, grid.contract_scale)
+    return list(_SplatFn.apply(geom, int(n_samples), origins, dirs, near, far, features))

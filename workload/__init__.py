@@ -38,7 +38,7 @@ import numpy as np
 
 __all__ = [
     "Config", "CONFIGS", "get_config", "counter_uniform", "make_grid",
-    "make_mlp", "make_rays", "make_bg", "make_grad_out", "make_grad_tau",
+    "make_mlp", "make_rays", "make_bg", "make_grad_out", "make_grad_tau", "make_features", "make_grid_grad",
     "camera_positions", "softplus_inv", "subset_indices",
 ]
 
@@ -92,6 +92,7 @@ class Config:
     contraction: int = 0      # scene contraction of sample points (0 none, 1 per-axis, 2 radial)
     contract_a: float = 1.0   # contraction scale a
     near_far: Optional[tuple] = None   # constant (near, far) for every ray (unbounded scenes)
+    op: str = "render"        # "render" (the renderer) or "splat" (the Splatter: widths unused)
 
     @property
     def n_rays(self) -> int:
@@ -142,6 +143,13 @@ CONFIGS = {
                  "unbounded scene: triplane 3x160x160 C=32, 3-layer MLP, 16 views at 256x256, "
                  "384 samples/ray, per-axis contraction a=1", contraction=1, contract_a=1.0,
                  near_far=(0.05, 12.0)),
+    # Splatter benchmark shape: N input feature maps lifted into a 160^3 voxel
+    # grid, MLPs off; 32-channel features, 160 points per ray. N = 64 maps
+    # of 128x128 pixels (the text gives neither N nor the map size: reading R28).
+    "s1": Config("s1", VOXEL, 160, 32, (32, 4), 64, 128, 160,
+                 "splatter: 64 feature maps of 128x128x32 into a 160^3 voxel grid, 160 points/ray", op="splat"),
+    "s2": Config("s2", TRIPLANE, 160, 32, (32, 4), 64, 128, 160,
+                 "splatter: 64 feature maps of 128x128x32 into 3x160x160 triplanes, 160 points/ray", op="splat"),
 }
 
 
@@ -299,6 +307,23 @@ def make_grad_out(idx: np.ndarray, C: int = 3, seed: int = 3) -> np.ndarray:
     idx = np.asarray(idx, dtype=np.uint64)
     e = idx[:, None] * np.uint64(C) + np.arange(C, dtype=np.uint64)[None, :]
     return counter_uniform(seed, e.reshape(-1), -1.0, 1.0).reshape(len(idx), C)
+
+
+def make_features(idx: np.ndarray, K: int, seed: int = 7) -> np.ndarray:
+    """Splatter input: per-pixel features U(-1,1) keyed on (global ray index, channel)."""
+    idx = np.asarray(idx, dtype=np.uint64)
+    e = idx[:, None] * np.uint64(K) + np.arange(K, dtype=np.uint64)[None, :]
+    return counter_uniform(seed, e.reshape(-1), -1.0, 1.0).reshape(len(idx), K)
+
+
+def make_grid_grad(shapes, seed: int = 8) -> List[np.ndarray]:
+    """Upstream gradient of a grid-shaped output: U(-1,1) keyed on the flat element index."""
+    out, base = [], 0
+    for s in shapes:
+        n = int(np.prod(s))
+        out.append(counter_uniform(seed, np.arange(base, base + n, dtype=np.uint64), -1.0, 1.0).reshape(s))
+        base += n
+    return out
 
 
 def make_grad_tau(idx: np.ndarray, seed: int = 4) -> np.ndarray:
