@@ -3,7 +3,6 @@ fp64 oracle on the same seeded inputs. The splat accumulates with fp32 atomics
 (order nondeterministic, like the renderer's gradients), so the normalised
 grid, the weights and the feature gradients are compared with the metric
 ||gpu - ref||_inf / ||ref||_inf against 1e-4 (reading R27)."""
-import dataclasses
 
 import numpy as np
 import pytest
@@ -90,7 +89,8 @@ def test_splat_full_size_properties(torch_cuda):
     assert int(touched.sum()) > 1000
     err = (out[0][touched] - c).abs().max().item()
     assert err < 1e-5 * 3.0, err
-    assert float(out[0][~touched].abs().max()) == 0.0
+    if bool((~touched).any()):
+        assert float(out[0][~touched].abs().max()) == 0.0
     # every sample of a hitting ray lies inside the cube (slab near/far): total weight = hits x S
     hits = int((f > n).sum())
     assert abs(float(wt[0].double().sum()) - hits * cfg.S) < 1e-5 * hits * cfg.S
