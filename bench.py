@@ -156,8 +156,8 @@ def cpu_oracle_rate(cfg, target_s: float, threads: int):
     import oracle
     from tests.gpu_problem import grid_np
     grid = grid_np(cfg.name)
-    params = wl.make_mlp(cfg.widths)
-    F = oracle.Field(cfg.kind, grid, cfg.widths, params, cfg.contraction, cfg.contract_a)
+    params = wl.make_params(cfg)
+    F = oracle.Field(cfg.kind, grid, cfg.widths, params, cfg.contraction, cfg.contract_a, cfg.dir_freqs)
     n = max(threads, 8)
     total_rays, total_t = 0, 0.0
     idx_all = wl.subset_indices(cfg, 1 << 16)
@@ -251,7 +251,7 @@ def run_ours(args):
 
     # ---- field and flat gradient buffer [grad theta | grad MLP] (16-byte aligned pieces)
     grid = wl.make_grid(cfg)
-    params = torch.from_numpy(wl.make_mlp(cfg.widths)).to(dev)
+    params = torch.from_numpy(wl.make_params(cfg)).to(dev)
     planes = [torch.from_numpy(g).to(dev) for g in grid]
     field = lpb.Field(cfg.kind, planes, cfg.widths, params, cfg.contraction, cfg.contract_a)
     grads = FlatGrads([p.shape for p in planes] + [params.shape], device=dev)

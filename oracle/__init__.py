@@ -54,15 +54,15 @@ def lib():
             L.lpo_mlp_forward.argtypes = [i32, P, P, i64, P, P]
             L.lpo_mlp_backward.argtypes = [i32, P, P, i64, P, P, P, P]
             L.lpo_render_forward.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
-                                             P, P, P, P, i32, P, P, P, P, i32, f64]
+                                             P, P, P, P, i32, P, P, P, P, i32, f64, i32]
             L.lpo_render_backward.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
-                                              P, P, P, P, i32, P, P, P, P, P, P, P, i32, P, i32, f64]
+                                              P, P, P, P, i32, P, P, P, P, P, P, P, i32, P, i32, f64, i32]
             L.lpo_trace.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, P, P, f64, f64, i32,
-                                    P, P, P, P, P, i32, f64]
+                                    P, P, P, P, P, i32, f64, i32]
             L.lpo_render_min_preact.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
-                                                P, P, P, P, i32, P, i32, f64]
+                                                P, P, P, P, i32, P, i32, f64, i32]
             L.lpo_render_relu_slack.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
-                                                P, P, P, P, i32, P, P, P, f64, P, P, P, P, P, i32, f64]
+                                                P, P, P, P, i32, P, P, P, f64, P, P, P, P, P, i32, f64, i32]
             L.lpo_contract.argtypes = [i32, f64, i64, P, P]
             L.lpo_splat_rays.argtypes = [i32, i32, i32, i32, i32, i64, i64, P, P, P, P, i32, P, P, P, P, P, P, P,
                                          i32, f64]
@@ -88,11 +88,14 @@ def _p(a: Optional[np.ndarray]):
 class Field:
     """theta (list of planes or one voxel volume, channel-last) + packed MLP,
     plus the scene contraction applied to sample points (0 none, 1 per-axis,
-    2 radial; scale a) -- lp_oracle.cpp contract()."""
+    2 radial; scale a) -- lp_oracle.cpp contract(). dir_freqs = F > 0 makes the
+    field view-dependent: params hold g_sigma (widths with output 1) then g_v
+    (input K + 6F, output C) -- lp_oracle.cpp split_nets()."""
 
     def __init__(self, kind: int, grid: Sequence[np.ndarray], widths: Sequence[int], params: np.ndarray,
-                 contraction: int = 0, contract_a: float = 1.0):
+                 contraction: int = 0, contract_a: float = 1.0, dir_freqs: int = 0):
         self.kind = int(kind)
+        self.dir_freqs = int(dir_freqs)
         self.contraction = int(contraction)
         self.contract_a = float(contract_a)
         self.grid = [_d(g) for g in grid]
@@ -119,7 +122,7 @@ class Field:
         return (self.kind, self.H, self.W, self.D, self.K)
 
     def _scene(self):
-        return (self.contraction, self.contract_a)
+        return (self.contraction, self.contract_a, self.dir_freqs)
 
 
 def contract(contraction: int, a: float, x: np.ndarray) -> np.ndarray:

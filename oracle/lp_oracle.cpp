@@ -31,6 +31,8 @@ struct Field {
   const double* params;  // W_0[w1][w0], b_0[w1], W_1[w2][w1], b_1[w2], ...
   int contraction;     // 0 none, 1 per-axis, 2 radial (see contract())
   double contract_a;   // scale a
+  int dir_freqs;       // F > 0: view-dependent field, two networks (see split_nets())
+  int wsig[10], wcol[10];  // widths of g_sigma / g_v when dir_freqs > 0
 };
 
 struct Tap {
@@ -195,12 +197,54 @@ void mlp_backward(const Field& F, const MlpTrace& tr, const double* dout, double
 double softplus(double x) { return (x > 0.0 ? x : 0.0) + std::log1p(std::exp(-std::fabs(x))); }
 double sigmoid(double x) { return 1.0 / (1.0 + std::exp(-x)); }
 
+// View-dependent colour ("f_v(x_ij) is calculated by another MLP g_v
+// taking the sampled feature and view directions as inputs"; reading R29).
+// direnc(d) = for each axis k, for each frequency f = 2^0 .. 2^{F-1}:
+// (sin(pi f d_k), cos(pi f d_k)), E = 6F values (F = 4 by default).
+void direnc(const double* d, int F, double* e) {
+  const double pi = 3.14159265358979323846;
+  for (int k = 0; k < 3; ++k)
+    for (int i = 0; i < F; ++i) {
+      double a = pi * std::ldexp(1.0, i) * d[k];
+      e[2 * (k * F + i)] = std::sin(a);
+      e[2 * (k * F + i) + 1] = std::cos(a);
+    }
+}
+
+// With dir_freqs = F > 0 the field's parameters hold two networks with the
+// hidden widths of `widths` (reading R29): g_sigma: K -> hidden... -> 1 (the
+// density logit) followed by g_v: K + 6F -> hidden... -> C (the colour logits),
+// each packed W_0, b_0, W_1, b_1, ... like a single network.
+int64_t net_params(int n_layers, const int* w) {
+  int64_t n = 0;
+  for (int l = 0; l < n_layers; ++l) n += (int64_t)w[l + 1] * w[l] + w[l + 1];
+  return n;
+}
+
+void split_nets(const Field& F, Field& Fs, Field& Fv) {
+  Fs = F;
+  Fv = F;
+  const int L = F.n_layers, C = F.widths[L] - 1;
+  for (int l = 0; l <= L; ++l) {
+    Fs.wsig[l] = F.widths[l];
+    Fv.wcol[l] = F.widths[l];
+  }
+  Fs.wsig[L] = 1;
+  Fv.wcol[0] = F.K + 6 * F.dir_freqs;
+  Fv.wcol[L] = C;
+  Fs.widths = Fs.wsig;
+  Fv.widths = Fv.wcol;
+  Fv.params = F.params + net_params(L, Fs.widths);
+}
+
 // Everything stored for one ray by the store-all forward.
 struct RayTrace {
   int S;
   double delta;
   std::vector<std::vector<Tap>> taps;
   std::vector<MlpTrace> mlp;
+  std::vector<MlpTrace> mlpv;             // g_v traces (view-dependent fields)
+  std::vector<double> e;                  // direnc(d) of the ray
   std::vector<double> t;                  // t_j = near + j Delta (ray parameter of sample j)
   std::vector<double> sigma, tau, T, w;   // tau_j = sum_{n<=j} Delta sigma_n, T_j = exp(-tau_j)
   std::vector<std::vector<double>> c;     // colours c_j (C each)
@@ -220,6 +264,7 @@ void trace_ray(const Field& F, const double* o, const double* d, double nearv, d
   rt.delta = (span > 0.0 ? span : 0.0) / (double)R;
   rt.taps.assign(S, {});
   rt.mlp.assign(S, {});
+  rt.mlpv.assign(F.dir_freqs > 0 ? S : 0, {});
   rt.t.assign(S, 0.0);
   rt.sigma.assign(S, 0.0);
   rt.tau.assign(S, 0.0);
@@ -227,6 +272,14 @@ void trace_ray(const Field& F, const double* o, const double* d, double nearv, d
   rt.w.assign(S, 0.0);
   rt.c.assign(S, std::vector<double>(C, 0.0));
   std::vector<double> h(F.K);
+  Field Fs, Fv;
+  std::vector<double> hv;
+  if (F.dir_freqs > 0) {
+    split_nets(F, Fs, Fv);
+    rt.e.assign(6 * F.dir_freqs, 0.0);
+    direnc(d, F.dir_freqs, rt.e.data());
+    hv.assign(F.K + 6 * F.dir_freqs, 0.0);
+  }
   double tau_prev = 0.0;
   for (int j = 0; j < S; ++j) {
     double t = nearv + (double)j * rt.delta;
@@ -235,10 +288,19 @@ void trace_ray(const Field& F, const double* o, const double* d, double nearv, d
     contract(F, x);
     sample_taps(F, x, rt.taps[j]);
     gather(F, rt.taps[j], h.data());
-    mlp_forward(F, h.data(), rt.mlp[j]);
-    const std::vector<double>& out = rt.mlp[j].a[F.n_layers];
-    rt.sigma[j] = softplus(out[0]);
-    for (int k = 0; k < C; ++k) rt.c[j][k] = sigmoid(out[1 + k]);
+    if (F.dir_freqs > 0) {   // sigma = g_sigma(h), c = g_v(h, direnc(d))
+      mlp_forward(Fs, h.data(), rt.mlp[j]);
+      for (int k = 0; k < F.K; ++k) hv[k] = h[k];
+      for (size_t k = 0; k < rt.e.size(); ++k) hv[F.K + k] = rt.e[k];
+      mlp_forward(Fv, hv.data(), rt.mlpv[j]);
+      rt.sigma[j] = softplus(rt.mlp[j].a[F.n_layers][0]);
+      for (int k = 0; k < C; ++k) rt.c[j][k] = sigmoid(rt.mlpv[j].a[F.n_layers][k]);
+    } else {
+      mlp_forward(F, h.data(), rt.mlp[j]);
+      const std::vector<double>& out = rt.mlp[j].a[F.n_layers];
+      rt.sigma[j] = softplus(out[0]);
+      for (int k = 0; k < C; ++k) rt.c[j][k] = sigmoid(out[1 + k]);
+    }
     double ds = rt.delta * rt.sigma[j];
     rt.tau[j] = tau_prev + ds;
     rt.T[j] = std::exp(-rt.tau[j]);
@@ -315,18 +377,39 @@ void backward_ray(const Field& F, const RayTrace& rt, const double* bg, const do
     }
   }
   std::vector<double> dout(1 + C), dh(F.K);
+  Field Fs, Fv;
+  std::vector<double> dhv, dsv;
+  int64_t nsig = 0;
+  if (F.dir_freqs > 0) {
+    split_nets(F, Fs, Fv);
+    nsig = net_params(F.n_layers, Fs.widths);
+    dhv.assign(F.K + 6 * F.dir_freqs, 0.0);
+    dsv.assign(F.K + 6 * F.dir_freqs, 0.0);
+  }
   for (int q = 0; q < S; ++q) {
-    const std::vector<double>& o = rt.mlp[q].a[F.n_layers];
-    dout[0] = dsig[q] * sigmoid(o[0]);  // softplus' = sigmoid
+    const double o0 = rt.mlp[q].a[F.n_layers][0];   // density logit (g_sigma's output when split)
+    dout[0] = dsig[q] * sigmoid(o0);  // softplus' = sigmoid
     for (int k = 0; k < C; ++k) {
       double dc = (q >= 1) ? rt.w[q] * p[k] : 0.0;
       dout[1 + k] = dc * rt.c[q][k] * (1.0 - rt.c[q][k]);
     }
-    mlp_backward(F, rt.mlp[q], dout.data(), grad_params, dh.data());
+    if (F.dir_freqs > 0) {   // dL/dh = g_sigma VJP + the h part of the g_v VJP (direnc gets none)
+      mlp_backward(Fs, rt.mlp[q], dout.data(), grad_params, dh.data());
+      mlp_backward(Fv, rt.mlpv[q], dout.data() + 1, grad_params + nsig, dhv.data());
+      for (int k = 0; k < F.K; ++k) dh[k] += dhv[k];
+    } else {
+      mlp_backward(F, rt.mlp[q], dout.data(), grad_params, dh.data());
+    }
     scatter(F, rt.taps[q], dh.data(), grad_planes);
     if (slack_params) {
       std::vector<double> ds(F.K);
-      mlp_slack(F, rt.mlp[q], dout.data(), band, slack_params, ds.data());
+      if (F.dir_freqs > 0) {
+        mlp_slack(Fs, rt.mlp[q], dout.data(), band, slack_params, ds.data());
+        mlp_slack(Fv, rt.mlpv[q], dout.data() + 1, band, slack_params + nsig, dsv.data());
+        for (int k = 0; k < F.K; ++k) ds[k] += dsv[k];
+      } else {
+        mlp_slack(F, rt.mlp[q], dout.data(), band, slack_params, ds.data());
+      }
       scatter(F, rt.taps[q], ds.data(), slack_planes);
     }
   }
@@ -397,8 +480,9 @@ void mlp_slack(const Field& F, const MlpTrace& tr, const double* dout, double ba
 
 Field make_field(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
                  int n_layers, const int* widths, const double* params, int contraction = 0,
-                 double contract_a = 1.0) {
+                 double contract_a = 1.0, int dir_freqs = 0) {
   Field F;
+  F.dir_freqs = dir_freqs;
   F.contraction = contraction;
   F.contract_a = contract_a;
   F.kind = kind;
@@ -500,9 +584,10 @@ int lpo_render_forward(int kind, int H, int W, int D, int K, const double* p0, c
                        int n_layers, const int* widths, const double* params, int64_t r0, int64_t r1,
                        const double* origins, const double* dirs, const double* nearv, const double* farv, int S,
                        const double* bg, double* out, double* tau_out, double* depth_out, int contraction,
-                       double contract_a) {
+                       double contract_a, int dir_freqs) {
   if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
-  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a);
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a,
+                       dir_freqs);
   const int C = widths[n_layers] - 1;
   RayTrace rt;
   for (int64_t r = r0; r < r1; ++r) {
@@ -519,9 +604,10 @@ int lpo_render_backward(int kind, int H, int W, int D, int K, const double* p0, 
                         const double* origins, const double* dirs, const double* nearv, const double* farv, int S,
                         const double* bg, const double* grad_out, const double* grad_tau, double* g0, double* g1,
                         double* g2, double* grad_params, int mode, const double* grad_depth, int contraction,
-                        double contract_a) {
+                        double contract_a, int dir_freqs) {
   if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
-  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a);
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a,
+                       dir_freqs);
   const int C = widths[n_layers] - 1;
   double* g[3] = {g0, g1, g2};
   RayTrace rt;
@@ -540,9 +626,10 @@ int lpo_render_relu_slack(int kind, int H, int W, int D, int K, const double* p0
                           int64_t r1, const double* origins, const double* dirs, const double* nearv,
                           const double* farv, int S, const double* bg, const double* grad_out,
                           const double* grad_tau, double band, double* s0, double* s1, double* s2,
-                          double* slack_params, const double* grad_depth, int contraction, double contract_a) {
+                          double* slack_params, const double* grad_depth, int contraction, double contract_a, int dir_freqs) {
   if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
-  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a);
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a,
+                       dir_freqs);
   const int C = widths[n_layers] - 1;
   double* sg[3] = {s0, s1, s2};
   int64_t np = 0;
@@ -653,9 +740,10 @@ int lpo_splat_rays_backward(int kind, int H, int W, int D, int K, int64_t r0, in
 int lpo_trace(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
               int n_layers, const int* widths, const double* params, const double* origin, const double* dir,
               double nearv, double farv, int S, double* sigma, double* tau, double* T, double* w, double* c,
-              int contraction, double contract_a) {
+              int contraction, double contract_a, int dir_freqs) {
   if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
-  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a);
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a,
+                       dir_freqs);
   const int C = widths[n_layers] - 1;
   RayTrace rt;
   trace_ray(F, origin, dir, nearv, farv, S, rt);
@@ -678,29 +766,40 @@ int lpo_trace(int kind, int H, int W, int D, int K, const double* p0, const doub
 int lpo_render_min_preact(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
                           int n_layers, const int* widths, const double* params, int64_t r0, int64_t r1,
                           const double* origins, const double* dirs, const double* nearv, const double* farv, int S,
-                          double* min_rel, int contraction, double contract_a) {
+                          double* min_rel, int contraction, double contract_a, int dir_freqs) {
   if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
-  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a);
+  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a,
+                       dir_freqs);
   RayTrace rt;
   for (int64_t r = r0; r < r1; ++r) {
     trace_ray(F, origins + 3 * r, dirs + 3 * r, nearv[r], farv[r], S, rt);
     double best = INFINITY;
-    for (int j = 0; j < S; ++j) {
-      const double* p = F.params;
-      for (int l = 0; l < n_layers - 1; ++l) {
-        int fin = widths[l], fout = widths[l + 1];
-        const double* Wl = p;
-        const double* bl = p + (int64_t)fout * fin;
-        p = bl + fout;
-        for (int i = 0; i < fout; ++i) {
-          double sc = std::fabs(bl[i]);
-          for (int k = 0; k < fin; ++k) sc += std::fabs(Wl[(int64_t)i * fin + k] * rt.mlp[j].a[l][k]);
-          if (sc > 0.0) {
-            double q = std::fabs(rt.mlp[j].z[l][i]) / sc;
-            if (q < best) best = q;
+    auto scan = [&](const Field& N, const std::vector<MlpTrace>& trs) {
+      for (int j = 0; j < S; ++j) {
+        const double* p = N.params;
+        for (int l = 0; l < n_layers - 1; ++l) {
+          int fin = N.widths[l], fout = N.widths[l + 1];
+          const double* Wl = p;
+          const double* bl = p + (int64_t)fout * fin;
+          p = bl + fout;
+          for (int i = 0; i < fout; ++i) {
+            double sc = std::fabs(bl[i]);
+            for (int k = 0; k < fin; ++k) sc += std::fabs(Wl[(int64_t)i * fin + k] * trs[j].a[l][k]);
+            if (sc > 0.0) {
+              double q = std::fabs(trs[j].z[l][i]) / sc;
+              if (q < best) best = q;
+            }
           }
         }
       }
+    };
+    if (dir_freqs > 0) {
+      Field Fs, Fv;
+      split_nets(F, Fs, Fv);
+      scan(Fs, rt.mlp);
+      scan(Fv, rt.mlpv);
+    } else {
+      scan(F, rt.mlp);
     }
     min_rel[r - r0] = best;
   }

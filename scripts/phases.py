@@ -10,7 +10,7 @@ cfg = wl.get_config(sys.argv[1] if len(sys.argv) > 1 else "c4")
 M = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 20
 o, d, n, f = wl.make_rays(cfg, start=0, count=M)
 T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
-field = lpb.Field(cfg.kind, [T(g) for g in wl.make_grid(cfg)], cfg.widths, T(wl.make_mlp(cfg.widths)))
+field = lpb.Field(cfg.kind, [T(g) for g in wl.make_grid(cfg)], cfg.widths, T(wl.make_params(cfg)))
 o, d, n, f = T(o), T(d), T(n), T(f)
 go = T(wl.make_grad_out(np.arange(M), cfg.C))
 fn = _lib.lib.lp_debug_phase_cycles

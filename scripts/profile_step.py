@@ -29,7 +29,7 @@ def main():
     o, d, n, f = wl.make_rays(cfg, start=start, count=M)
     dev = "cuda"
     T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)
-    field = lpb.Field(cfg.kind, [T(g) for g in wl.make_grid(cfg)], cfg.widths, T(wl.make_mlp(cfg.widths)),
+    field = lpb.Field(cfg.kind, [T(g) for g in wl.make_grid(cfg)], cfg.widths, T(wl.make_params(cfg)),
                       cfg.contraction, cfg.contract_a)
     o, d, n, f = T(o), T(d), T(n), T(f)
     go = T(wl.make_grad_out(np.arange(start, start + M), cfg.C))

@@ -25,7 +25,7 @@ def problem_np(cfg_name: str, idx=None, n: int = 2048, sigma_bias=None, with_gta
     idx = np.asarray(idx, dtype=np.int64)
     o, d, near, far = wl.make_rays(cfg, idx)
     return dict(
-        cfg=cfg, idx=idx, grid=grid_np(cfg_name), params=wl.make_mlp(cfg.widths, sigma_bias=sigma_bias),
+        cfg=cfg, idx=idx, grid=grid_np(cfg_name), params=wl.make_params(cfg, sigma_bias=sigma_bias),
         o=o, d=d, near=near, far=far, bg=wl.make_bg(cfg.C, zero=zero_bg), go=wl.make_grad_out(idx, cfg.C),
         gt=wl.make_grad_tau(idx) if with_gtau else None,
         gd=wl.make_grad_tau(idx, seed=6) if with_gdepth else None)
@@ -45,7 +45,8 @@ def to_cuda(pb, device="cuda"):
 def oracle_field(pb):
     import oracle
     cfg = pb["cfg"]
-    return oracle.Field(cfg.kind, pb["grid"], cfg.widths, pb["params"], cfg.contraction, cfg.contract_a)
+    return oracle.Field(cfg.kind, pb["grid"], cfg.widths, pb["params"], cfg.contraction, cfg.contract_a,
+                        cfg.dir_freqs)
 
 
 def oracle_rays(pb):

@@ -246,3 +246,150 @@ def test_depth_backward_eq3_equals_literal_derivative():
     b = oracle.render_backward(F, rays, p, None, None, mode=1, grad_depth=gd)
     for u, v in zip(a[0] + [a[1]], b[0] + [b[1]]):
         assert rel_inf(u, v) < 1e-12
+
+
+# ---------------------------------------------------------------- view-dependent colour (row 1)
+def _vd_field(kind=wl.TRIPLANE, dims=(4, 5, 6), K=3, hid=5, F=2, seed=61, sigma_bias=0.5, contraction=0):
+    cfg = wl.Config("t", kind, 4, K, (K, hid, 4), 1, 1, 2, dir_freqs=F)
+    grid, _ = tiny_field_arrays(kind, dims, K, (K, hid, 4), seed=seed)
+    params = wl.make_params(cfg, seed=seed + 1, sigma_bias=sigma_bias).astype(np.float64)
+    # nonzero hidden biases so that ReLU decisions vary
+    params = params + 0.1 * wl.counter_uniform(seed + 2, np.arange(params.size, dtype=np.uint64), -1, 1)
+    return oracle.Field(kind, grid, (K, hid, 4), params, contraction, 0.7, F), cfg
+
+
+def test_direnc_through_a_probe_network():
+    """g_v's colour logit k reads one direnc entry through an identity-like path, so
+    c_k = sigmoid(sin / cos(pi 2^i d_a)) exactly (per axis, per frequency
+    2^0..2^{F-1}, sin then cos)."""
+    K, hid, F = 2, 4, 3
+    E = 6 * F
+    grid = [np.zeros((3, 3, 3, K))]
+    nsig = hid * K + hid + hid + 1
+    wcol_in = K + E
+    p = np.zeros(nsig + hid * wcol_in + hid + 3 * hid + 3)
+    Wv0 = np.zeros((hid, wcol_in))
+    bv0 = np.full(hid, 10.0)                     # keep z > 0: relu is the identity (+10)
+    probes = [(0, 0, "sin"), (1, 2, "cos"), (2, 1, "sin")]   # (axis, freq index, fn) -> colour 0, 1, 2
+    for c, (ax, i, fn) in enumerate(probes):
+        Wv0[c, K + 2 * (ax * F + i) + (0 if fn == "sin" else 1)] = 1.0
+    Wv1 = np.zeros((3, hid))
+    for c in range(3):
+        Wv1[c, c] = 1.0
+    bv1 = np.full(3, -10.0)
+    p[nsig:] = np.concatenate([Wv0.ravel(), bv0, Wv1.ravel(), bv1])
+    Fd = oracle.Field(wl.VOXEL, grid, (K, hid, 4), p, 0, 1.0, F)
+    d = np.array([0.3, -0.5, 0.81])
+    d /= np.linalg.norm(d)
+    sigma, tau, T, w, col = oracle.trace(Fd, np.array([0.1, 0.2, -3.0]), d, 0.5, 5.0, 4)
+    for c, (ax, i, fn) in enumerate(probes):
+        v = (np.sin if fn == "sin" else np.cos)(np.pi * 2.0 ** i * d[ax])
+        assert np.max(np.abs(col[:, c] - 1.0 / (1.0 + np.exp(-v)))) < 1e-13
+
+
+def test_density_is_view_independent():
+    """sigma = g_sigma(h) only: the same points traversed in opposite directions get
+    the same densities (in reverse order); the colours differ."""
+    Fd, _ = _vd_field(kind=wl.VOXEL, dims=(3, 4, 5))
+    a, b = np.array([-0.7, -0.2, 0.5]), np.array([0.6, 0.4, -0.5])
+    L = np.linalg.norm(b - a)
+    d = (b - a) / L
+    s1, _, _, _, c1 = oracle.trace(Fd, a, d, 0.0, L, 9)
+    s2, _, _, _, c2 = oracle.trace(Fd, b, -d, 0.0, L, 9)
+    assert np.max(np.abs(s1 - s2[::-1])) < 1e-12
+    assert np.max(np.abs(c1 - c2[::-1])) > 1e-3
+
+
+@pytest.mark.parametrize("kind,contraction", [(wl.TRIPLANE, 0), (wl.VOXEL, 1)])
+def test_view_dependent_backward_matches_finite_differences(kind, contraction):
+    dims = (4, 5, 6) if kind == wl.TRIPLANE else (3, 4, 5)
+    F, _ = _vd_field(kind, dims, contraction=contraction)
+    o, d, near, far = tiny_rays(6)
+    rays = oracle.Rays(o, d, near, far * (2.0 if contraction else 1.0), 9)
+    p = wl.counter_uniform(71, np.arange(18, dtype=np.uint64), -1, 1).reshape(6, 3).astype(np.float64)
+    gt = wl.counter_uniform(72, np.arange(6, dtype=np.uint64), -1, 1).astype(np.float64)
+    gd = wl.counter_uniform(73, np.arange(6, dtype=np.uint64), -1, 1).astype(np.float64)
+    bg = np.array([0.2, 0.9, 0.5])
+    gg, gp = oracle.render_backward(F, rays, p, gt, bg, grad_depth=gd)
+    eps = 1e-6
+    for gi, g in enumerate(F.grid):
+        flat = g.reshape(-1)
+        fd = np.zeros(flat.size)
+        for i in range(flat.size):
+            v = flat[i]
+            flat[i] = v + eps
+            lp = _loss(F, rays, p, gt, gd, bg)
+            flat[i] = v - eps
+            lm = _loss(F, rays, p, gt, gd, bg)
+            flat[i] = v
+            fd[i] = (lp - lm) / (2 * eps)
+        assert np.max(np.abs(fd)) > 1e-3
+        assert rel_inf(gg[gi].reshape(-1), fd) < 1e-6
+    fd = np.zeros_like(F.params)
+    for i in range(F.params.size):
+        v = F.params[i]
+        F.params[i] = v + eps
+        lp = _loss(F, rays, p, gt, gd, bg)
+        F.params[i] = v - eps
+        lm = _loss(F, rays, p, gt, gd, bg)
+        F.params[i] = v
+        fd[i] = (lp - lm) / (2 * eps)
+    assert rel_inf(gp, fd) < 1e-6
+    a = oracle.render_backward(F, rays, p, gt, bg, mode=1, grad_depth=gd)
+    for u, v in zip(gg + [gp], a[0] + [a[1]]):
+        assert rel_inf(u, v) < 1e-12
+
+
+def test_view_dependent_matches_torch_autograd():
+    """The two networks, direnc and Eq. 1 written independently in torch fp64
+    (grid_sample for h, the literal T_{j-1} - T_j weights): forward and all
+    gradients agree with the oracle."""
+    torch = pytest.importorskip("torch")
+    K, hid, Fq = 3, 5, 2
+    F, _ = _vd_field(wl.TRIPLANE, (4, 5, 6), K, hid, Fq)
+    o, d, near, far = tiny_rays(6, inside_start=True)
+    S = 9
+    rays = oracle.Rays(o, d, near, far, S)
+    p = wl.counter_uniform(74, np.arange(18, dtype=np.uint64), -1, 1).reshape(6, 3).astype(np.float64)
+    out_o, _ = oracle.render_forward(F, rays, None)
+    gg, gp = oracle.render_backward(F, rays, p, None, None)
+
+    planes = [torch.tensor(g, dtype=torch.float64, requires_grad=True) for g in F.grid]
+    params = torch.tensor(F.params, dtype=torch.float64, requires_grad=True)
+    od, dd = torch.tensor(o, dtype=torch.float64), torch.tensor(d, dtype=torch.float64)
+    Dl = (torch.tensor(far, dtype=torch.float64) - torch.tensor(near, dtype=torch.float64)) / (S - 1)
+    t = torch.tensor(near, dtype=torch.float64)[:, None] + torch.arange(S, dtype=torch.float64)[None] * Dl[:, None]
+    x = od[:, None, :] + t[..., None] * dd[:, None, :]
+
+    def bil(plane, a, b):
+        inp = plane.permute(2, 0, 1)[None]
+        g = torch.stack([b, a], dim=-1)[None]
+        return torch.nn.functional.grid_sample(inp, g, mode="bilinear", align_corners=True)[0].permute(1, 2, 0)
+
+    h = bil(planes[0], x[..., 0], x[..., 1]) + bil(planes[1], x[..., 1], x[..., 2]) + bil(planes[2], x[..., 2], x[..., 0])
+    freqs = torch.tensor([2.0 ** i for i in range(Fq)], dtype=torch.float64)
+    ang = torch.pi * dd[:, :, None] * freqs[None, None, :]                  # [M][3][F]
+    e = torch.stack([torch.sin(ang), torch.cos(ang)], dim=-1).reshape(len(o), 6 * Fq)
+    E = 6 * Fq
+    n = 0
+
+    def take(*shape):
+        nonlocal n
+        cnt = int(np.prod(shape))
+        v = params[n:n + cnt].reshape(*shape)
+        n += cnt
+        return v
+    Ws0, bs0, Ws1, bs1 = take(hid, K), take(hid), take(1, hid), take(1)
+    Wv0, bv0, Wv1, bv1 = take(hid, K + E), take(hid), take(3, hid), take(3)
+    assert n == params.numel()
+    sig = torch.nn.functional.softplus((torch.relu(h @ Ws0.T + bs0) @ Ws1.T + bs1)[..., 0])
+    hv = torch.cat([h, e[:, None, :].expand(-1, S, -1)], dim=-1)
+    col = torch.sigmoid(torch.relu(hv @ Wv0.T + bv0) @ Wv1.T + bv1)
+    T = torch.exp(-torch.cumsum(Dl[:, None] * sig, dim=1))
+    wgt = T[:, :-1] - T[:, 1:]
+    out = (wgt[..., None] * col[:, 1:]).sum(1)
+    assert rel_inf(out.detach().numpy(), out_o) < 1e-12
+    (out * torch.tensor(p)).sum().backward()
+    for a, b in zip(gg, planes):
+        assert rel_inf(a, b.grad.numpy()) < 1e-10
+    assert rel_inf(gp, params.grad.numpy()) < 1e-10

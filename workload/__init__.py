@@ -38,7 +38,7 @@ import numpy as np
 
 __all__ = [
     "Config", "CONFIGS", "get_config", "counter_uniform", "make_grid",
-    "make_mlp", "make_rays", "make_bg", "make_grad_out", "make_grad_tau", "make_features", "make_grid_grad",
+    "make_mlp", "make_params", "n_params", "make_rays", "make_bg", "make_grad_out", "make_grad_tau", "make_features", "make_grid_grad",
     "camera_positions", "softplus_inv", "subset_indices",
 ]
 
@@ -93,6 +93,7 @@ class Config:
     contract_a: float = 1.0   # contraction scale a
     near_far: Optional[tuple] = None   # constant (near, far) for every ray (unbounded scenes)
     op: str = "render"        # "render" (the renderer) or "splat" (the Splatter: widths unused)
+    dir_freqs: int = 0        # F > 0: view-dependent colour, g_sigma(h) and g_v(h, direnc(d))
 
     @property
     def n_rays(self) -> int:
@@ -143,6 +144,13 @@ CONFIGS = {
                  "unbounded scene: triplane 3x160x160 C=32, 3-layer MLP, 16 views at 256x256, "
                  "384 samples/ray, per-axis contraction a=1", contraction=1, contract_a=1.0,
                  near_far=(0.05, 12.0)),
+    # View-dependent colour: sigma = g_sigma(h),
+    # c = g_v(h, direnc(d)) with F = 4 direction frequencies, each network
+    # with the config's hidden width (reading R29).
+    "c1v": Config("c1v", TRIPLANE, 16, 8, (8, 16, 4), 1, 64, 32,
+                  "c1 with view-dependent colour g_v(h, direnc(d)), F = 4", dir_freqs=4),
+    "c4v": Config("c4v", TRIPLANE, 256, 32, (32, 64, 4), 128, 256, 128,
+                  "c4 with view-dependent colour g_v(h, direnc(d)), F = 4", dir_freqs=4),
     # Splatter benchmark shape: N input feature maps lifted into a 160^3 voxel
     # grid, MLPs off; 32-channel features, 160 points per ray. N = 64 maps
     # of 128x128 pixels (the text gives neither N nor the map size: reading R28).
@@ -205,6 +213,27 @@ def make_mlp(widths: Sequence[int], seed: int = 1, sigma_bias: Optional[float] =
             b[0] = np.float32(sigma_bias)
         parts += [W.reshape(-1), b]
     return np.concatenate(parts).astype(np.float32)
+
+
+def make_params(cfg: Config, seed: int = 1, sigma_bias: Optional[float] = None) -> np.ndarray:
+    """The field's MLP parameters: one network (make_mlp), or for view-dependent
+    configs (dir_freqs = F > 0) g_sigma with widths (K, hidden..., 1) followed by
+    g_v with widths (K + 6F, hidden..., C) (reading R29)."""
+    if not cfg.dir_freqs:
+        return make_mlp(cfg.widths, seed=seed, sigma_bias=sigma_bias)
+    w = list(cfg.widths)
+    wsig = w[:-1] + [1]
+    wcol = [w[0] + 6 * cfg.dir_freqs] + w[1:-1] + [w[-1] - 1]
+    return np.concatenate([make_mlp(wsig, seed=seed, sigma_bias=sigma_bias),
+                           make_mlp(wcol, seed=seed + 100, sigma_bias=0.0)]).astype(np.float32)
+
+
+def n_params(cfg: Config) -> int:
+    w = list(cfg.widths)
+    if not cfg.dir_freqs:
+        return cfg.n_params
+    cnt = lambda ws: sum(ws[i + 1] * ws[i] + ws[i + 1] for i in range(len(ws) - 1))
+    return int(cnt(w[:-1] + [1]) + cnt([w[0] + 6 * cfg.dir_freqs] + w[1:-1] + [w[-1] - 1]))
 
 
 def camera_positions(views: int, radius: float = 4.0) -> np.ndarray:
