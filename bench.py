@@ -253,7 +253,7 @@ def run_ours(args):
     grid = wl.make_grid(cfg)
     params = torch.from_numpy(wl.make_params(cfg)).to(dev)
     planes = [torch.from_numpy(g).to(dev) for g in grid]
-    field = lpb.Field(cfg.kind, planes, cfg.widths, params, cfg.contraction, cfg.contract_a)
+    field = lpb.Field(cfg.kind, planes, cfg.widths, params, cfg.contraction, cfg.contract_a, cfg.dir_freqs)
     grads = FlatGrads([p.shape for p in planes] + [params.shape], device=dev)
     flat = grads.flat
     gplanes, gparams = grads.views[:-1], grads.views[-1]

@@ -90,11 +90,18 @@ typedef struct {
  * widths[0] = K, widths[n_layers] = 1 + C (output 0 = density logit, then C
  * colour logits). params packs, per layer l, W_l as [widths[l+1]][widths[l]]
  * row-major then b_l [widths[l+1]]. Compiled widths:
- * (8,16,4), (16,32,4), (32,64,4) and (32,64,64,4). */
+ * (8,16,4), (16,32,4), (32,64,4) and (32,64,64,4).
+ * dir_freqs = F > 0 selects the view-dependent field of P:249-250 (reading
+ * R29): two networks with the hidden widths of `widths`, g_sigma: K -> H -> 1
+ * and g_v: K + 6F -> H -> C fed [h, direnc(d)], direnc(d) = per axis k, per
+ * frequency 2^i (i < F): sin(pi 2^i d_k), cos(pi 2^i d_k). params packs g_sigma
+ * then g_v, each as above. Compiled: one hidden layer, (K, H) = (8, 16) or
+ * (32, 64), F <= 5. */
 typedef struct {
   int32_t n_layers;
   int32_t widths[LP_MAX_LAYERS + 1];
   const float* params;
+  int32_t dir_freqs;
 } lp_mlp;
 
 /* The M rays r_i with R+1 = n_samples equispaced points each.

@@ -33,7 +33,7 @@ class LpGrid(ctypes.Structure):
 
 class LpMlp(ctypes.Structure):
     _fields_ = [("n_layers", ctypes.c_int32), ("widths", ctypes.c_int32 * (LP_MAX_LAYERS + 1)),
-                ("params", ctypes.c_void_p)]
+                ("params", ctypes.c_void_p), ("dir_freqs", ctypes.c_int32)]
 
 
 class LpRays(ctypes.Structure):
@@ -92,8 +92,9 @@ def make_grid(kind: int, H: int, W: int, D: int, K: int, ptrs, contraction: int 
     return g
 
 
-def make_mlp(widths, params_ptr) -> LpMlp:
+def make_mlp(widths, params_ptr, dir_freqs: int = 0) -> LpMlp:
     m = LpMlp()
+    m.dir_freqs = int(dir_freqs)
     m.n_layers = len(widths) - 1
     for i, w in enumerate(widths):
         m.widths[i] = int(w)

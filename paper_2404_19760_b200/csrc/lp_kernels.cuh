@@ -37,6 +37,7 @@ struct KernelArgs {
   float* depth;          // fwd: [M] expected depth sum_j w_j t_j, or null
   const float* grad_depth;  // bwd: [M] or null
   Contract contract;     // sample-point contraction (mode 0 = none)
+  int dir_freqs;         // F > 0: view-dependent field (lp_tcv_kernels.cuh)
   unsigned long long* dbg;  // debug phase timers (LP_PHASES variant builds only), else null
 };
 

@@ -6,6 +6,7 @@
 
 #include "lp_internal.h"
 #include "lp_tc2_kernels.cuh"
+#include "lp_tcv_kernels.cuh"
 
 namespace lpi {
 
@@ -133,6 +134,21 @@ lp_status run_bwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
   }
   static LaunchShape shape;
   return launch(lp::lp_bwd_kernel<KIND, K, HID, NH>, shape, lp::bwd_smem_bytes<K, HID, NH>(), 128, 1, a.M, a, w, s);
+}
+
+// View-dependent fields (one hidden layer per network): K1tcv / K2tcv.
+template <int KIND, int K, int HID>
+lp_status run_fwd_vd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
+  static LaunchShape shape;
+  constexpr int G = 2;
+  return launch(lp::lp_fwd_tcv_kernel<KIND, K, HID, G>, shape, lp::FwdTcvSmem<KIND, K, HID, G>::BYTES, 256 * G, G,
+                a.M, a, w, s);
+}
+template <int KIND, int K, int HID>
+lp_status run_bwd_vd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
+  static LaunchShape shape;
+  return launch(lp::lp_bwd_tcv_kernel<KIND, K, HID>, shape, lp::BwdTcvSmem<KIND, K, HID>::BYTES, 256, 1, a.M, a, w,
+                s);
 }
 
 }  // namespace lpi

@@ -58,6 +58,7 @@ class Field:
     params: torch.Tensor
     contraction: int = CONTRACT_NONE
     contract_scale: float = 1.0
+    dir_freqs: int = 0          # F > 0: view-dependent field g_sigma(h), g_v(h, direnc(d)) (include/lp.h)
 
     def __post_init__(self):
         if self.kind == TRIPLANE:
@@ -78,7 +79,12 @@ class Field:
         self.H, self.W, self.D, self.K = int(H), int(W), int(D), int(K)
         self.widths = tuple(int(w) for w in self.widths)
         _req(self.params, "params")
-        n = sum(self.widths[i + 1] * self.widths[i] + self.widths[i + 1] for i in range(len(self.widths) - 1))
+        cnt = lambda w: sum(w[i + 1] * w[i] + w[i + 1] for i in range(len(w) - 1))
+        if self.dir_freqs:
+            w = list(self.widths)
+            n = cnt(w[:-1] + [1]) + cnt([w[0] + 6 * self.dir_freqs] + w[1:-1] + [w[-1] - 1])
+        else:
+            n = cnt(self.widths)
         if self.params.numel() != n:
             raise ValueError(f"params has {self.params.numel()} elements, widths {self.widths} need {n}")
         self.C = self.widths[-1] - 1
@@ -90,7 +96,7 @@ class Field:
 
     def c_mlp(self, params=None) -> _lib.LpMlp:
         params = self.params if params is None else params
-        return _lib.make_mlp(self.widths, params.data_ptr())
+        return _lib.make_mlp(self.widths, params.data_ptr(), self.dir_freqs)
 
 
 def _c_rays(origins, dirs, near, far, n_samples) -> _lib.LpRays:
@@ -155,8 +161,8 @@ def render_backward(field: Field, origins, dirs, near, far, n_samples: int, tau,
 class _RenderFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, geom, n_samples, origins, dirs, near, far, bg, params, *planes):
-        kind, widths, contraction, cscale = geom
-        field = Field(kind, list(planes), widths, params, contraction, cscale)
+        kind, widths, contraction, cscale, dfreq = geom
+        field = Field(kind, list(planes), widths, params, contraction, cscale, dfreq)
         out, tau, depth = render_forward(field, origins, dirs, near, far, n_samples, bg, return_depth=True)
         ctx.save_for_backward(origins, dirs, near, far, bg if bg is not None else torch.empty(0), params, tau,
                               *planes)
@@ -165,9 +171,9 @@ class _RenderFn(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, grad_out, grad_tau, grad_depth):
-        (kind, widths, contraction, cscale), n_samples, has_bg = ctx.meta
+        (kind, widths, contraction, cscale, dfreq), n_samples, has_bg = ctx.meta
         origins, dirs, near, far, bg, params, tau, *planes = ctx.saved_tensors
-        field = Field(kind, list(planes), widths, params, contraction, cscale)
+        field = Field(kind, list(planes), widths, params, contraction, cscale, dfreq)
         go = grad_out.contiguous() if grad_out is not None else torch.zeros((origins.shape[0], field.C),
                                                                            device=origins.device)
         gt = grad_tau.contiguous() if grad_tau is not None else None
@@ -181,7 +187,8 @@ def render(field: Field, origins, dirs, near, far, n_samples: int, bg=None, retu
     """Differentiable fused render: returns (out [M][C], tau [M]) -- and the
     expected depth [M] with return_depth; gradients flow to field.params and
     field.planes (not to rays, near/far or bg)."""
-    geom = (field.kind, tuple(field.widths), int(field.contraction), float(field.contract_scale))
+    geom = (field.kind, tuple(field.widths), int(field.contraction), float(field.contract_scale),
+            int(field.dir_freqs))
     out, tau, depth = _RenderFn.apply(geom, int(n_samples), origins, dirs, near, far, bg, field.params,
                                       *field.planes)
     return (out, tau, depth) if return_depth else (out, tau)

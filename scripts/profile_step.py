@@ -30,7 +30,7 @@ def main():
     dev = "cuda"
     T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)
     field = lpb.Field(cfg.kind, [T(g) for g in wl.make_grid(cfg)], cfg.widths, T(wl.make_params(cfg)),
-                      cfg.contraction, cfg.contract_a)
+                      cfg.contraction, cfg.contract_a, cfg.dir_freqs)
     o, d, n, f = T(o), T(d), T(n), T(f)
     go = T(wl.make_grad_out(np.arange(start, start + M), cfg.C))
     gp = [torch.zeros_like(p) for p in field.planes]

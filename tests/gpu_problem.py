@@ -37,7 +37,7 @@ def to_cuda(pb, device="cuda"):
     cfg = pb["cfg"]
     T = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(device)
     field = lpb.Field(cfg.kind, [T(g) for g in pb["grid"]], cfg.widths, T(pb["params"]), cfg.contraction,
-                      cfg.contract_a)
+                      cfg.contract_a, cfg.dir_freqs)
     return field, dict(o=T(pb["o"]), d=T(pb["d"]), near=T(pb["near"]), far=T(pb["far"]), bg=T(pb["bg"]),
                        go=T(pb["go"]), gt=T(pb["gt"]), gd=T(pb.get("gd")))
 

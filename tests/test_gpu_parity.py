@@ -245,3 +245,40 @@ def test_autograd_render_depth_contracted(torch_cuda):
     g = dict(out=out.detach().cpu().numpy(), tau=tau.detach().cpu().numpy(), depth=depth.detach().cpu().numpy(),
              gplanes=[p.grad.cpu().numpy() for p in field.planes], gparams=field.params.grad.cpu().numpy())
     _assert(_compare(g, r))
+
+
+# view-dependent colour, sigma = g_sigma(h), c = g_v(h, direnc(d))
+# on the K1tcv / K2tcv kernels, with depth and contraction riding along.
+VD_CASES = [("c1v", 2048, {}), ("c4v", 1024, {}), ("c1v", 1024, dict(kind=wl.VOXEL)),
+            ("c4v", 512, dict(contraction=1, contract_a=1.0, near_far=(0.05, 9.0)))]
+
+
+@pytest.mark.parametrize("cfg,n,over", VD_CASES)
+def test_parity_view_dependent(torch_cuda, cfg, n, over):
+    import dataclasses
+    pb = problem_np(cfg, n=n, with_gdepth=True)
+    if over:
+        pb["cfg"] = dataclasses.replace(pb["cfg"], **over)
+        if "kind" in over:
+            pb["grid"] = wl.make_grid(pb["cfg"])
+        if "near_far" in over:
+            pb["near"] = np.full_like(pb["near"], over["near_far"][0])
+            pb["far"] = np.full_like(pb["far"], over["near_far"][1])
+    g = _gpu_fwd_bwd(torch_cuda, pb, depth=True)
+    r = oracle_reference(pb, depth=True)
+    _assert(_compare(g, r))
+
+
+def test_autograd_view_dependent(torch_cuda):
+    import paper_2404_19760_b200 as lpb
+    pb = problem_np("c1v", n=2048)
+    field, t = to_cuda(pb)
+    field.params.requires_grad_(True)
+    for p in field.planes:
+        p.requires_grad_(True)
+    out, tau = lpb.render(field, t["o"], t["d"], t["near"], t["far"], pb["cfg"].S, t["bg"])
+    ((out * t["go"]).sum() + (tau * t["gt"]).sum()).backward()
+    r = oracle_reference(pb)
+    g = dict(out=out.detach().cpu().numpy(), tau=tau.detach().cpu().numpy(),
+             gplanes=[p.grad.cpu().numpy() for p in field.planes], gparams=field.params.grad.cpu().numpy())
+    _assert(_compare(g, r))
