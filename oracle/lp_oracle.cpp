@@ -633,7 +633,13 @@ int lpo_render_relu_slack(int kind, int H, int W, int D, int K, const double* p0
   const int C = widths[n_layers] - 1;
   double* sg[3] = {s0, s1, s2};
   int64_t np = 0;
-  for (int l = 0; l < n_layers; ++l) np += (int64_t)widths[l + 1] * widths[l] + widths[l + 1];
+  if (dir_freqs > 0) {   // g_sigma then g_v (split_nets)
+    Field Fs, Fv;
+    split_nets(F, Fs, Fv);
+    np = net_params(n_layers, Fs.widths) + net_params(n_layers, Fv.widths);
+  } else {
+    np = net_params(n_layers, widths);
+  }
   std::vector<double> gp(np, 0.0);
   std::vector<std::vector<double>> gg(3);
   double* gptr[3] = {nullptr, nullptr, nullptr};

@@ -393,3 +393,17 @@ def test_view_dependent_matches_torch_autograd():
     for a, b in zip(gg, planes):
         assert rel_inf(a, b.grad.numpy()) < 1e-10
     assert rel_inf(gp, params.grad.numpy()) < 1e-10
+
+
+def test_view_dependent_relu_slack_runs_and_bounds():
+    """relu_slack on a view-dependent field: buffers sized for both networks, slack >= 0,
+    and zero slack when no pre-activation is ambiguous (band = 0)."""
+    F, _ = _vd_field(wl.TRIPLANE, (4, 5, 6))
+    o, d, near, far = tiny_rays(6)
+    rays = oracle.Rays(o, d, near, far, 9)
+    p = wl.counter_uniform(75, np.arange(18, dtype=np.uint64), -1, 1).reshape(6, 3)
+    sg, sp = oracle.relu_slack(F, rays, p, band=1e-3)
+    assert sp.shape == F.params.shape and np.all(sp >= 0) and all(np.all(g >= 0) for g in sg)
+    sg0, sp0 = oracle.relu_slack(F, rays, p, band=0.0)
+    assert float(np.abs(sp0).sum()) == 0.0
+    assert np.all(np.isfinite(oracle.min_preact(F, rays)))
