@@ -227,6 +227,21 @@ def config_dict(cfg, n):
                   "by design (steady-state training)"}
 
 
+def init_device_and_group(torch, dist, local, world):
+    """One process per GPU: cuda:LOCAL_RANK and an NCCL process group. LP_DIST_BACKEND=gloo
+    (with more ranks than GPUs: rank -> GPU local % count) exercises the N > 1 code path
+    on a single GPU for plumbing checks only; its timings are not measurements."""
+    backend = os.environ.get("LP_DIST_BACKEND", "nccl")
+    dev = torch.device("cuda", local % torch.cuda.device_count() if backend != "nccl" else local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return dev
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import torch
@@ -235,10 +250,7 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_device_and_group(torch, dist, local, world)
 
     import paper_2404_19760_b200 as lpb
     from paper_2404_19760_b200.dist import FlatGrads, allreduce_grads, shard_range
@@ -448,10 +460,7 @@ def run_splat(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_device_and_group(torch, dist, local, world)
     cfg = wl.get_config(args.config)
     lo, hi = shard_range(cfg.n_rays, rank, world)
     M, S = hi - lo, cfg.S
