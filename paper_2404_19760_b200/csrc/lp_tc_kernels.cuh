@@ -58,6 +58,13 @@ namespace lp {
 // iterations of the cooperative gather whose loads are kept in flight together
 constexpr int kGatherUnroll = LP_GATHER_UNROLL;
 
+#ifndef LP_BWD_HPIECES
+#define LP_BWD_HPIECES 3
+#endif
+// bf16 pieces of the backward's H tile (3: the forward's fp32-class Z; 2: 5 products,
+// ~2^-17 relative, frees 12 KB of shared memory per group for L1 -- experiment)
+constexpr int kBwdHPieces = LP_BWD_HPIECES;
+
 template <int KIND, int K, int HID>
 struct TcShape {
   static constexpr int KP = K < 16 ? 16 : K;     // H tile columns / MMA K for Z, N for dH
@@ -400,7 +407,7 @@ struct BwdTcSmem {
   static constexpr uint32_t FP = W0P + 3 * S::W0_PIECE;
   static constexpr uint32_t GRP = (FP + TcParams<K, HID>::N * 4 + 127) & ~127u;
   static constexpr uint32_t H = 0;                             // [H | 1 | DO], 3 pieces
-  static constexpr uint32_t DA = H + 3 * S::HB_PIECE;          // [D1 | A1], 2 pieces; after the
+  static constexpr uint32_t DA = H + kBwdHPieces * S::HB_PIECE;  // [D1 | A1], 2 pieces; after the
                                                                // MMAs: fp32 dH staging + tap records
   static constexpr uint32_t PTAPS = DA + S::DA_PIECE;
   static constexpr uint32_t TAPS = DA + 2 * S::DA_PIECE;      // [T halves][128][NPL]
@@ -510,10 +517,10 @@ __global__ void __launch_bounds__(128 * T * G, 1) lp_bwd_tc_kernel(const KernelA
       LP_PT(0)
 #ifndef LP_ABL_NOGATHER
       if (pending)   // warp-uniform
-        coop_gather<KIND, K, S::HC, 3, true>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, gplanes, ptaps, dhs,
+        coop_gather<KIND, K, S::HC, kBwdHPieces, true>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, gplanes, ptaps, dhs,
                                              it0, it1);
       else
-        coop_gather<KIND, K, S::HC, 3>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, nullptr, nullptr,
+        coop_gather<KIND, K, S::HC, kBwdHPieces>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, nullptr, nullptr,
                                        nullptr, it0, it1);
       pending = false;
 #endif
@@ -525,11 +532,12 @@ __global__ void __launch_bounds__(128 * T * G, 1) lp_bwd_tc_kernel(const KernelA
       if (gt == 0) {
         tc::fence_after_sync();
         constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
+        constexpr int NPROD = kBwdHPieces == 3 ? 6 : 5;   // products with H piece < kBwdHPieces
         uint32_t acc = 0;
 #pragma unroll
         for (int ks = 0; ks < S::KP / 16; ++ks)
 #pragma unroll
-          for (int c = 0; c < 6; ++c) {
+          for (int c = 0; c < NPROD; ++c) {
             tc::mma_bf16(tZ, tc::desc_kmajor(h_addr + PA[c] * S::HB_PIECE, S::HC, ks),
                          tc::desc_kmajor(w_addr + PB[c] * S::W0_PIECE, S::KP, ks), id_z, acc);
             acc = 1;
