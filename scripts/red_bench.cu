@@ -2,6 +2,7 @@
 //   A: 8 lanes x red.global.add.v4.f32 per line (4 lines per warp instruction)
 //   B: stage the line in shared memory, cp.reduce.async.bulk (UBLKRED) per line
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -37,9 +38,12 @@ __global__ void redB(float* g, const int* lines, int nl_per_warp, int nlines_tot
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
+  // usage: red_bench [n_sm]  -- with n_sm < 148: one 1024-thread block per SM on n_sm SMs
+  // (per-SM scaling of the reduction rate); default: 4 x 256-thread blocks per SM on all 148
   const int nlines = 24 * 1024 * 1024 / 128;  // 24 MB buffer
-  const int blocks = 148 * 4, threads = 256, warps = blocks * threads / 32;
+  const int n_sm = argc > 1 ? atoi(argv[1]) : 148;
+  const int blocks = argc > 1 ? n_sm : 148 * 4, threads = argc > 1 ? 1024 : 256, warps = blocks * threads / 32;
   const int per = 4096;
   float* g; int* lines;
   cudaMalloc(&g, (size_t)nlines * 128); cudaMemset(g, 0, (size_t)nlines * 128);
