@@ -282,3 +282,16 @@ def test_autograd_view_dependent(torch_cuda):
     g = dict(out=out.detach().cpu().numpy(), tau=tau.detach().cpu().numpy(),
              gplanes=[p.grad.cpu().numpy() for p in field.planes], gparams=field.params.grad.cpu().numpy())
     _assert(_compare(g, r))
+
+
+@pytest.mark.parametrize("cfg", ["c4p", "c1v"])
+def test_ragged_tail_other_kernel_families(torch_cuda, cfg):
+    """M not a multiple of 128 and minimal S on the 3-layer (K1tc2/K2tc2) and the
+    view-dependent (K1tcv/K2tcv) kernels."""
+    import dataclasses
+    idx = np.arange(1000, dtype=np.int64) * 7 + 3
+    pb = problem_np(cfg, idx=idx, with_gdepth=True)
+    _assert(_compare(_gpu_fwd_bwd(torch_cuda, pb, depth=True), oracle_reference(pb, depth=True)))
+    pb2 = dict(pb)
+    pb2["cfg"] = dataclasses.replace(pb["cfg"], S=2)
+    _assert(_compare(_gpu_fwd_bwd(torch_cuda, pb2, depth=True), oracle_reference(pb2, depth=True)))

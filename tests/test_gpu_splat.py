@@ -113,3 +113,28 @@ def test_splat_autograd(torch_cuda):
     ref_gf = oracle.splat_backward_threaded(spec, R, gout, ref_wt, threads=8)
     assert max(rel_inf(p.detach().cpu().numpy(), r) for p, r in zip(planes, ref_out)) < TOL
     assert rel_inf(feats.grad.cpu().numpy(), ref_gf) < TOL
+
+
+def test_splat_edge_cases(torch_cuda):
+    """M = 0 is a no-op; a ragged M splats exactly like the oracle; misaligned
+    feature pointers are rejected before any launch."""
+    import paper_2404_19760_b200 as lpb
+    from paper_2404_19760_b200._lib import LpError
+    torch = torch_cuda
+    grid = lpb.SplatGrid(wl.VOXEL, (20, 20, 20), 8)
+    z3, z1 = torch.zeros((0, 3), device="cuda"), torch.zeros((0,), device="cuda")
+    th, wt = lpb.splat_forward(grid, z3, z3, z1, z1, 16, torch.zeros((0, 8), device="cuda"))
+    torch.cuda.synchronize()
+    assert float(th[0].abs().sum()) == 0.0 and float(wt[0].abs().sum()) == 0.0
+    cfg, idx, rays, v = _problem("s1", 333, res=20, K=8)
+    spec = _spec(cfg)
+    R = oracle.Rays(*rays, cfg.S)
+    ref_out, _, ref_wt = oracle.splat_forward(spec, R, v)
+    gout = wl.make_grid_grad(spec.shapes())
+    out, wt, gf = _gpu(torch, cfg, rays, v, gout)
+    assert rel_inf(out[0], ref_out[0]) < TOL and rel_inf(wt[0], ref_wt[0]) < TOL
+    assert rel_inf(gf, oracle.splat_backward(spec, R, gout, ref_wt)) < TOL
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    feats = torch.zeros(len(v) * 8 + 1, device="cuda")[1:].view(len(v), 8)   # 4-byte offset
+    with pytest.raises(LpError):
+        lpb.splat_forward(grid, *(T(a) for a in rays), cfg.S, feats)
