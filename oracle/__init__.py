@@ -67,11 +67,17 @@ def lib():
             L.lpo_splat_rays.argtypes = [i32, i32, i32, i32, i32, i64, i64, P, P, P, P, i32, P, P, P, P, P, P, P,
                                          i32, f64]
             L.lpo_splat_normalize.argtypes = [i64, i32, P, P, P]
+            L.lpo_splat_rays_mlp.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, i32, P, P, i32, i32, i64, i64,
+                                             P, P, P, P, i32, P, P, P, P, P, P, P, i32, f64]
+            L.lpo_splat_rays_mlp_backward.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, i32, P, P, i32, i32,
+                                                      i64, i64, P, P, P, P, i32, P, P, P, P, P, P, P, P, P, P, P,
+                                                      P, i32, f64]
             L.lpo_splat_rays_backward.argtypes = [i32, i32, i32, i32, i32, i64, i64, P, P, P, P, i32, P, P, P,
                                                   P, P, P, P, i32, f64]
             for f in (L.lpo_render_relu_slack, L.lpo_render_min_preact, L.lpo_sample, L.lpo_splat, L.lpo_mlp_forward, L.lpo_mlp_backward,
                       L.lpo_render_forward, L.lpo_render_backward, L.lpo_trace, L.lpo_contract,
-                      L.lpo_splat_rays, L.lpo_splat_normalize, L.lpo_splat_rays_backward):
+                      L.lpo_splat_rays, L.lpo_splat_normalize, L.lpo_splat_rays_backward,
+                      L.lpo_splat_rays_mlp, L.lpo_splat_rays_mlp_backward):
                 f.restype = ctypes.c_int
             _lib = L
     return _lib
@@ -405,3 +411,47 @@ def splat_backward_threaded(spec: GridSpec, rays: Rays, grad_out, theta_weight, 
     for t in ts:
         t.join()
     return out
+
+
+class SplatMlp:
+    """g_s of Eq. 2: prior grid theta^ (same kind/dims as the target,
+    K_p channels), MLP widths (C_in + K_p + 6F, hidden..., K) and packed params."""
+
+    def __init__(self, prior: Sequence[np.ndarray], widths: Sequence[int], params, C_in: int, dir_freqs: int):
+        self.prior = [_d(g) for g in prior]
+        self.Kp = int(self.prior[0].shape[-1])
+        self.widths = np.ascontiguousarray(np.asarray(widths, dtype=np.int32))
+        self.params = _d(params)
+        self.C_in, self.F = int(C_in), int(dir_freqs)
+        assert self.widths[0] == self.C_in + self.Kp + 6 * self.F
+
+    def _args(self):
+        q = _ptr3(self.prior)
+        return (self.Kp, *q, len(self.widths) - 1, _p(self.widths), _p(self.params), self.C_in, self.F)
+
+
+def splat_forward_mlp(spec: GridSpec, rays: Rays, features, g: SplatMlp):
+    """Splatter with g_s: (normalised theta, theta, theta_weight)."""
+    v = _d(features).reshape(rays.n, g.C_in)
+    th = [np.zeros(s) for s in spec.shapes()]
+    wt = [np.zeros(s) for s in spec.shapes(1)]
+    rc = lib().lpo_splat_rays_mlp(*spec._geom(), *g._args(), 0, rays.n, _p(rays.o), _p(rays.d), _p(rays.near),
+                                  _p(rays.far), rays.S, _p(v), *_ptr3(th), *_ptr3(wt), spec.contraction,
+                                  spec.contract_a)
+    assert rc == 0
+    return splat_normalize(th, wt), th, wt
+
+
+def splat_backward_mlp(spec: GridSpec, rays: Rays, features, g: SplatMlp, grad_out, theta_weight):
+    """(dL/d features [n][C_in], dL/d prior planes, dL/d g_s params)."""
+    v = _d(features).reshape(rays.n, g.C_in)
+    gv = np.zeros((rays.n, g.C_in))
+    gpr = [np.zeros_like(a) for a in g.prior]
+    gpar = np.zeros_like(g.params)
+    go = [_d(a) for a in grad_out]
+    w = [_d(a) for a in theta_weight]
+    rc = lib().lpo_splat_rays_mlp_backward(*spec._geom(), *g._args(), 0, rays.n, _p(rays.o), _p(rays.d),
+                                           _p(rays.near), _p(rays.far), rays.S, _p(v), *_ptr3(go), *_ptr3(w),
+                                           _p(gv), *_ptr3(gpr), _p(gpar), spec.contraction, spec.contract_a)
+    assert rc == 0
+    return gv, gpr, gpar

@@ -742,6 +742,133 @@ int lpo_splat_rays_backward(int kind, int H, int W, int D, int K, int64_t r0, in
   return 0;
 }
 
+// ---------------------------------------------------------------- Splatter with g_s (Eq. 2)
+// v~_ij = g_s(v_i, h_prior(x_ij), direnc(d_i)) (reading R30): the input is the
+// concatenation [v_i (C_in) ; h_prior(x_ij) (K_p, the prior grid theta^ sampled
+// with the same scheme h, same kind and dims as theta) ; direnc(d_i) (6F)], g_s
+// an MLP (ReLU hidden, identity output) with widths[0] = C_in + K_p + 6F and
+// widths[L] = K (theta's channels). Pass 1 splats v~_ij, pass 2 (MLPs off,
+// P:748) splats 1 into theta_weight exactly as lpo_splat_rays.
+struct SplatMlp {
+  Field F;        // target geometry (K = C_out), contraction
+  Field Fp;       // prior grid (K = K_p)
+  Field Fm;       // g_s (widths / params)
+  int C_in, F_dir;
+};
+
+SplatMlp make_splat_mlp(int kind, int H, int W, int D, int K, int Kp, const double* q0, const double* q1,
+                        const double* q2, int n_layers, const int* widths, const double* params, int C_in, int F_dir,
+                        int contraction, double contract_a) {
+  SplatMlp m;
+  m.F = make_field(kind, H, W, D, K, nullptr, nullptr, nullptr, 0, nullptr, nullptr, contraction, contract_a);
+  m.Fp = make_field(kind, H, W, D, Kp, q0, q1, q2, 0, nullptr, nullptr, contraction, contract_a);
+  m.Fm = make_field(kind, H, W, D, widths[0], nullptr, nullptr, nullptr, n_layers, widths, params);
+  m.C_in = C_in;
+  m.F_dir = F_dir;
+  return m;
+}
+
+// u = [v ; h_prior(x) ; direnc(d)] and the prior taps of point x
+void splat_mlp_input(const SplatMlp& m, const double* v, const double* x, const double* e, std::vector<Tap>& taps,
+                     std::vector<double>& u) {
+  const int Kp = m.Fp.K;
+  u.assign(m.Fm.widths[0], 0.0);
+  for (int k = 0; k < m.C_in; ++k) u[k] = v[k];
+  sample_taps(m.Fp, x, taps);
+  gather(m.Fp, taps, u.data() + m.C_in);
+  for (int k = 0; k < 6 * m.F_dir; ++k) u[m.C_in + Kp + k] = e[k];
+}
+
+int lpo_splat_rays_mlp(int kind, int H, int W, int D, int K, int Kp, const double* q0, const double* q1,
+                       const double* q2, int n_layers, const int* widths, const double* params, int C_in, int F_dir,
+                       int64_t r0, int64_t r1, const double* origins, const double* dirs, const double* nearv,
+                       const double* farv, int S, const double* features, double* t0, double* t1, double* t2,
+                       double* w0, double* w1, double* w2, int contraction, double contract_a) {
+  if (widths[0] != C_in + Kp + 6 * F_dir || widths[n_layers] != K || S < 2) return 1;
+  SplatMlp m = make_splat_mlp(kind, H, W, D, K, Kp, q0, q1, q2, n_layers, widths, params, C_in, F_dir, contraction,
+                              contract_a);
+  Field F1 = make_field(kind, H, W, D, 1, nullptr, nullptr, nullptr, 0, nullptr, nullptr, contraction, contract_a);
+  double* tg[3] = {t0, t1, t2};
+  double* wg[3] = {w0, w1, w2};
+  const double one = 1.0;
+  const int R = S - 1;
+  std::vector<Tap> taps, ptaps;
+  std::vector<double> u, e(6 * F_dir);
+  MlpTrace tr;
+  for (int64_t r = r0; r < r1; ++r) {
+    const double* o = origins + 3 * r;
+    const double* d = dirs + 3 * r;
+    direnc(d, F_dir, e.data());
+    double span = farv[r] - nearv[r];
+    double delta = (span > 0.0 ? span : 0.0) / (double)R;
+    for (int j = 0; j < S; ++j) {
+      double t = nearv[r] + (double)j * delta;
+      double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+      contract(m.F, x);
+      sample_taps(m.F, x, taps);
+      if (taps.empty()) continue;                 // nothing to splat outside the cube
+      splat_mlp_input(m, features + r * C_in, x, e.data(), ptaps, u);
+      mlp_forward(m.Fm, u.data(), tr);
+      scatter(m.F, taps, tr.a[n_layers].data(), tg);   // pass 1: v~_ij
+      scatter(F1, taps, &one, wg);                     // pass 2: 1 (MLPs off)
+    }
+  }
+  return 0;
+}
+
+// Backward of the normalised g_s splat (theta_weight constant): per sample
+// dv~_ij = h_{g'}(x_ij), g' = grad_out / theta_weight; then the g_s VJP gives
+// dL/dv_i (summed over j, overwritten for rays [r0, r1)), the prior gradient
+// (scattered with the prior's sampling weights, accumulated) and the g_s
+// parameter gradient (accumulated).
+int lpo_splat_rays_mlp_backward(int kind, int H, int W, int D, int K, int Kp, const double* q0, const double* q1,
+                                const double* q2, int n_layers, const int* widths, const double* params, int C_in,
+                                int F_dir, int64_t r0, int64_t r1, const double* origins, const double* dirs,
+                                const double* nearv, const double* farv, int S, const double* features,
+                                const double* g0, const double* g1, const double* g2, const double* w0,
+                                const double* w1, const double* w2, double* grad_features, double* gp0, double* gp1,
+                                double* gp2, double* grad_params, int contraction, double contract_a) {
+  if (widths[0] != C_in + Kp + 6 * F_dir || widths[n_layers] != K || S < 2) return 1;
+  SplatMlp m = make_splat_mlp(kind, H, W, D, K, Kp, q0, q1, q2, n_layers, widths, params, C_in, F_dir, contraction,
+                              contract_a);
+  const double* gg[3] = {g0, g1, g2};
+  const double* wg[3] = {w0, w1, w2};
+  double* gpr[3] = {gp0, gp1, gp2};
+  const int R = S - 1;
+  std::vector<Tap> taps, ptaps;
+  std::vector<double> u, e(6 * F_dir), dv(K), du(widths[0]);
+  MlpTrace tr;
+  for (int64_t r = r0; r < r1; ++r) {
+    const double* o = origins + 3 * r;
+    const double* d = dirs + 3 * r;
+    direnc(d, F_dir, e.data());
+    double span = farv[r] - nearv[r];
+    double delta = (span > 0.0 ? span : 0.0) / (double)R;
+    double* gv = grad_features + r * C_in;
+    for (int k = 0; k < C_in; ++k) gv[k] = 0.0;
+    for (int j = 0; j < S; ++j) {
+      double t = nearv[r] + (double)j * delta;
+      double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+      contract(m.F, x);
+      sample_taps(m.F, x, taps);
+      if (taps.empty()) continue;
+      for (int k = 0; k < K; ++k) dv[k] = 0.0;
+      for (const Tap& tp : taps) {
+        double wc = wg[tp.plane][tp.cell];
+        if (!(wc > 0.0)) continue;
+        const double* g = gg[tp.plane] + tp.cell * K;
+        for (int k = 0; k < K; ++k) dv[k] += tp.w * (g[k] / wc);
+      }
+      splat_mlp_input(m, features + r * C_in, x, e.data(), ptaps, u);
+      mlp_forward(m.Fm, u.data(), tr);
+      mlp_backward(m.Fm, tr, dv.data(), grad_params, du.data());
+      for (int k = 0; k < C_in; ++k) gv[k] += du[k];
+      scatter(m.Fp, ptaps, du.data() + C_in, gpr);   // prior gradient
+    }
+  }
+  return 0;
+}
+
 // Per-sample trace of one ray for invariant tests: sigma[S], tau[S], T[S], w[S], c[S][C].
 int lpo_trace(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
               int n_layers, const int* widths, const double* params, const double* origin, const double* dir,

@@ -133,3 +133,127 @@ def test_splat_backward_matches_finite_differences(kind, contraction):
         fd[idx] = (loss(vp) - loss(vm)) / (2 * eps)
     assert np.max(np.abs(fd)) > 1e-2
     assert rel_inf(gv, fd) < 1e-8
+
+
+# ---------------------------------------------------------------- g_s (Eq. 2)
+def _identity_gs(C_in, Kp, F, K, block):
+    """g_s with widths (C_in + Kp + 6F, 2K, K) whose output is one input block exactly:
+    hidden = [relu(x), relu(-x)], output = hidden_+ - hidden_- (block: 'v', 'prior' or 'dir')."""
+    nin = C_in + Kp + 6 * F
+    off = {"v": 0, "prior": C_in, "dir": C_in + Kp}[block]
+    W0 = np.zeros((2 * K, nin))
+    for k in range(K):
+        W0[k, off + k] = 1.0
+        W0[K + k, off + k] = -1.0
+    W1 = np.concatenate([np.eye(K), -np.eye(K)], axis=1)
+    params = np.concatenate([W0.ravel(), np.zeros(2 * K), W1.ravel(), np.zeros(K)])
+    return (nin, 2 * K, K), params
+
+
+def _prior(spec, Kp, seed=95):
+    return [wl.counter_uniform(seed + i, np.arange(int(np.prod(s)), dtype=np.uint64), -1, 1).reshape(s).astype(np.float64)
+            for i, s in enumerate(spec.shapes(Kp))]
+
+
+@pytest.mark.parametrize("kind", [wl.TRIPLANE, wl.VOXEL])
+def test_gs_identity_on_features_reduces_to_the_plain_splat(kind):
+    spec = _spec(kind)
+    o, d, near, far = tiny_rays(6)
+    rays = oracle.Rays(o, d, near, far, 9)
+    v = wl.counter_uniform(96, np.arange(6 * spec.K, dtype=np.uint64), -1, 1).reshape(6, spec.K)
+    widths, params = _identity_gs(spec.K, 2, 2, spec.K, "v")
+    g = oracle.SplatMlp(_prior(spec, 2), widths, params, spec.K, 2)
+    a = oracle.splat_forward_mlp(spec, rays, v, g)
+    b = oracle.splat_forward(spec, rays, v)
+    for u, w in zip(a[0] + a[1] + a[2], b[0] + b[1] + b[2]):
+        assert np.max(np.abs(u - w)) < 1e-13
+
+
+@pytest.mark.parametrize("kind,contraction", [(wl.TRIPLANE, 0), (wl.VOXEL, 1)])
+def test_gs_reading_the_prior_splats_the_prior_samples(kind, contraction):
+    """g_s = the prior block: theta = sum_ij w(x_ij) h_prior(x_ij), built independently
+    from oracle.sample (scipy-pinned) and oracle.splat (adjoint-pinned) on the point list."""
+    spec = _spec(kind, K=3, contraction=contraction)
+    o, d, near, far = tiny_rays(6)
+    rays = oracle.Rays(o, d, near, far * (2.0 if contraction else 1.0), 9)
+    prior = _prior(spec, 3)
+    widths, params = _identity_gs(2, 3, 1, 3, "prior")
+    g = oracle.SplatMlp(prior, widths, params, 2, 1)
+    v = np.zeros((6, 2))
+    out, th, wt = oracle.splat_forward_mlp(spec, rays, v, g)
+    x, _ = _points(rays)
+    if contraction:
+        x = oracle.contract(contraction, spec.contract_a, x)
+    Fp = oracle.Field(kind, prior, (3, 2), np.zeros(3 * 2 + 2))
+    vals = oracle.sample(Fp, x)
+    ref = oracle.splat(Fp, x, vals)
+    for a, b in zip(th, ref):
+        assert np.max(np.abs(a - b)) < 1e-13
+    assert max(np.max(np.abs(a)) for a in th) > 0.1
+
+
+def test_gs_reading_direnc():
+    """g_s = the direnc block (F = 1: sin(pi d_x), cos(pi d_x), sin(pi d_y)): equals the
+    plain splat of those per-ray values (numpy sin / cos)."""
+    spec = _spec(wl.VOXEL)
+    o, d, near, far = tiny_rays(6)
+    rays = oracle.Rays(o, d, near, far, 9)
+    widths, params = _identity_gs(2, 2, 1, 3, "dir")
+    g = oracle.SplatMlp(_prior(spec, 2), widths, params, 2, 1)
+    a = oracle.splat_forward_mlp(spec, rays, np.zeros((6, 2)), g)
+    dd = rays.d
+    feats = np.stack([np.sin(np.pi * dd[:, 0]), np.cos(np.pi * dd[:, 0]), np.sin(np.pi * dd[:, 1])], axis=1)
+    b = oracle.splat_forward(spec, rays, feats)
+    for u, w in zip(a[0] + a[1], b[0] + b[1]):
+        assert np.max(np.abs(u - w)) < 1e-12
+
+
+@pytest.mark.parametrize("kind", [wl.TRIPLANE, wl.VOXEL])
+def test_gs_backward_matches_finite_differences(kind):
+    spec = _spec(kind, K=3)
+    o, d, near, far = tiny_rays(4)
+    rays = oracle.Rays(o, d, near, far, 6)
+    C_in, Kp, F, hid = 2, 2, 1, 5
+    widths = (C_in + Kp + 6 * F, hid, spec.K)
+    params = wl.make_mlp(widths, seed=97, hidden_bias_scale=0.3).astype(np.float64)
+    prior = _prior(spec, Kp)
+    g = oracle.SplatMlp(prior, widths, params, C_in, F)
+    v = wl.counter_uniform(98, np.arange(4 * C_in, dtype=np.uint64), -1, 1).reshape(4, C_in).astype(np.float64)
+    gout = [wl.counter_uniform(99 + i, np.arange(int(np.prod(s)), dtype=np.uint64), -1, 1).reshape(s).astype(np.float64)
+            for i, s in enumerate(spec.shapes())]
+    _, _, wt = oracle.splat_forward_mlp(spec, rays, v, g)
+
+    def loss(vv, gg):
+        out, _, _ = oracle.splat_forward_mlp(spec, rays, vv, gg)
+        return sum(float(np.sum(a * b)) for a, b in zip(out, gout))
+
+    gv, gpr, gpar = oracle.splat_backward_mlp(spec, rays, v, g, gout, wt)
+    eps = 1e-6
+    fd = np.zeros_like(v)
+    for idx in np.ndindex(*v.shape):
+        vp, vm = v.copy(), v.copy()
+        vp[idx] += eps
+        vm[idx] -= eps
+        fd[idx] = (loss(vp, g) - loss(vm, g)) / (2 * eps)
+    assert rel_inf(gv, fd) < 1e-6
+    fdp = np.zeros_like(params)
+    for i in range(params.size):
+        for sgn, store in ((1, 0), (-1, 1)):
+            pp = params.copy()
+            pp[i] += sgn * eps
+            val = loss(v, oracle.SplatMlp(prior, widths, pp, C_in, F))
+            fdp[i] += sgn * val / (2 * eps)
+    assert rel_inf(gpar, fdp) < 1e-6
+    for pi_, pl in enumerate(prior):
+        flat = pl.reshape(-1)
+        fdq = np.zeros(flat.size)
+        for i in range(flat.size):
+            keep = flat[i]
+            flat[i] = keep + eps
+            lp = loss(v, oracle.SplatMlp(prior, widths, params, C_in, F))
+            flat[i] = keep - eps
+            lm = loss(v, oracle.SplatMlp(prior, widths, params, C_in, F))
+            flat[i] = keep
+            fdq[i] = (lp - lm) / (2 * eps)
+        assert rel_inf(gpr[pi_].reshape(-1), fdq) < 1e-6
+    assert np.max(np.abs(gv)) > 1e-3 and max(np.max(np.abs(a)) for a in gpr) > 1e-3
