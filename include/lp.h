@@ -182,6 +182,36 @@ lp_status lp_splat_normalize(const lp_grid* grid, const float* const theta[3], c
 lp_status lp_splat_backward(const lp_grid* grid, const lp_rays* rays, const float* const grad_out[3],
                             const float* const theta_weight[3], float* grad_features, void* stream);
 
+/* Splatter with its MLP g_s (Eq. 2; reading R30):
+ *   v~_ij = g_s(v_i, h_prior(x_ij), direnc(d_i)),  theta += sum_ij w(x_ij) v~_ij,
+ * theta_weight as in lp_splat_forward (the weight pass runs with the MLP off,
+ * P:748). g_s = Linear(C_in + K_prior + 6F -> hidden) -> ReLU -> Linear(-> K),
+ * params packed W0 [hidden][C_in + K_prior + 6F] (input order: v, h_prior,
+ * direnc as in lp_mlp), b0, W1 [K][hidden], b1. The prior grid has the kind,
+ * dims and contraction of `grid`, K_prior channels, channel-last, 16-byte
+ * aligned. Compiled: C_in = K_prior = K = 32, hidden = 64, dir_freqs <= 5. */
+typedef struct {
+  const float* params;
+  int32_t hidden;
+  int32_t C_in;
+  int32_t dir_freqs;
+  int32_t K_prior;
+  const float* prior[3];
+} lp_splat_mlp;
+
+/* theta, theta_weight ACCUMULATED (+=). features [M][C_in]. */
+lp_status lp_splat_forward_mlp(const lp_grid* grid, const lp_rays* rays, const float* features,
+                               const lp_splat_mlp* gs, float* const theta[3], float* const theta_weight[3],
+                               void* stream);
+
+/* Backward of the normalised g_s splat (theta_weight constant):
+ * grad_features [M][C_in] OVERWRITTEN; grad_prior (prior shapes) and
+ * grad_params (params packing) ACCUMULATED (+=, fp32 atomics). */
+lp_status lp_splat_backward_mlp(const lp_grid* grid, const lp_rays* rays, const float* features,
+                                const lp_splat_mlp* gs, const float* const grad_out[3],
+                                const float* const theta_weight[3], float* grad_features, float* const grad_prior[3],
+                                float* grad_params, void* stream);
+
 /* Optional: keep theta resident in L2 for kernels launched by this library on
  * the calling thread's current device (access-policy window on each launch,
  * hit ratio in (0,1]; 0 disables). Sets cudaLimitPersistingL2CacheSize. */

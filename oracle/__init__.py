@@ -69,6 +69,8 @@ def lib():
             L.lpo_splat_normalize.argtypes = [i64, i32, P, P, P]
             L.lpo_splat_rays_mlp.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, i32, P, P, i32, i32, i64, i64,
                                              P, P, P, P, i32, P, P, P, P, P, P, P, i32, f64]
+            L.lpo_splat_mlp_min_preact.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, i32, P, P, i32, i32, i64,
+                                                   i64, P, P, P, P, i32, P, P, i32, f64]
             L.lpo_splat_rays_mlp_backward.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, i32, P, P, i32, i32,
                                                       i64, i64, P, P, P, P, i32, P, P, P, P, P, P, P, P, P, P, P,
                                                       P, i32, f64]
@@ -77,7 +79,7 @@ def lib():
             for f in (L.lpo_render_relu_slack, L.lpo_render_min_preact, L.lpo_sample, L.lpo_splat, L.lpo_mlp_forward, L.lpo_mlp_backward,
                       L.lpo_render_forward, L.lpo_render_backward, L.lpo_trace, L.lpo_contract,
                       L.lpo_splat_rays, L.lpo_splat_normalize, L.lpo_splat_rays_backward,
-                      L.lpo_splat_rays_mlp, L.lpo_splat_rays_mlp_backward):
+                      L.lpo_splat_rays_mlp, L.lpo_splat_rays_mlp_backward, L.lpo_splat_mlp_min_preact):
                 f.restype = ctypes.c_int
             _lib = L
     return _lib
@@ -455,3 +457,14 @@ def splat_backward_mlp(spec: GridSpec, rays: Rays, features, g: SplatMlp, grad_o
                                            _p(gv), *_ptr3(gpr), _p(gpar), spec.contraction, spec.contract_a)
     assert rc == 0
     return gv, gpr, gpar
+
+
+def splat_mlp_min_preact(spec: GridSpec, rays: Rays, features, g: SplatMlp) -> np.ndarray:
+    """Per ray: min |z| / scale over g_s's hidden units (lp_oracle.cpp)."""
+    v = _d(features).reshape(rays.n, g.C_in)
+    out = np.zeros(rays.n)
+    rc = lib().lpo_splat_mlp_min_preact(*spec._geom(), *g._args(), 0, rays.n, _p(rays.o), _p(rays.d),
+                                        _p(rays.near), _p(rays.far), rays.S, _p(v), _p(out), spec.contraction,
+                                        spec.contract_a)
+    assert rc == 0
+    return out

@@ -869,6 +869,54 @@ int lpo_splat_rays_mlp_backward(int kind, int H, int W, int D, int K, int Kp, co
   return 0;
 }
 
+// Per ray: min over in-cube samples and hidden units of g_s of |z| / (sum_k |W_ik u_k| + |b_i|)
+// (the ReLU-decision conditioning used by the GPU parity tests to leave out rays whose
+// ReLU'(z) is decided within rounding).
+int lpo_splat_mlp_min_preact(int kind, int H, int W, int D, int K, int Kp, const double* q0, const double* q1,
+                             const double* q2, int n_layers, const int* widths, const double* params, int C_in,
+                             int F_dir, int64_t r0, int64_t r1, const double* origins, const double* dirs,
+                             const double* nearv, const double* farv, int S, const double* features, double* min_rel,
+                             int contraction, double contract_a) {
+  if (widths[0] != C_in + Kp + 6 * F_dir || widths[n_layers] != K || S < 2) return 1;
+  SplatMlp m = make_splat_mlp(kind, H, W, D, K, Kp, q0, q1, q2, n_layers, widths, params, C_in, F_dir, contraction,
+                              contract_a);
+  const int R = S - 1;
+  std::vector<Tap> taps, ptaps;
+  std::vector<double> u, e(6 * F_dir);
+  MlpTrace tr;
+  for (int64_t r = r0; r < r1; ++r) {
+    const double* o = origins + 3 * r;
+    const double* d = dirs + 3 * r;
+    direnc(d, F_dir, e.data());
+    double span = farv[r] - nearv[r];
+    double delta = (span > 0.0 ? span : 0.0) / (double)R;
+    double best = INFINITY;
+    for (int j = 0; j < S; ++j) {
+      double t = nearv[r] + (double)j * delta;
+      double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+      contract(m.F, x);
+      sample_taps(m.F, x, taps);
+      if (taps.empty()) continue;
+      splat_mlp_input(m, features + r * C_in, x, e.data(), ptaps, u);
+      mlp_forward(m.Fm, u.data(), tr);
+      const double* p = params;
+      for (int l = 0; l < n_layers - 1; ++l) {
+        int fin = widths[l], fout = widths[l + 1];
+        const double* Wl = p;
+        const double* bl = p + (int64_t)fout * fin;
+        p = bl + fout;
+        for (int i = 0; i < fout; ++i) {
+          double sc = std::fabs(bl[i]);
+          for (int k = 0; k < fin; ++k) sc += std::fabs(Wl[(int64_t)i * fin + k] * tr.a[l][k]);
+          if (sc > 0.0 && std::fabs(tr.z[l][i]) / sc < best) best = std::fabs(tr.z[l][i]) / sc;
+        }
+      }
+    }
+    min_rel[r - r0] = best;
+  }
+  return 0;
+}
+
 // Per-sample trace of one ray for invariant tests: sigma[S], tau[S], T[S], w[S], c[S][C].
 int lpo_trace(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
               int n_layers, const int* widths, const double* params, const double* origin, const double* dir,

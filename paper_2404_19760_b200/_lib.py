@@ -22,6 +22,7 @@ _STATUS = {0: "LP_OK", 1: "LP_ERR_INVALID_ARG", 2: "LP_ERR_UNSUPPORTED", 3: "LP_
 # Every symbol include/lp.h declares (tests check the library exports them all).
 EXPORTED = ("lp_render_forward", "lp_render_backward", "lp_fwd_bwd_host_workspace_bytes",
             "lp_render_fwd_bwd_host", "lp_splat_forward", "lp_splat_normalize", "lp_splat_backward",
+            "lp_splat_forward_mlp", "lp_splat_backward_mlp",
             "lp_set_l2_persist", "lp_last_error", "lp_abi_version")
 
 
@@ -39,6 +40,11 @@ class LpMlp(ctypes.Structure):
 class LpRays(ctypes.Structure):
     _fields_ = [("n_rays", ctypes.c_int64), ("origins", ctypes.c_void_p), ("dirs", ctypes.c_void_p),
                 ("t_near", ctypes.c_void_p), ("t_far", ctypes.c_void_p), ("n_samples", ctypes.c_int32)]
+
+
+class LpSplatMlp(ctypes.Structure):
+    _fields_ = [("params", ctypes.c_void_p), ("hidden", ctypes.c_int32), ("C_in", ctypes.c_int32),
+                ("dir_freqs", ctypes.c_int32), ("K_prior", ctypes.c_int32), ("prior", ctypes.c_void_p * 3)]
 
 
 class LpError(RuntimeError):
@@ -64,10 +70,14 @@ def _load():
     L.lp_splat_forward.argtypes = [gp, rp, P, P3, P3, P]
     L.lp_splat_normalize.argtypes = [gp, P3, P3, P3, P]
     L.lp_splat_backward.argtypes = [gp, rp, P3, P3, P, P]
+    sp = ctypes.POINTER(LpSplatMlp)
+    L.lp_splat_forward_mlp.argtypes = [gp, rp, P, sp, P3, P3, P]
+    L.lp_splat_backward_mlp.argtypes = [gp, rp, P, sp, P3, P3, P, P3, P, P]
     L.lp_set_l2_persist.argtypes = [ctypes.c_float]
     L.lp_last_error.restype = ctypes.c_char_p
     for f in (L.lp_render_forward, L.lp_render_backward, L.lp_render_fwd_bwd_host, L.lp_set_l2_persist,
-              L.lp_abi_version, L.lp_splat_forward, L.lp_splat_normalize, L.lp_splat_backward):
+              L.lp_abi_version, L.lp_splat_forward, L.lp_splat_normalize, L.lp_splat_backward,
+              L.lp_splat_forward_mlp, L.lp_splat_backward_mlp):
         f.restype = ctypes.c_int
     if L.lp_abi_version() != LP_ABI_VERSION:
         raise ImportError(f"{LIB_PATH} has ABI {L.lp_abi_version()}, expected {LP_ABI_VERSION}: rebuild it")

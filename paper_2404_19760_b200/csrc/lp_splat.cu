@@ -6,7 +6,7 @@
 
 #include "../../include/lp.h"
 #include "lp_internal.h"
-#include "lp_splat_kernels.cuh"
+#include "lp_splat_mlp_kernels.cuh"
 
 namespace {
 using namespace lpi;
@@ -180,3 +180,98 @@ lp_status lp_splat_backward(const lp_grid* grid, const lp_rays* rays, const floa
 }
 
 }  // extern "C"
+
+namespace {
+
+lp_status validate_gs(const lp_grid* grid, const lp_splat_mlp* gs) {
+  if (!gs || !gs->params) return fail(LP_ERR_INVALID_ARG, "null g_s descriptor / params");
+  if (gs->hidden != lp::kGsH || gs->C_in != lp::kGsC || gs->K_prior != lp::kGsKp || grid->K != lp::kGsK)
+    return fail(LP_ERR_UNSUPPORTED, "g_s instance: C_in = K_prior = K = 32, hidden = 64 (got %d, %d, %d, %d)",
+                gs->C_in, gs->K_prior, grid->K, gs->hidden);
+  if (gs->dir_freqs < 0 || 6 * gs->dir_freqs > lp::kDirEP) return fail(LP_ERR_INVALID_ARG, "dir_freqs must be in [0, 5]");
+  return check_planes(grid, gs->prior, "prior");
+}
+
+template <bool FWD, int KIND>
+lp_status run_gs(const lp::SplatMlpArgs& a, cudaStream_t s) {
+  static std::once_flag once;
+  static int blocks = 0;
+  static cudaError_t err = cudaSuccess;
+  auto kernel = FWD ? lp::lp_splat_mlp_fwd_kernel<KIND> : lp::lp_splat_mlp_bwd_kernel<KIND>;
+  const size_t smem = FWD ? lp::GsFwdSmem<KIND>::BYTES : lp::GsBwdSmem<KIND>::BYTES;
+  std::call_once(once, [&] {
+    int dev = 0, sms = 0, occ = 0;
+    err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (err == cudaSuccess) err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, smem);
+    if (err == cudaSuccess && occ < 1) err = cudaErrorInvalidConfiguration;
+    blocks = sms * occ;
+  });
+  if (err != cudaSuccess) return cuda_check(err, "g_s splat kernel setup");
+  const int64_t tiles = (a.s.M + 127) / 128;
+  if (tiles == 0) return LP_OK;
+  kernel<<<(int)(tiles < blocks ? tiles : blocks), 256, smem, s>>>(a);
+  return cuda_check(cudaGetLastError(), "g_s splat kernel launch");
+}
+
+}  // namespace
+
+extern "C" lp_status lp_splat_forward_mlp(const lp_grid* grid, const lp_rays* rays, const float* features,
+                                          const lp_splat_mlp* gs, float* const theta[3], float* const theta_weight[3],
+                                          void* stream) {
+  lp_status st = validate(grid, rays);
+  if (st != LP_OK) return st;
+  if (!rays) return fail(LP_ERR_INVALID_ARG, "null rays descriptor");
+  if ((st = validate_gs(grid, gs)) != LP_OK) return st;
+  if ((st = check_planes(grid, theta, "theta")) != LP_OK) return st;
+  if ((st = check_weights(grid, theta_weight, "theta_weight")) != LP_OK) return st;
+  if (rays->n_rays > 0 && (!features || !aligned16(features))) return fail(LP_ERR_MISALIGNED, "features null or not 16-byte aligned");
+  lp::SplatMlpArgs a{};
+  a.s = make_args(grid, rays);
+  const int np = grid->kind == LP_GRID_TRIPLANE ? 3 : 1;
+  for (int i = 0; i < 3; ++i) {
+    a.s.theta[i] = i < np ? theta[i] : nullptr;
+    a.s.weight[i] = i < np ? theta_weight[i] : nullptr;
+    a.prior[i] = i < np ? gs->prior[i] : nullptr;
+  }
+  a.s.feat = features;
+  a.params = gs->params;
+  a.dir_freqs = gs->dir_freqs;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return grid->kind == LP_GRID_TRIPLANE ? run_gs<true, 0>(a, s) : run_gs<true, 1>(a, s);
+}
+
+extern "C" lp_status lp_splat_backward_mlp(const lp_grid* grid, const lp_rays* rays, const float* features,
+                                           const lp_splat_mlp* gs, const float* const grad_out[3],
+                                           const float* const theta_weight[3], float* grad_features,
+                                           float* const grad_prior[3], float* grad_params, void* stream) {
+  lp_status st = validate(grid, rays);
+  if (st != LP_OK) return st;
+  if (!rays) return fail(LP_ERR_INVALID_ARG, "null rays descriptor");
+  if ((st = validate_gs(grid, gs)) != LP_OK) return st;
+  if ((st = check_planes(grid, grad_out, "grad_out")) != LP_OK) return st;
+  if ((st = check_weights(grid, theta_weight, "theta_weight")) != LP_OK) return st;
+  if ((st = check_planes(grid, grad_prior, "grad_prior")) != LP_OK) return st;
+  if (!grad_params) return fail(LP_ERR_INVALID_ARG, "null grad_params");
+  if (rays->n_rays > 0 && (!features || !aligned16(features) || !grad_features || !aligned16(grad_features)))
+    return fail(LP_ERR_MISALIGNED, "features / grad_features null or not 16-byte aligned");
+  lp::SplatMlpArgs a{};
+  a.s = make_args(grid, rays);
+  const int np = grid->kind == LP_GRID_TRIPLANE ? 3 : 1;
+  for (int i = 0; i < 3; ++i) {
+    a.s.gout[i] = i < np ? grad_out[i] : nullptr;
+    a.s.weight[i] = i < np ? const_cast<float*>(theta_weight[i]) : nullptr;
+    a.prior[i] = i < np ? gs->prior[i] : nullptr;
+    a.gprior[i] = i < np ? grad_prior[i] : nullptr;
+  }
+  a.s.feat = features;
+  a.s.gfeat = grad_features;
+  a.params = gs->params;
+  a.gparams = grad_params;
+  a.dir_freqs = gs->dir_freqs;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return grid->kind == LP_GRID_TRIPLANE ? run_gs<false, 0>(a, s) : run_gs<false, 1>(a, s);
+}
+
+

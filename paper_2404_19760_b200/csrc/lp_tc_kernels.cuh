@@ -154,7 +154,8 @@ template <int KIND, int K, int C, int NP, bool SCATTER = false>
 __device__ __forceinline__ void coop_gather(const float* const* planes, const float4* taps, const GridDims& g,
                                             uint8_t* Htile, uint32_t piece_stride, int row0, int lane,
                                             float* const* gplanes = nullptr, const float4* ptaps = nullptr,
-                                            const float* dhs = nullptr, int it0 = 0, int it1 = K / 4) {
+                                            const float* dhs = nullptr, int it0 = 0, int it1 = K / 4,
+                                            float* const* wplanes = nullptr) {
   constexpr int KC = K / 4, RPI = 32 / KC, NPL = KIND == 0 ? 3 : 1;
   const int ch = lane % KC, sub = lane / KC;
 #pragma unroll kGatherUnroll
@@ -182,6 +183,10 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
             const float w = pc.w[cc];
             atomicAdd(reinterpret_cast<float4*>(gpl + pc.off[cc]), make_float4(w * d.x, w * d.y, w * d.z, w * d.w));
           }
+          if (wplanes && ch == 0) {   // the Splatter's weight pass (scalar 1 per sample)
+#pragma unroll
+            for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) atomicAdd(wplanes[p] + pc.off[cc] / K, pc.w[cc]);
+          }
         }
       }
 #pragma unroll
@@ -200,7 +205,8 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
 // dh rows are fp32 in `dhs` ([128][K + 4]).
 template <int KIND, int K>
 __device__ __forceinline__ void coop_scatter(float* const* gplanes, const float4* taps, const GridDims& g,
-                                             const float* dhs, int row0, int lane, int it0 = 0, int it1 = K / 4) {
+                                             const float* dhs, int row0, int lane, int it0 = 0, int it1 = K / 4,
+                                             float* const* wplanes = nullptr) {
   constexpr int KC = K / 4, RPI = 32 / KC, NPL = KIND == 0 ? 3 : 1;
   const int ch = lane % KC, sub = lane / KC;
 #pragma unroll 1
@@ -218,6 +224,10 @@ __device__ __forceinline__ void coop_scatter(float* const* gplanes, const float4
       for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) {
         const float w = c.w[cc];
         atomicAdd(reinterpret_cast<float4*>(pl + c.off[cc]), make_float4(w * d.x, w * d.y, w * d.z, w * d.w));
+      }
+      if (wplanes && ch == 0) {
+#pragma unroll
+        for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) atomicAdd(wplanes[p] + c.off[cc] / K, c.w[cc]);
       }
     }
   }

@@ -120,3 +120,94 @@ def splat(grid: SplatGrid, origins, dirs, near, far, n_samples: int, features) -
     gradients flow to `features` (the saved state is theta_weight only)."""
     geom = (grid.kind, tuple(grid.dims), grid.K, grid.contraction, grid.contract_scale)
     return list(_SplatFn.apply(geom, int(n_samples), origins, dirs, near, far, features))
+
+
+# ---------------------------------------------------------------- Splatter with g_s (Eq. 2)
+@dataclass
+class SplatMlp:
+    """g_s of Eq. 2: params (W0 [hidden][C_in + K_prior + 6F], b0, W1 [K][hidden], b1),
+    the prior grid theta^ (same kind / dims as the target, K_prior channels), C_in, dir_freqs."""
+    params: torch.Tensor
+    prior: List[torch.Tensor]
+    C_in: int = 32
+    dir_freqs: int = 4
+    hidden: int = 64
+
+    def c_struct(self, grid: "SplatGrid", params=None, prior=None) -> _lib.LpSplatMlp:
+        params = self.params if params is None else params
+        prior = self.prior if prior is None else prior
+        Kp = int(prior[0].shape[-1])
+        _planes(grid, prior, "prior", Kp)
+        _req(params, "g_s params")
+        m = _lib.LpSplatMlp()
+        m.params, m.hidden, m.C_in, m.dir_freqs, m.K_prior = params.data_ptr(), self.hidden, self.C_in, \
+            self.dir_freqs, Kp
+        for i in range(3):
+            m.prior[i] = prior[i].data_ptr() if i < len(prior) else None
+        return m
+
+
+def splat_forward_mlp(grid: SplatGrid, origins, dirs, near, far, n_samples: int, features, gs: SplatMlp,
+                      theta=None, weight=None):
+    """Accumulate the g_s splat: returns (theta planes, theta_weight planes)."""
+    M = origins.shape[0]
+    rays = _c_rays(origins, dirs, near, far, n_samples)
+    _req(features, "features", (M, gs.C_in))
+    theta = grid.zeros(origins.device) if theta is None else theta
+    weight = grid.zeros(origins.device, 1) if weight is None else weight
+    g, m = grid.c_grid(), gs.c_struct(grid)
+    _lib.check(_lib.lib.lp_splat_forward_mlp(ctypes.byref(g), ctypes.byref(rays), _ptr(features), ctypes.byref(m),
+                                             _planes(grid, theta, "theta"), _planes(grid, weight, "weight", 1),
+                                             _stream()))
+    return theta, weight
+
+
+def splat_backward_mlp(grid: SplatGrid, origins, dirs, near, far, n_samples: int, features, gs: SplatMlp,
+                       grad_out, weight, grad_features=None, grad_prior=None, grad_params=None):
+    """Gradients of the normalised g_s splat: (features [M][C_in] overwritten, prior
+    planes and g_s params accumulated)."""
+    M = origins.shape[0]
+    rays = _c_rays(origins, dirs, near, far, n_samples)
+    _req(features, "features", (M, gs.C_in))
+    gf = torch.empty((M, gs.C_in), device=origins.device) if grad_features is None else grad_features
+    gpr = [torch.zeros_like(p) for p in gs.prior] if grad_prior is None else grad_prior
+    gpa = torch.zeros_like(gs.params) if grad_params is None else grad_params
+    Kp = int(gs.prior[0].shape[-1])
+    g, m = grid.c_grid(), gs.c_struct(grid)
+    _lib.check(_lib.lib.lp_splat_backward_mlp(ctypes.byref(g), ctypes.byref(rays), _ptr(features), ctypes.byref(m),
+                                              _planes(grid, grad_out, "grad_out"), _planes(grid, weight, "weight", 1),
+                                              _ptr(gf), _planes(grid, gpr, "grad_prior", Kp), _ptr(gpa), _stream()))
+    return gf, gpr, gpa
+
+
+class _SplatMlpFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, geom, gsmeta, n_samples, origins, dirs, near, far, features, params, *prior):
+        grid = SplatGrid(*geom)
+        gs = SplatMlp(params, list(prior), *gsmeta)
+        theta, weight = splat_forward_mlp(grid, origins, dirs, near, far, n_samples, features, gs)
+        out = splat_normalize(grid, theta, weight, out=theta)
+        ctx.save_for_backward(origins, dirs, near, far, features, params, *prior, *weight)
+        ctx.meta = (geom, gsmeta, n_samples, len(prior))
+        return tuple(out)
+
+    @staticmethod
+    def backward(ctx, *grad_out):
+        geom, gsmeta, n_samples, npl = ctx.meta
+        origins, dirs, near, far, features, params, *rest = ctx.saved_tensors
+        prior, weight = rest[:npl], rest[npl:]
+        grid = SplatGrid(*geom)
+        gs = SplatMlp(params, list(prior), *gsmeta)
+        go = [g.contiguous() if g is not None else torch.zeros(s, device=origins.device)
+              for g, s in zip(grad_out, grid.shapes())]
+        gf, gpr, gpa = splat_backward_mlp(grid, origins, dirs, near, far, n_samples, features, gs, go, weight)
+        return (None, None, None, None, None, None, None, gf, gpa, *gpr)
+
+
+def splat_mlp(grid: SplatGrid, origins, dirs, near, far, n_samples: int, features, gs: SplatMlp) -> List[torch.Tensor]:
+    """Differentiable Splatter with g_s: normalised planes; gradients flow to the
+    features, the prior grid and the g_s parameters."""
+    geom = (grid.kind, tuple(grid.dims), grid.K, grid.contraction, grid.contract_scale)
+    gsmeta = (gs.C_in, gs.dir_freqs, gs.hidden)
+    return list(_SplatMlpFn.apply(geom, gsmeta, int(n_samples), origins, dirs, near, far, features, gs.params,
+                                  *gs.prior))
