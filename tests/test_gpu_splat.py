@@ -152,7 +152,7 @@ def test_splat_mlp_parity(torch_cuda, kind, res, over):
     RELU_BAND of 0 (relative) are left out of the comparison."""
     import paper_2404_19760_b200 as lpb
     torch = torch_cuda
-    cfg = wl.get_config("s1" if kind == wl.VOXEL else "s2", res=res, **over)
+    cfg = wl.get_config("s1" if kind == wl.VOXEL else "s2", res=res, S=48, **over)
     spec = _spec(cfg)
     F = 4
     widths = (32 + 32 + 6 * F, 64, 32)
