@@ -433,6 +433,12 @@ def cpu_splat_rate(cfg, target_s: float):
     import oracle
     spec = oracle.GridSpec(cfg.kind, (cfg.res,) * 3, cfg.K, cfg.contraction, cfg.contract_a)
     gout = wl.make_grid_grad(spec.shapes())
+    g = None
+    if cfg.splat_mlp:
+        prior = [wl.counter_uniform(9 + i, np.arange(int(np.prod(sh)), dtype=np.uint64), -1, 1).reshape(sh)
+                 for i, sh in enumerate(spec.shapes())]
+        g = oracle.SplatMlp(prior, cfg.widths, wl.make_mlp(cfg.widths, seed=10, hidden_bias_scale=0.2), cfg.K,
+                            cfg.dir_freqs)
     idx_all = wl.subset_indices(cfg, 1 << 14)
     n, total_rays, total_t, pos = 256, 0, 0.0, 0
     while total_t < target_s:
@@ -441,8 +447,12 @@ def cpu_splat_rate(cfg, target_s: float):
         R = oracle.Rays(*wl.make_rays(cfg, idx), cfg.S)
         v = wl.make_features(idx, cfg.K)
         t0 = time.perf_counter()
-        out, th, wt = oracle.splat_forward(spec, R, v)
-        oracle.splat_backward(spec, R, gout, wt)
+        if g is not None:
+            out, th, wt = oracle.splat_forward_mlp(spec, R, v, g)
+            oracle.splat_backward_mlp(spec, R, v, g, gout, wt)
+        else:
+            out, th, wt = oracle.splat_forward(spec, R, v)
+            oracle.splat_backward(spec, R, gout, wt)
         total_t += time.perf_counter() - t0
         total_rays += len(idx)
     return total_rays / total_t, total_rays, total_t
@@ -469,6 +479,14 @@ def run_splat(args):
     o, d, near, far = (T(a) for a in wl.make_rays(cfg, start=lo, count=M))
     feats = T(wl.make_features(np.arange(lo, hi), cfg.K))
     gout = [T(g) for g in wl.make_grid_grad(grid.shapes())]
+    gs = None
+    if cfg.splat_mlp:   # g_s of Eq. 2: prior grid of the target's shape, MLP widths cfg.widths
+        prior = [T(wl.counter_uniform(9 + i, np.arange(int(np.prod(sh)), dtype=np.uint64), -1, 1).reshape(sh))
+                 for i, sh in enumerate(grid.shapes())]
+        gs = lpb.SplatMlp(T(wl.make_mlp(cfg.widths, seed=10, hidden_bias_scale=0.2)), prior, cfg.K, cfg.dir_freqs,
+                          cfg.widths[1])
+        gprior = [torch.zeros_like(p) for p in prior]
+        gparams = torch.zeros_like(gs.params)
     theta, weight = grid.zeros(dev), grid.zeros(dev, 1)
     gf = torch.empty((M, cfg.K), device=dev)
     stream = torch.cuda.current_stream()
@@ -478,7 +496,10 @@ def run_splat(args):
             t.zero_()
         if ev:
             ev[0].record(stream)
-        lpb.splat_forward(grid, o, d, near, far, S, feats, theta, weight)
+        if gs is not None:
+            lpb.splat_forward_mlp(grid, o, d, near, far, S, feats, gs, theta, weight)
+        else:
+            lpb.splat_forward(grid, o, d, near, far, S, feats, theta, weight)
         if world > 1:   # the splat of a sharded view batch is a sum over ranks (one all-reduce)
             for t in theta + weight:
                 dist.all_reduce(t)
@@ -487,7 +508,10 @@ def run_splat(args):
         lpb.splat_normalize(grid, theta, weight, out=theta)
         if ev:
             ev[2].record(stream)
-        lpb.splat_backward(grid, o, d, near, far, S, gout, weight, gf)
+        if gs is not None:
+            lpb.splat_backward_mlp(grid, o, d, near, far, S, feats, gs, gout, weight, gf, gprior, gparams)
+        else:
+            lpb.splat_backward(grid, o, d, near, far, S, gout, weight, gf)
         if ev:
             ev[3].record(stream)
 
@@ -537,7 +561,7 @@ def run_splat(args):
     red_b = corners * (cfg.K * 4 + 4)          # feature + weight reductions per sample
     ach = red_b * M * S / (t_f / 1000.0) / 1e9
     line = {
-        "metric": "rays/s splat fwd+bwd", "value": cfg.n_rays / (ms / 1000.0), "unit": "rays/s", "n_gpus": world,
+        "metric": "rays/s splat fwd+bwd" + (" (g_s)" if gs is not None else ""), "value": cfg.n_rays / (ms / 1000.0), "unit": "rays/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.note}", "rays": cfg.n_rays, "samples_per_ray": S,
@@ -545,7 +569,8 @@ def run_splat(args):
                    "parallelism": f"dp{world} (rays sharded, grid all-reduce)",
                    "l2": "theta + theta_weight (grid-sized, L2-resident for s2, not for s1) re-zeroed every step"},
         "breakdown_ms": {"splat_fwd": t_f, "normalize": t_n, "splat_bwd": t_b},
-        "roofline": {"bound": "l2_atomic", "kernel": "lp_splat_fwd_kernel", "achieved": ach, "peak": L2_RED_GBS,
+        "roofline": {"bound": "l2_atomic", "kernel": "lp_splat_mlp_fwd_kernel" if gs is not None else "lp_splat_fwd_kernel",
+                     "achieved": ach, "peak": L2_RED_GBS,
                      "unit": "GB/s", "frac": ach / L2_RED_GBS, "traffic": None,
                      "algorithmic": f"{red_b} B of fp32 reductions per sample (corners x (K + 1) x 4)",
                      "peak_source": "measured: scripts/red_bench.cu, profiles/r1_red_bench.txt"},

@@ -94,6 +94,7 @@ class Config:
     near_far: Optional[tuple] = None   # constant (near, far) for every ray (unbounded scenes)
     op: str = "render"        # "render" (the renderer) or "splat" (the Splatter: widths unused)
     dir_freqs: int = 0        # F > 0: view-dependent colour, g_sigma(h) and g_v(h, direnc(d))
+    splat_mlp: bool = False   # Splatter with g_s (Eq. 2): prior grid + MLP (dir_freqs = F of its direnc)
 
     @property
     def n_rays(self) -> int:
@@ -158,6 +159,14 @@ CONFIGS = {
                  "splatter: 64 feature maps of 128x128x32 into a 160^3 voxel grid, 160 points/ray", op="splat"),
     "s2": Config("s2", TRIPLANE, 160, 32, (32, 4), 64, 128, 160,
                  "splatter: 64 feature maps of 128x128x32 into 3x160x160 triplanes, 160 points/ray", op="splat"),
+    # ... with the MLP g_s of Eq. 2 (v~ = g_s(v, h_prior(x), direnc(d)); 32-channel prior grid of
+    # the target's shape, F = 4, hidden 64; reading R30) -- the paper's triplane Splatter
+    "s1g": Config("s1g", VOXEL, 160, 32, (88, 64, 32), 64, 128, 160,
+                  "splatter with g_s: 64 maps of 128x128x32 into a 160^3 voxel grid, prior 160^3x32, 160 points/ray",
+                  op="splat", dir_freqs=4, splat_mlp=True),
+    "s2g": Config("s2g", TRIPLANE, 160, 32, (88, 64, 32), 64, 128, 160,
+                  "splatter with g_s: 64 maps of 128x128x32 into 3x160x160 triplanes, prior of the same shape, "
+                  "160 points/ray", op="splat", dir_freqs=4, splat_mlp=True),
 }
 
 
