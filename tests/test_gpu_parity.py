@@ -289,7 +289,7 @@ def test_ragged_tail_other_kernel_families(torch_cuda, cfg):
     """M not a multiple of 128 and minimal S on the 3-layer (K1tc2/K2tc2) and the
     view-dependent (K1tcv/K2tcv) kernels."""
     import dataclasses
-    idx = np.arange(1000, dtype=np.int64) * 7 + 3
+    idx = np.arange(1000, dtype=np.int64) * 4 + 3      # within c1v's 4096 rays
     pb = problem_np(cfg, idx=idx, with_gdepth=True)
     _assert(_compare(_gpu_fwd_bwd(torch_cuda, pb, depth=True), oracle_reference(pb, depth=True)))
     pb2 = dict(pb)
