@@ -69,6 +69,16 @@ def algorithmic_flops_per_sample(cfg):
     return 2 * fwd, 2 * bwd
 
 
+def tensor_flops_per_sample_bwd(cfg):
+    """Split-bf16 MMA FLOP the one-hidden-layer backward issues per sample (K2tc):
+    Z recompute 6 products x 2 K_p H, dH 3 x 2 H K_p, weight gradients 3 x 2 (2 H_p) (K_p + 16)."""
+    K = cfg.K
+    KP = max(K, 16)
+    H = cfg.widths[1]
+    HP = max(H, 64)
+    return 6 * 2 * KP * H + 3 * 2 * H * KP + 3 * 2 * (2 * HP) * (KP + 16)
+
+
 def fp32_peak_tflops(sm_mhz):
     return N_SM * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
 
@@ -388,6 +398,7 @@ def run_ours(args):
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     alu_peak = fp32_peak_tflops(sm_max)
     traffic = ncu_traffic(cfg.name)
+    tc_bwd_f = tensor_flops_per_sample_bwd(cfg)
     kname = (("lp_fwd_tc2_kernel (K1tc2)", "lp_bwd_tc2_kernel (K2tc2, backward)") if len(cfg.widths) == 4 else
              ("lp_fwd_tc_kernel (K1tc)", "lp_bwd_tc_kernel (K2tc, backward)"))
     line = {
@@ -407,6 +418,14 @@ def run_ours(args):
                              "peak_tflops": alu_peak,
                              "peak_source": f"FP32 FFMA {N_SM} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz "
                                             f"(sm_max_mhz {peak_src}); algorithmic {bwd_f} FLOP/sample"},
+                     "tensor": {"issued_bf16_tflops": tc_bwd_f * samples / (t_bwd / 1000.0) / 1e12,
+                                "peak_tflops": float(peaks.get("bf16_tflops", 2250.0)),
+                                "peak_source": f"MEASURED_PEAKS.json bf16 ({peak_src}); issued split-bf16 "
+                                               f"MMA FLOP per sample {tc_bwd_f}"},
+                     "hbm": {"achieved_gbs": ((traffic * M / traffic_rays(cfg.name)) / (t_bwd / 1000.0) / 1e9)
+                             if traffic else None,
+                             "peak_gbs": float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS)),
+                             "peak_source": f"MEASURED_PEAKS.json ({peak_src}); traffic from profiles/ncu_traffic.json"},
                      "fwd_kernel": {"kernel": kname[0],
                                     "achieved_tflops": fwd_f * samples / (t_fwd / 1000.0) / 1e12,
                                     "alu_frac": fwd_f * samples / (t_fwd / 1000.0) / 1e12 / alu_peak}},
