@@ -295,3 +295,33 @@ def test_ragged_tail_other_kernel_families(torch_cuda, cfg):
     pb2 = dict(pb)
     pb2["cfg"] = dataclasses.replace(pb["cfg"], S=2)
     _assert(_compare(_gpu_fwd_bwd(torch_cuda, pb2, depth=True), oracle_reference(pb2, depth=True)))
+
+
+_FMA_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from tests.gpu_problem import problem_np, oracle_reference, parity_errors, to_cuda
+import paper_2404_19760_b200 as lpb
+pb = problem_np({cfg!r}, n={n})
+field, t = to_cuda(pb)
+out, tau, depth = lpb.render_forward(field, t["o"], t["d"], t["near"], t["far"], pb["cfg"].S, t["bg"], return_depth=True)
+gpl, gpar = lpb.render_backward(field, t["o"], t["d"], t["near"], t["far"], pb["cfg"].S, tau, t["go"], t["gt"], t["bg"])
+g = dict(out=out.cpu().numpy(), tau=tau.cpu().numpy(), gplanes=[a.cpu().numpy() for a in gpl], gparams=gpar.cpu().numpy())
+e = parity_errors(g, oracle_reference(pb))
+print(e)
+assert e["out"] < 1e-4 and e["tau"] < 1e-4 and all(v < 1e-3 for k, v in e.items() if k.startswith("g")), e
+"""
+
+
+@pytest.mark.parametrize("cfg,n", [("c1", 2048), ("c4", 1024), ("c4p", 512), ("c2", 256)])
+def test_ffma_baseline_kernels_parity(torch_cuda, cfg, n):
+    """The FFMA kernels K1/K2 (the A/B baseline, LP_KERNELS=fma, read once per process)
+    against the oracle, in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LP_KERNELS="fma")
+    r = subprocess.run([sys.executable, "-c", _FMA_SCRIPT.format(root=root, cfg=cfg, n=n)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
