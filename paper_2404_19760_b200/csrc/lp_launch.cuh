@@ -122,7 +122,7 @@ lp_status run_bwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
       static LaunchShape shape;
       constexpr int G = kBwdGroups, T = LP_BWD_T;
       return launch(lp::lp_bwd_tc_kernel<KIND, K, HID, G, T>, shape, lp::BwdTcSmem<KIND, K, HID, G, T>::BYTES,
-                    128 * T * G, G, a.M, a, w, s);
+                    128 * T * G + 32 * lp::bwd_scatter_warps<T>(), G, a.M, a, w, s);
     }
   }
   if constexpr (NH == 2 && HID == 64 && K >= 8) {

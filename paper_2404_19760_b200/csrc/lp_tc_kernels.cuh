@@ -91,7 +91,8 @@ struct TcShape {
 
 // ---------------------------------------------------------------- taps (F2, F3)
 // Compact per-plane record of a sample: (element offset of corner (0,0[,0]),
-// f_a, f_b[, f_c]) as float4; offset -1 marks a point outside the cube (R11).
+// f_a, f_b[, f_c | packed cell indices]) as float4; offset -1 marks a point
+// outside the cube (R11).
 template <int KIND, int K>
 __device__ __forceinline__ void write_taps(float4* rec, const double x[3], const GridDims& g) {
   const bool inside = fabs(x[0]) <= 1.0 && fabs(x[1]) <= 1.0 && fabs(x[2]) <= 1.0;
@@ -104,9 +105,10 @@ __device__ __forceinline__ void write_taps(float4* rec, const double x[3], const
     const int base = inside ? (((ix * g.W + iy) * g.D + iz) * K) : -1;
     rec[0] = make_float4(__int_as_float(base), fx, fy, fz);
   } else {
-    rec[0] = make_float4(__int_as_float(inside ? (ix * g.W + iy) * K : -1), fx, fy, 0.0f);
-    rec[1] = make_float4(__int_as_float(inside ? (iy * g.D + iz) * K : -1), fy, fz, 0.0f);
-    rec[2] = make_float4(__int_as_float(inside ? (iz * g.H + ix) * K : -1), fz, fx, 0.0f);
+    // .w: the cell's (a, b) indices packed as a << 16 | b (window scatter, coop_gather)
+    rec[0] = make_float4(__int_as_float(inside ? (ix * g.W + iy) * K : -1), fx, fy, __int_as_float((ix << 16) | iy));
+    rec[1] = make_float4(__int_as_float(inside ? (iy * g.D + iz) * K : -1), fy, fz, __int_as_float((iy << 16) | iz));
+    rec[2] = make_float4(__int_as_float(inside ? (iz * g.H + ix) * K : -1), fz, fx, __int_as_float((iz << 16) | ix));
   }
 }
 
@@ -144,11 +146,91 @@ __device__ __forceinline__ void record_corners(const float4 rec, int p, const Gr
   }
 }
 
+// Row (ray of the 128-ray tile) a lane serves in cooperative iteration `it`. A warp's
+// 32 rays are an 8x4-pixel block in raster order (workload `pixel_of`); with K = 32
+// (4 rays per iteration) an iteration takes a 2x2-pixel quad, whose corner sets
+// overlap most (window scatter below); otherwise consecutive rows.
+template <int RPI>
+__device__ __forceinline__ int coop_row(int row0, int it, int sub) {
+  if constexpr (RPI == 4) return row0 + ((it >> 2) * 2 + (sub >> 1)) * 8 + (it & 3) * 2 + (sub & 1);
+  else return row0 + it * RPI + sub;
+}
+
+#ifndef LP_WINDOW_SCATTER
+#define LP_WINDOW_SCATTER 0
+#endif
+
+// B6 for one triplane plane and the 4 rays of a cooperative iteration (K = 32),
+// merged over shared corners. If the inside rays' cells span at most 3 x 3 cells,
+// the union of their corners lies in a 4 x 4 vertex window anchored at the minimum
+// cell (amin, bmin); lane (sub, ch) owns window column bmin + sub and, for each row
+// amin + k, sums w_t(vertex) dh_t over the rays t (the bilinear weight factors per
+// axis), then issues one 16-byte reduction per touched vertex. The reductions of a
+// quad drop to the number of distinct corner lines (c4: ~55% of 4 per ray, c3:
+// ~33%). Returns false (nothing issued) when the cells do not fit the window; the
+// caller then reduces each ray's own corners. Sums are reassociated (fp32), as the
+// atomics already are.
+template <int K>
+__device__ __forceinline__ bool window_scatter_plane(float* gpl, const float4* ptaps, const float* dhs,
+                                                     const int (&rows)[4], int p, int sub, int sa) {
+  constexpr int NPL = 3;
+  // all shared-memory reads first (broadcast records, the rays' dh chunks): with two
+  // warps per scheduler the merge must be short dependent chains over 4 independent rays
+  float4 pr[4], d[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) pr[t] = ptaps[rows[t] * NPL + p];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) d[t] = *reinterpret_cast<const float4*>(dhs + rows[t] * (K + 4));
+  int ia[4], ib[4];
+  bool in[4];
+  int amin = 1 << 30, amax = -1, bmin = 1 << 30, bmax = -1;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int pk = __float_as_int(pr[t].w);
+    in[t] = __float_as_int(pr[t].x) >= 0;
+    ia[t] = pk >> 16;
+    ib[t] = pk & 0xffff;
+    amin = min(amin, in[t] ? ia[t] : 1 << 30);
+    amax = max(amax, in[t] ? ia[t] : -1);
+    bmin = min(bmin, in[t] ? ib[t] : 1 << 30);
+    bmax = max(bmax, in[t] ? ib[t] : -1);
+  }
+  if (amax < 0) return true;                                    // no ray inside: nothing to reduce
+  if (amax - amin > 2 || bmax - bmin > 2) return false;         // warp-uniform
+  float4 acc[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc[k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  unsigned touched = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int ca = ia[t] - amin, cb = sub - (ib[t] - bmin);   // ca in [0, 2]; this lane's column touched iff cb in {0, 1}
+    const float fa = pr[t].y, fb = pr[t].z;
+    const float m0 = (in[t] && cb == 0) ? 1.0f : 0.0f, m1 = (in[t] && cb == 1) ? 1.0f : 0.0f;
+    const float wb = fmaf(m1, fb, m0 * (1.0f - fb));
+    touched |= (m0 + m1 != 0.0f ? 3u : 0u) << ca;
+    const float4 e = make_float4(wb * d[t].x, wb * d[t].y, wb * d[t].z, wb * d[t].w);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float c = (ca == k ? 1.0f - fa : 0.0f) + (ca == k - 1 ? fa : 0.0f);
+      acc[k].x = fmaf(c, e.x, acc[k].x);
+      acc[k].y = fmaf(c, e.y, acc[k].y);
+      acc[k].z = fmaf(c, e.z, acc[k].z);
+      acc[k].w = fmaf(c, e.w, acc[k].w);
+    }
+  }
+  float* col = gpl + (amin * sa + (bmin + sub) * K);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if ((touched >> k) & 1u) atomicAdd(reinterpret_cast<float4*>(col + k * sa), acc[k]);
+  return true;
+}
+
 // Warp-cooperative gather of the warp's 32 rays: lane = (ray RPI-subgroup, chunk).
 // Writes h into rows [row0, row0 + 32) of the H tile (NP bf16 pieces).
 // With SCATTER, each iteration also issues the grid-gradient reductions of the
-// previous march step for the same lane slot (records `ptaps`, dh rows `dhs`):
-// the L2 reductions of step q+1 overlap the corner loads of step q (B6 || F3).
+// previous march step for the same lane slot (records `ptaps`, dh rows `dhs`),
+// merged per quad where their corners overlap (window_scatter_plane): the L2
+// reductions of step q+1 overlap the corner loads of step q (B6 || F3).
 // Iterations [it0, it1) of the KC = K/4 per warp (two warps may split one row block).
 template <int KIND, int K, int C, int NP, bool SCATTER = false>
 __device__ __forceinline__ void coop_gather(const float* const* planes, const float4* taps, const GridDims& g,
@@ -160,7 +242,7 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
   const int ch = lane % KC, sub = lane / KC;
 #pragma unroll kGatherUnroll
   for (int it = it0; it < it1; ++it) {
-    const int row = row0 + it * RPI + sub;
+    const int row = coop_row<RPI>(row0, it, sub);
     float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
     for (int p = 0; p < NPL; ++p) {
@@ -171,7 +253,17 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
       float4 v[Corners<KIND, K>::N];
 #pragma unroll
       for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) v[cc] = __ldg(reinterpret_cast<const float4*>(pl + c.off[cc]));
-      if constexpr (SCATTER) {
+      bool merged = false;
+      if constexpr (SCATTER && KIND == 0 && RPI == 4 && LP_WINDOW_SCATTER) {
+        if (!wplanes) {
+          int rows[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) rows[t] = coop_row<RPI>(row0, it, t);
+          const int sa = (p == 0 ? g.W : p == 1 ? g.D : g.H) * K;
+          merged = window_scatter_plane<K>(gplanes[p] + 4 * ch, ptaps, dhs + 4 * ch, rows, p, sub, sa);
+        }
+      }
+      if constexpr (SCATTER) if (!merged) {
         const float4 prec = ptaps[row * NPL + p];
         if (__float_as_int(prec.x) >= 0) {
           const float4 d = *reinterpret_cast<const float4*>(dhs + row * (K + 4) + 4 * ch);
@@ -180,6 +272,9 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
           float* gpl = gplanes[p] + 4 * ch;
 #pragma unroll
           for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) {
+#ifdef LP_ABL_SKIPRED   // ablation (timing only, wrong results): bit (p * 4 + cc) set = reduction skipped
+            if ((LP_ABL_SKIPRED >> (p * 4 + cc)) & 1) continue;
+#endif
             const float w = pc.w[cc];
             atomicAdd(reinterpret_cast<float4*>(gpl + pc.off[cc]), make_float4(w * d.x, w * d.y, w * d.z, w * d.w));
           }
@@ -211,7 +306,7 @@ __device__ __forceinline__ void coop_scatter(float* const* gplanes, const float4
   const int ch = lane % KC, sub = lane / KC;
 #pragma unroll 1
   for (int it = it0; it < it1; ++it) {
-    const int row = row0 + it * RPI + sub;
+    const int row = coop_row<RPI>(row0, it, sub);
     const float4 d = *reinterpret_cast<const float4*>(dhs + row * (K + 4) + 4 * ch);
 #pragma unroll
     for (int p = 0; p < NPL; ++p) {
@@ -423,8 +518,8 @@ struct BwdTcSmem {
   static constexpr uint32_t TAPS = DA + 2 * S::DA_PIECE;      // [T halves][128][NPL]
   static constexpr uint32_t XO = TAPS + T * S::TAPS;           // T = 2: [2][128] float4 partial outputs
   static constexpr uint32_t GSIZE = (XO + (T == 2 ? 2 * 128 * 16 : 0) + 127) & ~127u;
-  static constexpr uint32_t BAR = GRP + G * GSIZE;             // 2 mbarriers per group + tmem slot
-  static constexpr uint32_t BYTES = BAR + 16 * G + 16;
+  static constexpr uint32_t BAR = GRP + G * GSIZE;             // 4 mbarriers per group + tmem slot
+  static constexpr uint32_t BYTES = BAR + 32 * G + 16;
   static constexpr uint32_t TMEM_COLS = G == 1 ? 256 : 512;
   static_assert(S::DA_PIECE >= 128 * (K + 4) * 4 && S::DA_PIECE >= 128 * S::NPL * 16, "staging fits the DA tile");
 };
@@ -435,8 +530,20 @@ struct BwdTcSmem {
 // [half*HID/2, (half+1)*HID/2) of every epilogue and half of the gather
 // iterations, as in lp_tc2_kernels.cuh; the halves exchange their partial
 // output-layer sums through shared memory.
+#ifndef LP_BWD_SW
+#define LP_BWD_SW 4
+#endif
+// Scatter warps of K2tc (T = 1): the grid-gradient reductions (B6) of each staged
+// step are issued by dedicated warps (SW / G per group) while the group's compute
+// warps gather and contract the next step, so the L2 reductions are not in the
+// compute warps' instruction stream. 0: the compute warps issue them inside the
+// next step's gather (fused scatter).
+constexpr int kBwdScatterWarps = LP_BWD_SW;
+template <int T>
+constexpr int bwd_scatter_warps() { return T == 1 ? kBwdScatterWarps : 0; }
+
 template <int KIND, int K, int HID, int G, int T>
-__global__ void __launch_bounds__(128 * T * G, 1) lp_bwd_tc_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(128 * T * G + 32 * bwd_scatter_warps<T>(), 1) lp_bwd_tc_kernel(const KernelArgs a) {
   using S = TcShape<KIND, K, HID>;
   using L = BwdTcSmem<KIND, K, HID, G, T>;
   constexpr int GT = 128 * T, HH = HID / T, KC = K / 4;
@@ -448,7 +555,9 @@ __global__ void __launch_bounds__(128 * T * G, 1) lp_bwd_tc_kernel(const KernelA
   uint8_t* w0p = smem + L::W0P;
   float* fp = reinterpret_cast<float*>(smem + L::FP);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 16 * G);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 32 * G);
+  constexpr int SW = bwd_scatter_warps<T>(), SWG = SW / G;
+  static_assert(SW % G == 0 && (SW == 0 || 4 % SWG == 0), "scatter warps per group");
 
   const int g = threadIdx.x / GT, gt = threadIdx.x % GT, hf = gt >> 7, rt = gt & 127;
   const int wg = (gt >> 5) & 3, lane = gt & 31;
@@ -468,256 +577,294 @@ __global__ void __launch_bounds__(128 * T * G, 1) lp_bwd_tc_kernel(const KernelA
     *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
   __syncthreads();
   stage_tc_weights<K, HID, S::KP>(w0p, fp, a.params);
-  if (threadIdx.x < 2 * G) tc::mbar_init(&bars[threadIdx.x], 1);
+  // per group: Z done, dH/dW done (tcgen05.commit), staged (128 compute threads),
+  // drained (the group's scatter warps)
+  if (threadIdx.x < 4 * G) tc::mbar_init(&bars[threadIdx.x], threadIdx.x % 4 == 2 ? 128 : threadIdx.x % 4 == 3 ? SWG : 1);
   if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
   tc::fence_async_smem();
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
-  const uint32_t tbase = *tslot + (uint32_t)(g * 256);
-  const uint32_t tZ = tbase, tDH = tbase + 64, tW = tbase + 96;
-  // ones column of the H tile (piece 0 = 1, pieces 1, 2 = 0; written once, never overwritten)
-  if (hf == 0) *reinterpret_cast<__nv_bfloat16*>(Ht + tc::cm_off(rt, S::KP, S::HC)) = __float2bfloat16_rn(1.0f);
-  tc::fence_async_smem();
-  const uint32_t tlane = (uint32_t)(wg * 32) << 16;
-  uint64_t* bar_z = &bars[2 * g];
-  uint64_t* bar_d = &bars[2 * g + 1];
-
-  const int R = a.S - 1;
-  const float* planes[3] = {a.grid[0], a.grid[1], a.grid[2]};
-  float* gplanes[3] = {a.ggrid[0], a.ggrid[1], a.ggrid[2]};
-  float bg[kC];
-#pragma unroll
-  for (int c = 0; c < kC; ++c) bg[c] = a.bg ? __ldg(a.bg + c) : 0.0f;
-  const uint32_t id_z = tc::idesc_bf16(128, HID, 0, 0);
-  const uint32_t id_dh = tc::idesc_bf16(128, S::KP, 0, 1);
-  const uint32_t id_w = tc::idesc_bf16(128, S::HC, 1, 1);
-  const uint32_t h_addr = tc::smem_u32(Ht), w_addr = tc::smem_u32(w0p), da_addr = tc::smem_u32(DAt);
-  uint32_t phase = 0, wacc = 0;   // wacc: weight-gradient accumulators initialised (issuing thread)
-  float dbo[kOut];
-#pragma unroll
-  for (int i = 0; i < kOut; ++i) dbo[i] = 0.0f;
-  LP_PT_DECL
-
-  const int64_t ntiles = (a.M + 127) / 128;
-  for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
-    const int64_t r0 = tile * 128 + rt;
-    const bool valid = r0 < a.M;
-    const int64_t r = valid ? r0 : a.M - 1;   // tail rows march a real ray with zero upstream
-    const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
-    float p[kC];
-#pragma unroll
-    for (int c = 0; c < kC; ++c) p[c] = valid ? __ldg(a.grad_out + 3 * r + c) : 0.0f;
-    const float gtau = (valid && a.grad_tau) ? __ldg(a.grad_tau + r) : 0.0f;
-    const float gdep = (valid && a.grad_depth) ? __ldg(a.grad_depth + r) : 0.0f;
-    const float tauR = __ldg(a.tau + r);
-    float pbg = 0.0f;
-#pragma unroll
-    for (int c = 0; c < kC; ++c) pbg = fmaf(p[c], bg[c], pbg);
-    float G_ = expf(-tauR) * pbg;      // B1
-    float U = 0.0f, Ue = 0.0f;
-
-    for (int q = R; q >= 0; --q) {
-      // ---- B2: recompute sample q: taps, cooperative gather, Z = H W0^T
-      double x[3];
-      sample_point(ray, q, a.contract, x);
-      write_taps<KIND, K>(taps + rt * S::NPL, x, a.dims);
-      __syncwarp();
-      LP_PT(0)
-#ifndef LP_ABL_NOGATHER
-      if (pending)   // warp-uniform
-        coop_gather<KIND, K, S::HC, kBwdHPieces, true>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, gplanes, ptaps, dhs,
-                                             it0, it1);
-      else
-        coop_gather<KIND, K, S::HC, kBwdHPieces>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, nullptr, nullptr,
-                                       nullptr, it0, it1);
-      pending = false;
-#endif
-      LP_PT(1)
-      tc::fence_async_smem();
-      tc::fence_before_sync();
-      tc::named_bar(1 + g, GT);
-      LP_PT(2)
-      if (gt == 0) {
-        tc::fence_after_sync();
-        constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
-        constexpr int NPROD = kBwdHPieces == 3 ? 6 : 5;   // products with H piece < kBwdHPieces
-        uint32_t acc = 0;
-#pragma unroll
-        for (int ks = 0; ks < S::KP / 16; ++ks)
-#pragma unroll
-          for (int c = 0; c < NPROD; ++c) {
-            tc::mma_bf16(tZ, tc::desc_kmajor(h_addr + PA[c] * S::HB_PIECE, S::HC, ks),
-                         tc::desc_kmajor(w_addr + PB[c] * S::W0_PIECE, S::KP, ks), id_z, acc);
-            acc = 1;
-          }
-        tc::mma_commit(bar_z);
-      }
-      tc::mbar_wait(bar_z, phase);
-      LP_PT(3)
-      tc::fence_after_sync();
-      float a1[HH];
-      tc::tmem_ld<HH>(tZ + tlane + (uint32_t)(hf * HH), a1);
-      float o[kOut];
-      if constexpr (T == 1) {
-        tc_head_layer<HID>(fp + F::B0, fp + F::WOT, fp + F::BO, a1, o);   // a1 = relu(z + b0)
-      } else {   // this half's units: a1 = relu(z + b0), partial output layer, exchange
-        float4 part = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-#pragma unroll
-        for (int i = 0; i < HH; ++i) {
-          a1[i] = fmaxf(a1[i] + fp[F::B0 + hf * HH + i], 0.0f);
-          const float4 w = reinterpret_cast<const float4*>(fp + F::WOT)[hf * HH + i];
-          part.x = fmaf(w.x, a1[i], part.x);
-          part.y = fmaf(w.y, a1[i], part.y);
-          part.z = fmaf(w.z, a1[i], part.z);
-          part.w = fmaf(w.w, a1[i], part.w);
+  if constexpr (SW > 0) {
+    if (threadIdx.x >= GT * G) {   // ---- scatter warps: B6 of every step the group stages
+      const int sw = (threadIdx.x - GT * G) / 32, lane = threadIdx.x & 31;
+      const int sg = sw / SWG, part = sw % SWG;
+      const uint8_t* sgsm = smem + L::GRP + sg * L::GSIZE;
+      const float* sdhs = reinterpret_cast<const float*>(sgsm + L::DA);
+      const float4* sptaps = reinterpret_cast<const float4*>(sgsm + L::PTAPS);
+      float* sgpl[3] = {a.ggrid[0], a.ggrid[1], a.ggrid[2]};
+      uint32_t ph = 0;
+      const int64_t nt = (a.M + 127) / 128;
+      for (int64_t tile = (int64_t)blockIdx.x * G + sg; tile < nt; tile += (int64_t)gridDim.x * G)
+        for (int q = 0; q < a.S; ++q) {
+          tc::mbar_wait(&bars[4 * sg + 2], ph);
+          ph ^= 1;
+          for (int rb = part; rb < 4; rb += SWG) coop_scatter<KIND, K>(sgpl, sptaps, a.dims, sdhs, rb * 32, lane);
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&bars[4 * sg + 3]);
         }
-        xo[hf * 128 + rt] = part;
+    }
+  }
+  if (SW == 0 || threadIdx.x < GT * G) {   // ---- compute warps
+    const uint32_t tbase = *tslot + (uint32_t)(g * 256);
+    const uint32_t tZ = tbase, tDH = tbase + 64, tW = tbase + 96;
+    // ones column of the H tile (piece 0 = 1, pieces 1, 2 = 0; written once, never overwritten)
+    if (hf == 0) *reinterpret_cast<__nv_bfloat16*>(Ht + tc::cm_off(rt, S::KP, S::HC)) = __float2bfloat16_rn(1.0f);
+    tc::fence_async_smem();
+    const uint32_t tlane = (uint32_t)(wg * 32) << 16;
+    uint64_t* bar_z = &bars[4 * g];
+    uint64_t* bar_d = &bars[4 * g + 1];
+    uint64_t* bar_st = &bars[4 * g + 2];
+    uint64_t* bar_dr = &bars[4 * g + 3];
+    uint32_t dphase = 0;
+    bool staged = false;   // a step of this group is staged for the scatter warps
+
+    const int R = a.S - 1;
+    const float* planes[3] = {a.grid[0], a.grid[1], a.grid[2]};
+    float* gplanes[3] = {a.ggrid[0], a.ggrid[1], a.ggrid[2]};
+    float bg[kC];
+#pragma unroll
+    for (int c = 0; c < kC; ++c) bg[c] = a.bg ? __ldg(a.bg + c) : 0.0f;
+    const uint32_t id_z = tc::idesc_bf16(128, HID, 0, 0);
+    const uint32_t id_dh = tc::idesc_bf16(128, S::KP, 0, 1);
+    const uint32_t id_w = tc::idesc_bf16(128, S::HC, 1, 1);
+    const uint32_t h_addr = tc::smem_u32(Ht), w_addr = tc::smem_u32(w0p), da_addr = tc::smem_u32(DAt);
+    uint32_t phase = 0, wacc = 0;   // wacc: weight-gradient accumulators initialised (issuing thread)
+    float dbo[kOut];
+#pragma unroll
+    for (int i = 0; i < kOut; ++i) dbo[i] = 0.0f;
+    LP_PT_DECL
+
+    const int64_t ntiles = (a.M + 127) / 128;
+    for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
+      const int64_t r0 = tile * 128 + rt;
+      const bool valid = r0 < a.M;
+      const int64_t r = valid ? r0 : a.M - 1;   // tail rows march a real ray with zero upstream
+      const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
+      float p[kC];
+#pragma unroll
+      for (int c = 0; c < kC; ++c) p[c] = valid ? __ldg(a.grad_out + 3 * r + c) : 0.0f;
+      const float gtau = (valid && a.grad_tau) ? __ldg(a.grad_tau + r) : 0.0f;
+      const float gdep = (valid && a.grad_depth) ? __ldg(a.grad_depth + r) : 0.0f;
+      const float tauR = __ldg(a.tau + r);
+      float pbg = 0.0f;
+#pragma unroll
+      for (int c = 0; c < kC; ++c) pbg = fmaf(p[c], bg[c], pbg);
+      float G_ = expf(-tauR) * pbg;      // B1
+      float U = 0.0f, Ue = 0.0f;
+
+      for (int q = R; q >= 0; --q) {
+        // ---- B2: recompute sample q: taps, cooperative gather, Z = H W0^T
+        double x[3];
+        sample_point(ray, q, a.contract, x);
+        write_taps<KIND, K>(taps + rt * S::NPL, x, a.dims);
+        __syncwarp();
+        LP_PT(0)
+#ifndef LP_ABL_NOGATHER
+        if (SW == 0 && pending)   // warp-uniform
+          coop_gather<KIND, K, S::HC, kBwdHPieces, true>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, gplanes, ptaps, dhs,
+                                               it0, it1);
+        else
+          coop_gather<KIND, K, S::HC, kBwdHPieces>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, nullptr, nullptr,
+                                         nullptr, it0, it1);
+        pending = false;
+#endif
+        LP_PT(1)
+        tc::fence_async_smem();
         tc::fence_before_sync();
         tc::named_bar(1 + g, GT);
-        const float4 p0 = xo[rt], p1 = xo[128 + rt];
-        o[0] = fp[F::BO + 0] + p0.x + p1.x;
-        o[1] = fp[F::BO + 1] + p0.y + p1.y;
-        o[2] = fp[F::BO + 2] + p0.z + p1.z;
-        o[3] = fp[F::BO + 3] + p0.w + p1.w;
-      }
-      const float s_sig = sigmoid_f(o[0]);
-      const float ds = (float)ray.delta * softplus_f(o[0]);
-      float col[kC];
+        LP_PT(2)
+        if (gt == 0) {
+          tc::fence_after_sync();
+          constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
+          constexpr int NPROD = kBwdHPieces == 3 ? 6 : 5;   // products with H piece < kBwdHPieces
+          uint32_t acc = 0;
 #pragma unroll
-      for (int c = 0; c < kC; ++c) col[c] = sigmoid_f(o[1 + c]);
-      // ---- B3: Eq. 3, log-domain reverse update (R12)
-      const float tau_q = (tauR - U) - Ue;
-      two_sum_add(U, Ue, ds);
-      const float tau_qm1 = (tauR - U) - Ue;
-      float aq = 0.0f;
+          for (int ks = 0; ks < S::KP / 16; ++ks)
 #pragma unroll
-      for (int c = 0; c < kC; ++c) aq = fmaf(p[c], col[c], aq);
-      aq = fmaf(gdep, (float)ray_t(ray, q), aq);   // depth channel: "colour" t_q, no MLP gradient
-      const float wq = q > 0 ? expf(-tau_qm1) * (-expm1f(-ds)) : 0.0f;
-      const float Tq_aq = q > 0 ? expf(-tau_q) * aq : 0.0f;
-      const float dsig = (float)ray.delta * (gtau - (G_ - Tq_aq));
-      G_ = fmaf(wq, aq, G_);
-      // ---- B4: head VJP
-      float dout[8];
-      dout[0] = dsig * s_sig;
-#pragma unroll
-      for (int c = 0; c < kC; ++c) dout[1 + c] = wq * p[c] * col[c] * (1.0f - col[c]);
-#pragma unroll
-      for (int c = 4; c < 8; ++c) dout[c] = 0.0f;
-      // ---- B5: per 8-unit chunk: stage a1, delta1 = ReLU'(z) (Wo^T dout), stage delta1
-      if (hf == 0) {
-#pragma unroll
-        for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
-        tc::store8<2>(Ht, S::HB_PIECE, rt, S::KP + 8, S::HC, dout);
-      }
-#pragma unroll
-      for (int c = 0; c < HH / 8; ++c) {
-        tc::store8<2>(DAt, S::DA_PIECE, rt, S::HP + hf * HH + 8 * c, 2 * S::HP, a1 + 8 * c);
-        float d1[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const float4 w = reinterpret_cast<const float4*>(fp + F::WOT)[hf * HH + 8 * c + u];
-          float sacc = w.x * dout[0];
-          sacc = fmaf(w.y, dout[1], sacc);
-          sacc = fmaf(w.z, dout[2], sacc);
-          sacc = fmaf(w.w, dout[3], sacc);
-          d1[u] = a1[8 * c + u] > 0.0f ? sacc : 0.0f;
+            for (int c = 0; c < NPROD; ++c) {
+              tc::mma_bf16(tZ, tc::desc_kmajor(h_addr + PA[c] * S::HB_PIECE, S::HC, ks),
+                           tc::desc_kmajor(w_addr + PB[c] * S::W0_PIECE, S::KP, ks), id_z, acc);
+              acc = 1;
+            }
+          tc::mma_commit(bar_z);
         }
-        tc::store8<2>(DAt, S::DA_PIECE, rt, hf * HH + 8 * c, 2 * S::HP, d1);
-      }
-      LP_PT(4)
-      tc::fence_async_smem();
-      tc::fence_before_sync();
-      tc::named_bar(1 + g, GT);
-      if (gt == 0) {
+        tc::mbar_wait(bar_z, phase);
+        LP_PT(3)
         tc::fence_after_sync();
-        constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
-        // dH = D1 W0   (B = W0 viewed MN-major: MN = channel, K = hidden)
+        float a1[HH];
+        tc::tmem_ld<HH>(tZ + tlane + (uint32_t)(hf * HH), a1);
+        float o[kOut];
+        if constexpr (T == 1) {
+          tc_head_layer<HID>(fp + F::B0, fp + F::WOT, fp + F::BO, a1, o);   // a1 = relu(z + b0)
+        } else {   // this half's units: a1 = relu(z + b0), partial output layer, exchange
+          float4 part = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
-        for (int ks = 0; ks < HID / 16; ++ks)
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            tc::mma_bf16(tDH, tc::desc_kmajor(da_addr + QA[c] * S::DA_PIECE, 2 * S::HP, ks),
-                         tc::desc_mnmajor(w_addr + QB[c] * S::W0_PIECE, S::KP, ks), id_dh, (ks | c) != 0);
-        // [dW0 | db0 | . ; . | dWo^T] += [D1 | A1]^T [H | 1 | DOUT]   (K = the 128 samples of this step)
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            tc::mma_bf16(tW, tc::desc_mnmajor(da_addr + QA[c] * S::DA_PIECE, 2 * S::HP, ks),
-                         tc::desc_mnmajor(h_addr + QB[c] * S::HB_PIECE, S::HC, ks), id_w, wacc);
-            wacc = 1;
+          for (int i = 0; i < HH; ++i) {
+            a1[i] = fmaxf(a1[i] + fp[F::B0 + hf * HH + i], 0.0f);
+            const float4 w = reinterpret_cast<const float4*>(fp + F::WOT)[hf * HH + i];
+            part.x = fmaf(w.x, a1[i], part.x);
+            part.y = fmaf(w.y, a1[i], part.y);
+            part.z = fmaf(w.z, a1[i], part.z);
+            part.w = fmaf(w.w, a1[i], part.w);
           }
-        tc::mma_commit(bar_d);
-      }
-      tc::mbar_wait(bar_d, phase);
-      phase ^= 1;
-      LP_PT(5)
-      tc::fence_after_sync();
-      // ---- B6: dH row -> fp32 staging -> cooperative scatter
-      {
-        constexpr int HK = S::KP / T;   // this thread's dH columns
-        float dh[HK];
-        tc::tmem_ld<HK>(tDH + tlane + (uint32_t)(hf * HK), dh);
+          xo[hf * 128 + rt] = part;
+          tc::fence_before_sync();
+          tc::named_bar(1 + g, GT);
+          const float4 p0 = xo[rt], p1 = xo[128 + rt];
+          o[0] = fp[F::BO + 0] + p0.x + p1.x;
+          o[1] = fp[F::BO + 1] + p0.y + p1.y;
+          o[2] = fp[F::BO + 2] + p0.z + p1.z;
+          o[3] = fp[F::BO + 3] + p0.w + p1.w;
+        }
+        const float s_sig = sigmoid_f(o[0]);
+        const float ds = (float)ray.delta * softplus_f(o[0]);
+        float col[kC];
 #pragma unroll
-        for (int k4 = 0; k4 < HK / 4; ++k4)
-          if (hf * HK + 4 * k4 < K)
-            *reinterpret_cast<float4*>(dhs + rt * (K + 4) + hf * HK + 4 * k4) =
-                make_float4(dh[4 * k4], dh[4 * k4 + 1], dh[4 * k4 + 2], dh[4 * k4 + 3]);
-      }
-      tc::fence_before_sync();
-      // keep this step's tap records for its scatter, fused into the next gather
-      if (hf == 0) {
+        for (int c = 0; c < kC; ++c) col[c] = sigmoid_f(o[1 + c]);
+        // ---- B3: Eq. 3, log-domain reverse update (R12)
+        const float tau_q = (tauR - U) - Ue;
+        two_sum_add(U, Ue, ds);
+        const float tau_qm1 = (tauR - U) - Ue;
+        float aq = 0.0f;
 #pragma unroll
-        for (int pp = 0; pp < S::NPL; ++pp) ptaps[rt * S::NPL + pp] = taps[rt * S::NPL + pp];
-      }
+        for (int c = 0; c < kC; ++c) aq = fmaf(p[c], col[c], aq);
+        aq = fmaf(gdep, (float)ray_t(ray, q), aq);   // depth channel: "colour" t_q, no MLP gradient
+        const float wq = q > 0 ? expf(-tau_qm1) * (-expm1f(-ds)) : 0.0f;
+        const float Tq_aq = q > 0 ? expf(-tau_q) * aq : 0.0f;
+        const float dsig = (float)ray.delta * (gtau - (G_ - Tq_aq));
+        G_ = fmaf(wq, aq, G_);
+        // ---- B4: head VJP
+        float dout[8];
+        dout[0] = dsig * s_sig;
+#pragma unroll
+        for (int c = 0; c < kC; ++c) dout[1 + c] = wq * p[c] * col[c] * (1.0f - col[c]);
+#pragma unroll
+        for (int c = 4; c < 8; ++c) dout[c] = 0.0f;
+        // ---- B5: per 8-unit chunk: stage a1, delta1 = ReLU'(z) (Wo^T dout), stage delta1
+        if (hf == 0) {
+#pragma unroll
+          for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
+          tc::store8<2>(Ht, S::HB_PIECE, rt, S::KP + 8, S::HC, dout);
+        }
+        if (SW > 0 && staged) {   // the DA tile still holds the previous step's staging
+          tc::mbar_wait(bar_dr, dphase);
+          dphase ^= 1;
+        }
+#pragma unroll
+        for (int c = 0; c < HH / 8; ++c) {
+          tc::store8<2>(DAt, S::DA_PIECE, rt, S::HP + hf * HH + 8 * c, 2 * S::HP, a1 + 8 * c);
+          float d1[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 w = reinterpret_cast<const float4*>(fp + F::WOT)[hf * HH + 8 * c + u];
+            float sacc = w.x * dout[0];
+            sacc = fmaf(w.y, dout[1], sacc);
+            sacc = fmaf(w.z, dout[2], sacc);
+            sacc = fmaf(w.w, dout[3], sacc);
+            d1[u] = a1[8 * c + u] > 0.0f ? sacc : 0.0f;
+          }
+          tc::store8<2>(DAt, S::DA_PIECE, rt, hf * HH + 8 * c, 2 * S::HP, d1);
+        }
+        LP_PT(4)
+        tc::fence_async_smem();
+        tc::fence_before_sync();
+        tc::named_bar(1 + g, GT);
+        if (gt == 0) {
+          tc::fence_after_sync();
+          constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
+          // dH = D1 W0   (B = W0 viewed MN-major: MN = channel, K = hidden)
+#pragma unroll
+          for (int ks = 0; ks < HID / 16; ++ks)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              tc::mma_bf16(tDH, tc::desc_kmajor(da_addr + QA[c] * S::DA_PIECE, 2 * S::HP, ks),
+                           tc::desc_mnmajor(w_addr + QB[c] * S::W0_PIECE, S::KP, ks), id_dh, (ks | c) != 0);
+          // [dW0 | db0 | . ; . | dWo^T] += [D1 | A1]^T [H | 1 | DOUT]   (K = the 128 samples of this step)
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              tc::mma_bf16(tW, tc::desc_mnmajor(da_addr + QA[c] * S::DA_PIECE, 2 * S::HP, ks),
+                           tc::desc_mnmajor(h_addr + QB[c] * S::HB_PIECE, S::HC, ks), id_w, wacc);
+              wacc = 1;
+            }
+          tc::mma_commit(bar_d);
+        }
+        tc::mbar_wait(bar_d, phase);
+        phase ^= 1;
+        LP_PT(5)
+        tc::fence_after_sync();
+        // ---- B6: dH row -> fp32 staging -> cooperative scatter
+        {
+          constexpr int HK = S::KP / T;   // this thread's dH columns
+          float dh[HK];
+          tc::tmem_ld<HK>(tDH + tlane + (uint32_t)(hf * HK), dh);
+#pragma unroll
+          for (int k4 = 0; k4 < HK / 4; ++k4)
+            if (hf * HK + 4 * k4 < K)
+              *reinterpret_cast<float4*>(dhs + rt * (K + 4) + hf * HK + 4 * k4) =
+                  make_float4(dh[4 * k4], dh[4 * k4 + 1], dh[4 * k4 + 2], dh[4 * k4 + 3]);
+        }
+        tc::fence_before_sync();
+        // keep this step's tap records for its scatter, fused into the next gather
+        if (hf == 0) {
+#pragma unroll
+          for (int pp = 0; pp < S::NPL; ++pp) ptaps[rt * S::NPL + pp] = taps[rt * S::NPL + pp];
+        }
 #ifndef LP_ABL_NOSCATTER   // ablation hooks (timing experiments only; results are wrong when set)
-      pending = true;
+        pending = true;
 #endif
-      if constexpr (T == 1) __syncwarp();
-      else tc::named_bar(1 + g, GT);   // the other half's warps read these rows
-      LP_PT(6)
+        if constexpr (SW > 0) {
+          tc::mbar_arrive(bar_st);
+          staged = true;
+        } else if constexpr (T == 1) {
+          __syncwarp();
+        } else {
+          tc::named_bar(1 + g, GT);   // the other half's warps read these rows
+        }
+        LP_PT(6)
+      }
     }
-  }
-  if (pending) {   // the last step's scatter
-    __syncwarp();
-    coop_scatter<KIND, K>(gplanes, ptaps, a.dims, dhs, wg * 32, lane, it0, it1);
-    __syncwarp();
-  }
-  LP_PT_FLUSH(1)
+    if (SW == 0 && pending) {   // the last step's scatter
+      __syncwarp();
+      coop_scatter<KIND, K>(gplanes, ptaps, a.dims, dhs, wg * 32, lane, it0, it1);
+      __syncwarp();
+    }
+    LP_PT_FLUSH(1)
 
-  // ---- B7: flush this group's gradient partials (TMEM accumulators + register bias sums)
-  tc::fence_after_sync();
-  const bool had_tiles = (int64_t)blockIdx.x * G + g < ntiles;
-  if (hf == 0) {
-    // M = 128 accumulator: row i lives in TMEM lane i (warp i / 32); rows [0, HP) are
-    // hidden units of D1 (dW0, db0), rows [HP, 2 HP) hidden units of A1 (dWo^T)
-    float wrow[S::HC];
-    tc::tmem_ld<S::HC>(tW + tlane, wrow);
-    const int row = 32 * wg + lane;
-    if (had_tiles && row < HID) {
+    // ---- B7: flush this group's gradient partials (TMEM accumulators + register bias sums)
+    tc::fence_after_sync();
+    const bool had_tiles = (int64_t)blockIdx.x * G + g < ntiles;
+    if (hf == 0) {
+      // M = 128 accumulator: row i lives in TMEM lane i (warp i / 32); rows [0, HP) are
+      // hidden units of D1 (dW0, db0), rows [HP, 2 HP) hidden units of A1 (dWo^T)
+      float wrow[S::HC];
+      tc::tmem_ld<S::HC>(tW + tlane, wrow);
+      const int row = 32 * wg + lane;
+      if (had_tiles && row < HID) {
 #pragma unroll
-      for (int c = 0; c < K; ++c) atomicAdd(a.gparams + P::W0 + row * K + c, wrow[c]);
-      atomicAdd(a.gparams + P::B0 + row, wrow[S::KP]);   // ones column: db0
+        for (int c = 0; c < K; ++c) atomicAdd(a.gparams + P::W0 + row * K + c, wrow[c]);
+        atomicAdd(a.gparams + P::B0 + row, wrow[S::KP]);   // ones column: db0
+      }
+      if (had_tiles && row >= S::HP && row - S::HP < HID) {
+#pragma unroll
+        for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + (row - S::HP), wrow[S::KP + 8 + rr]);
+      }
+#pragma unroll
+      for (int i = 0; i < kOut; ++i) {
+        float s = dbo[i];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        dbo[i] = s;
+      }
+      if (lane == 0 && had_tiles) {
+#pragma unroll
+        for (int i = 0; i < kOut; ++i) atomicAdd(a.gparams + P::BO + i, dbo[i]);
+      }
     }
-    if (had_tiles && row >= S::HP && row - S::HP < HID) {
-#pragma unroll
-      for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + (row - S::HP), wrow[S::KP + 8 + rr]);
-    }
-#pragma unroll
-    for (int i = 0; i < kOut; ++i) {
-      float s = dbo[i];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      dbo[i] = s;
-    }
-    if (lane == 0 && had_tiles) {
-#pragma unroll
-      for (int i = 0; i < kOut; ++i) atomicAdd(a.gparams + P::BO + i, dbo[i]);
-    }
-  }
+  }   // compute warps
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 32) {
