@@ -128,8 +128,8 @@ lp_status run_bwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
   if constexpr (NH == 2 && HID == 64 && K >= 8) {
     if (!force_fma()) {
       static LaunchShape shape;
-      return launch(lp::lp_bwd_tc2_kernel<KIND, K, HID>, shape, lp::Bwd2Smem<KIND, K, HID>::BYTES, 256, 1, a.M, a, w,
-                    s);
+      return launch(lp::lp_bwd_tc2_kernel<KIND, K, HID>, shape, lp::Bwd2Smem<KIND, K, HID>::BYTES,
+                    256 + 32 * lp::kBwd2ScatterWarps, 1, a.M, a, w, s);
     }
   }
   static LaunchShape shape;

@@ -749,8 +749,10 @@ __global__ void __launch_bounds__(128 * T * G + 32 * bwd_scatter_warps<T>(), 1) 
           tc::store8<2>(Ht, S::HB_PIECE, rt, S::KP + 8, S::HC, dout);
         }
         if (SW > 0 && staged) {   // the DA tile still holds the previous step's staging
+          LP_PT(4)
           tc::mbar_wait(bar_dr, dphase);
           dphase ^= 1;
+          LP_PT(7)
         }
 #pragma unroll
         for (int c = 0; c < HH / 8; ++c) {

@@ -25,7 +25,7 @@ lpb.render_backward(field, o, d, n, f, cfg.S, tau, go); e2.record()
 torch.cuda.synchronize(); fn(buf, 0)
 v = np.array(list(buf), dtype=np.float64).reshape(2, 8)
 names = [["taps", "gather", "bar", "mma-issue", "mma-wait", "epilogue", "-", "-"],
-         ["taps", "gather", "bar1", "mma1-wait", "epilogue", "bar2+mma2-wait", "scatter", "-"]]
+         ["taps", "gather", "bar1", "mma1-wait", "epilogue", "bar2+mma2-wait", "scatter", "drained-wait"]]
 for k, nm in enumerate(("fwd", "bwd")):
     tot = v[k].sum()
     print(nm, f"{(e0.elapsed_time(e1) if k == 0 else e1.elapsed_time(e2)):.2f} ms",
