@@ -147,8 +147,8 @@ lp_status run_fwd_vd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s)
 template <int KIND, int K, int HID>
 lp_status run_bwd_vd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
   static LaunchShape shape;
-  return launch(lp::lp_bwd_tcv_kernel<KIND, K, HID>, shape, lp::BwdTcvSmem<KIND, K, HID>::BYTES, 256, 1, a.M, a, w,
-                s);
+  return launch(lp::lp_bwd_tcv_kernel<KIND, K, HID>, shape, lp::BwdTcvSmem<KIND, K, HID>::BYTES,
+                256 + 32 * lp::kBwdvScatterWarps, 1, a.M, a, w, s);
 }
 
 }  // namespace lpi
