@@ -35,6 +35,15 @@ N_SM = 148
 # Measured L2 reduction throughput for full 128-byte fp32 lines (scripts/red_bench.cu,
 # profiles/r1_red_bench.txt): the roofline of the backward's grid-gradient scatter.
 L2_RED_GBS = 6070.0
+# The same per corner-vector size (K x 4 bytes: 128 B for K = 32, 64 B for K = 16, 32 B for
+# K = 8), random granules of an L2-resident 24 MB buffer (scripts/red_bench.cu gran mode,
+# profiles/r1_red_bench_gran.txt): the L2 reduction unit's rate is per granule, so a 64-B
+# corner vector is bound by 76.5 G granules/s = 4.90 TB/s, not by the full-line payload rate.
+L2_RED_GBS_BY_GRAN = {128: 6070.0, 64: 4900.0, 32: 3560.0}
+
+
+def red_peak_gbs(K: int) -> float:
+    return L2_RED_GBS_BY_GRAN.get(4 * K, L2_RED_GBS)
 
 
 def parse():
@@ -399,7 +408,8 @@ def run_ours(args):
     alu_peak = fp32_peak_tflops(sm_max)
     traffic = ncu_traffic(cfg.name)
     tc_bwd_f = tensor_flops_per_sample_bwd(cfg)
-    kname = (("lp_fwd_tc2_kernel (K1tc2)", "lp_bwd_tc2_kernel (K2tc2, backward)") if len(cfg.widths) == 4 else
+    kname = (("lp_fwd_tcv_kernel (K1tcv)", "lp_bwd_tcv_kernel (K2tcv, backward)") if cfg.dir_freqs > 0 else
+             ("lp_fwd_tc2_kernel (K1tc2)", "lp_bwd_tc2_kernel (K2tc2, backward)") if len(cfg.widths) == 4 else
              ("lp_fwd_tc_kernel (K1tc)", "lp_bwd_tc_kernel (K2tc, backward)"))
     line = {
         "metric": "rays/s fwd+bwd", "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
@@ -408,12 +418,13 @@ def run_ours(args):
         "breakdown_ms": {"fwd": t_fwd, "bwd": t_bwd, "allreduce": t_ar},
         "peak_bytes_per_ray": bytes_per_ray,
         "roofline": {"bound": "l2_atomic", "kernel": kname[1],
-                     "achieved": achieved_red, "peak": L2_RED_GBS, "unit": "GB/s",
-                     "frac": achieved_red / L2_RED_GBS,
+                     "achieved": achieved_red, "peak": red_peak_gbs(cfg.K), "unit": "GB/s",
+                     "frac": achieved_red / red_peak_gbs(cfg.K),
                      "traffic": (traffic * M / traffic_rays(cfg.name)) if traffic else None,
                      "algorithmic": f"{red_b} B of fp32 grid-gradient reductions per sample (corners x K x 4)",
-                     "peak_source": "measured: scripts/red_bench.cu full-line red.global.add.v4.f32 into a "
-                                    "24 MB buffer, profiles/r1_red_bench.txt",
+                     "peak_source": f"measured: scripts/red_bench.cu red.global.add.v4.f32 of {4 * cfg.K}-B corner "
+                                    "vectors into an L2-resident 24 MB buffer, profiles/r1_red_bench.txt, "
+                                    "profiles/r1_red_bench_gran.txt",
                      "alu": {"achieved_tflops": bwd_f * samples / (t_bwd / 1000.0) / 1e12,
                              "peak_tflops": alu_peak,
                              "peak_source": f"FP32 FFMA {N_SM} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz "
@@ -589,8 +600,8 @@ def run_splat(args):
                    "l2": "theta + theta_weight (grid-sized, L2-resident for s2, not for s1) re-zeroed every step"},
         "breakdown_ms": {"splat_fwd": t_f, "normalize": t_n, "splat_bwd": t_b},
         "roofline": {"bound": "l2_atomic", "kernel": "lp_splat_mlp_fwd_kernel" if gs is not None else "lp_splat_fwd_kernel",
-                     "achieved": ach, "peak": L2_RED_GBS,
-                     "unit": "GB/s", "frac": ach / L2_RED_GBS, "traffic": None,
+                     "achieved": ach, "peak": red_peak_gbs(cfg.K),
+                     "unit": "GB/s", "frac": ach / red_peak_gbs(cfg.K), "traffic": None,
                      "algorithmic": f"{red_b} B of fp32 reductions per sample (corners x (K + 1) x 4)",
                      "peak_source": "measured: scripts/red_bench.cu, profiles/r1_red_bench.txt"},
         "clocks": clk.summary(), "gpu_launches": (3 if cfg.kind == wl.TRIPLANE else 1) + 2,

@@ -1,6 +1,9 @@
 // red_bench.cu -- throughput of full-line (128 B) gradient scatters into a 24 MB fp32 buffer:
 //   A: 8 lanes x red.global.add.v4.f32 per line (4 lines per warp instruction)
 //   B: stage the line in shared memory, cp.reduce.async.bulk (UBLKRED) per line
+//   gran <bytes> <MB>: A with <bytes>-granules (corner vectors of K = bytes/4 channels,
+//   bytes/16 lanes each) at random granule-aligned offsets of a <MB> buffer -- the
+//   ceilings of the K = 16 voxel grid (c2: 64 B into 128 MB) and of the 2 GiB c5 grid
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
@@ -38,7 +41,46 @@ __global__ void redB(float* g, const int* lines, int nl_per_warp, int nlines_tot
   }
 }
 
+__global__ void redG(float* g, const long long* offs, int n_per_warp, int lanes_per_gran) {
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, per_inst = 32 / lanes_per_gran;
+  const int sub = lane / lanes_per_gran, ch = lane % lanes_per_gran;
+  const long long* L = offs + warp * n_per_warp;
+  for (int i = 0; i < n_per_warp; i += per_inst) {
+    float4 v = make_float4(1.f, 1.f, 1.f, 1.f);
+    atomicAdd(reinterpret_cast<float4*>(g + L[i + sub] + 4 * ch), v);
+  }
+}
+
+static int gran_mode(int gbytes, long long mb) {
+  const long long nfl = mb * 1024 * 1024 / 4, ngran = nfl / (gbytes / 4);
+  const int blocks = 148 * 4, threads = 256, warps = blocks * threads / 32, per = 4096;
+  float* g; long long* offs;
+  if (cudaMalloc(&g, (size_t)nfl * 4) != cudaSuccess) { printf("alloc failed\n"); return 1; }
+  cudaMemset(g, 0, (size_t)nfl * 4);
+  cudaMalloc(&offs, (size_t)warps * per * 8);
+  long long* h = new long long[(size_t)warps * per];
+  unsigned long long s = 88172645463325252ull;
+  for (size_t i = 0; i < (size_t)warps * per; ++i) {
+    s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+    h[i] = (long long)(s % (unsigned long long)ngran) * (gbytes / 4);
+  }
+  cudaMemcpy(offs, h, (size_t)warps * per * 8, cudaMemcpyHostToDevice);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(a);
+    redG<<<blocks, threads>>>(g, offs, per, gbytes / 16);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    const double n = (double)warps * per;
+    printf("gran %3d B into %5lld MB: %.3f ms  %.2f G granules/s  %.2f TB/s payload  (%s)\n", gbytes, mb, ms,
+           n / ms / 1e6, n * gbytes / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 3 && argv[1][0] == 'g') return gran_mode(atoi(argv[2]), atoll(argv[3]));
   // usage: red_bench [n_sm]  -- with n_sm < 148: one 1024-thread block per SM on n_sm SMs
   // (per-SM scaling of the reduction rate); default: 4 x 256-thread blocks per SM on all 148
   const int nlines = 24 * 1024 * 1024 / 128;  // 24 MB buffer
