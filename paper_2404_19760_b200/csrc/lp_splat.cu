@@ -199,19 +199,20 @@ lp_status run_gs(const lp::SplatMlpArgs& a, cudaStream_t s) {
   static cudaError_t err = cudaSuccess;
   auto kernel = FWD ? lp::lp_splat_mlp_fwd_kernel<KIND> : lp::lp_splat_mlp_bwd_kernel<KIND>;
   const size_t smem = FWD ? lp::GsFwdSmem<KIND>::BYTES : lp::GsBwdSmem<KIND>::BYTES;
+  const int threads = FWD ? 256 + 32 * lp::kSplatScatterWarps : 256;
   std::call_once(once, [&] {
     int dev = 0, sms = 0, occ = 0;
     err = cudaGetDevice(&dev);
     if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (err == cudaSuccess) err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, smem);
+    if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
     if (err == cudaSuccess && occ < 1) err = cudaErrorInvalidConfiguration;
     blocks = sms * occ;
   });
   if (err != cudaSuccess) return cuda_check(err, "g_s splat kernel setup");
   const int64_t tiles = (a.s.M + 127) / 128;
   if (tiles == 0) return LP_OK;
-  kernel<<<(int)(tiles < blocks ? tiles : blocks), 256, smem, s>>>(a);
+  kernel<<<(int)(tiles < blocks ? tiles : blocks), threads, smem, s>>>(a);
   return cuda_check(cudaGetLastError(), "g_s splat kernel launch");
 }
 

@@ -97,12 +97,19 @@ struct GsFwdSmem : GsLayout {
   static constexpr uint32_t DHS = A1 + 3 * A1_PIECE;           // fp32 v~ rows [128][K + 4]
   static constexpr uint32_t PTAPS = DHS + 128 * (kGsK + 4) * 4;
   static constexpr uint32_t TAPS = PTAPS + 128 * NPL * 16;     // [2 halves][128][NPL]
-  static constexpr uint32_t BAR = (TAPS + 2 * 128 * NPL * 16 + 127) & ~127u;
-  static constexpr uint32_t BYTES = BAR + 16;
+  static constexpr uint32_t BAR = (TAPS + 2 * 128 * NPL * 16 + 127) & ~127u;   // MMA, tmem slot, staged, drained
+  static constexpr uint32_t BYTES = BAR + 32;
 };
 
+// dedicated warps issue each staged step's splat reductions (v~ and the weight pass),
+// as the renderer backward's scatter warps do (lp_tc_kernels.cuh)
+#ifndef LP_SPLAT_SW
+#define LP_SPLAT_SW 4
+#endif
+constexpr int kSplatScatterWarps = LP_SPLAT_SW;
+
 template <int KIND>
-__global__ void __launch_bounds__(256, 1) lp_splat_mlp_fwd_kernel(const SplatMlpArgs a) {
+__global__ void __launch_bounds__(256 + 32 * kSplatScatterWarps, 1) lp_splat_mlp_fwd_kernel(const SplatMlpArgs a) {
   using L = GsFwdSmem<KIND>;
   constexpr int NPL = L::NPL, KC = kGsKp / 4;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -113,6 +120,10 @@ __global__ void __launch_bounds__(256, 1) lp_splat_mlp_fwd_kernel(const SplatMlp
   const float* fp = reinterpret_cast<const float*>(smem + L::FP);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::BAR);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 8);
+  uint64_t* bar_st = reinterpret_cast<uint64_t*>(smem + L::BAR + 16);   // 256 compute threads
+  uint64_t* bar_dr = reinterpret_cast<uint64_t*>(smem + L::BAR + 24);   // the scatter warps
+  constexpr int SW = kSplatScatterWarps;
+  static_assert(SW == 0 || 4 % SW == 0, "scatter warps");
   const int gt = threadIdx.x, hf = gt >> 7, rt = gt & 127, wq = (gt >> 5) & 3, lane = gt & 31;
   float4* taps = reinterpret_cast<float4*>(smem + L::TAPS) + hf * 128 * NPL;
   const SplatArgs& s = a.s;
@@ -121,110 +132,141 @@ __global__ void __launch_bounds__(256, 1) lp_splat_mlp_fwd_kernel(const SplatMlp
     *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
   __syncthreads();
   stage_gs_weights(smem, a.params, 6 * a.dir_freqs);
-  if (threadIdx.x == 0) tc::mbar_init(bar, 1);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(bar, 1);
+    tc::mbar_init(bar_st, 256);
+    tc::mbar_init(bar_dr, SW > 0 ? SW : 1);
+  }
   if (threadIdx.x < 32) tc::tmem_alloc(tslot, 128);
   tc::fence_async_smem();
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
-  const uint32_t tZ = *tslot, tV = *tslot + 64;
-  const uint32_t tq = (uint32_t)(wq * 32) << 16;
-  const int it0 = hf * (KC / 2), it1 = it0 + KC / 2;
-  const uint32_t a_addr = tc::smem_u32(At), a1_addr = tc::smem_u32(A1t);
-  const uint32_t w0_addr = tc::smem_u32(smem + L::W0P), w1_addr = tc::smem_u32(smem + L::W1P);
-  const uint32_t id_z = tc::idesc_bf16(128, kGsH, 0, 0), id_v = tc::idesc_bf16(128, kGsK, 0, 0);
-  const float* prior[3] = {a.prior[0], a.prior[1], a.prior[2]};
-  float* theta[3] = {s.theta[0], s.theta[1], s.theta[2]};
-  float* weight[3] = {s.weight[0], s.weight[1], s.weight[2]};
-  uint32_t phase = 0;
-  bool pending = false;
-  const int R = s.S - 1;
-  auto to_tensor_core = [&]() {
-    tc::fence_async_smem();
-    tc::fence_before_sync();
-    tc::named_bar(1, 256);
-  };
-  auto mma_done = [&]() {
-    tc::mbar_wait(bar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
-  };
-
-  const int64_t ntiles = (s.M + 127) / 128;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * 128 + rt;
-    const bool valid = r0 < s.M;
-    const int64_t r = valid ? r0 : s.M - 1;
-    const RayIn ray = load_ray(s.orig, s.dir, s.tnear, s.tfar, r, R);
-    if (hf == 0) {   // the pixel feature v_i: columns [0, 32)
-      float v[kGsC];
-#pragma unroll
-      for (int k4 = 0; k4 < kGsC / 4; ++k4) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(s.feat + r * kGsC) + k4);
-        v[4 * k4] = t.x, v[4 * k4 + 1] = t.y, v[4 * k4 + 2] = t.z, v[4 * k4 + 3] = t.w;
-      }
-      store32<3>(At, L::A_PIECE, rt, 0, kGsKA, v);
-    } else {         // direnc(d_i): columns [64, 96)
-      write_direnc(At, L::A_PIECE, rt, kGsC + kGsKp, kGsKA, ray.d, a.dir_freqs);
-    }
-    for (int j = 0; j <= R; ++j) {
-      double x[3];
-      sample_point(ray, j, s.contract, x);
-      write_taps<KIND, kGsKp>(taps + rt * NPL, x, s.dims);
-      if (!valid) {
-#pragma unroll
-        for (int p = 0; p < NPL; ++p) taps[rt * NPL + p].x = __int_as_float(-1);
-      }
-      __syncwarp();
-      // h_prior -> columns [32, 64) (byte offset 4 core-matrix columns), fused with step j-1's splat
-      if (pending)
-        coop_gather<KIND, kGsKp, kGsKA, 3, true>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, theta,
-                                                 ptaps, dhs, it0, it1, weight);
-      else
-        coop_gather<KIND, kGsKp, kGsKA, 3>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, nullptr,
-                                           nullptr, nullptr, it0, it1);
-      pending = false;
-      to_tensor_core();
-      if (gt == 0) {
-        tc::fence_after_sync();
-        mma_split6(tZ, a_addr, L::A_PIECE, kGsKA, w0_addr, L::W0_PIECE, kGsKA, kGsKA / 16, id_z);
-        tc::mma_commit(bar);
-      }
-      mma_done();
-      {   // a1 = relu(z + b0), this half's 32 hidden units
-        float z[32];
-        tc::tmem_ld<32>(tZ + tq + (uint32_t)(hf * 32), z);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) z[i] = fmaxf(z[i] + fp[hf * 32 + i], 0.0f);
-        store32<3>(A1t, L::A1_PIECE, rt, hf * 32, kGsH, z);
-      }
-      to_tensor_core();
-      if (gt == 0) {
-        tc::fence_after_sync();
-        mma_split6(tV, a1_addr, L::A1_PIECE, kGsH, w1_addr, L::W1_PIECE, kGsH, kGsH / 16, id_v);
-        tc::mma_commit(bar);
-      }
-      mma_done();
-      {   // v~ = V~ + b1 (this half's 16 channels) -> fp32 staging
-        float v[16];
-        tc::tmem_ld<16>(tV + tq + (uint32_t)(hf * 16), v);
-#pragma unroll
-        for (int k4 = 0; k4 < 4; ++k4)
-          *reinterpret_cast<float4*>(dhs + rt * (kGsK + 4) + hf * 16 + 4 * k4) =
-              make_float4(v[4 * k4] + fp[kGsH + hf * 16 + 4 * k4], v[4 * k4 + 1] + fp[kGsH + hf * 16 + 4 * k4 + 1],
-                          v[4 * k4 + 2] + fp[kGsH + hf * 16 + 4 * k4 + 2], v[4 * k4 + 3] + fp[kGsH + hf * 16 + 4 * k4 + 3]);
-      }
-      if (hf == 0) {
-#pragma unroll
-        for (int p = 0; p < NPL; ++p) ptaps[rt * NPL + p] = taps[rt * NPL + p];
-      }
-      pending = true;
-      tc::fence_before_sync();
-      tc::named_bar(1, 256);
+  if constexpr (SW > 0) {
+    if (threadIdx.x >= 256) {   // ---- scatter warps: the splat of every staged step
+      const int sw = (threadIdx.x - 256) / 32, sl = threadIdx.x & 31;
+      float* sth[3] = {s.theta[0], s.theta[1], s.theta[2]};
+      float* swt[3] = {s.weight[0], s.weight[1], s.weight[2]};
+      uint32_t ph = 0;
+      const int64_t nt = (s.M + 127) / 128;
+      for (int64_t tile = blockIdx.x; tile < nt; tile += gridDim.x)
+        for (int j = 0; j < s.S; ++j) {
+          tc::mbar_wait(bar_st, ph);
+          ph ^= 1;
+          for (int rb = sw; rb < 4; rb += SW) coop_scatter<KIND, kGsK>(sth, ptaps, s.dims, dhs, rb * 32, sl, 0, kGsK / 4, swt);
+          __syncwarp();
+          if (sl == 0) tc::mbar_arrive(bar_dr);
+        }
     }
   }
-  if (pending) coop_scatter<KIND, kGsK>(theta, ptaps, s.dims, dhs, wq * 32, lane, it0, it1, weight);
+  if (SW == 0 || threadIdx.x < 256) {   // ---- compute warps
+    const uint32_t tZ = *tslot, tV = *tslot + 64;
+    const uint32_t tq = (uint32_t)(wq * 32) << 16;
+    const int it0 = hf * (KC / 2), it1 = it0 + KC / 2;
+    const uint32_t a_addr = tc::smem_u32(At), a1_addr = tc::smem_u32(A1t);
+    const uint32_t w0_addr = tc::smem_u32(smem + L::W0P), w1_addr = tc::smem_u32(smem + L::W1P);
+    const uint32_t id_z = tc::idesc_bf16(128, kGsH, 0, 0), id_v = tc::idesc_bf16(128, kGsK, 0, 0);
+    const float* prior[3] = {a.prior[0], a.prior[1], a.prior[2]};
+    float* theta[3] = {s.theta[0], s.theta[1], s.theta[2]};
+    float* weight[3] = {s.weight[0], s.weight[1], s.weight[2]};
+    uint32_t phase = 0, dphase = 0;
+    bool pending = false, staged = false;
+    const int R = s.S - 1;
+    auto to_tensor_core = [&]() {
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      tc::named_bar(1, 256);
+    };
+    auto mma_done = [&]() {
+      tc::mbar_wait(bar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+    };
+
+    const int64_t ntiles = (s.M + 127) / 128;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t r0 = tile * 128 + ray_slot<kGsKp>(rt);
+      const bool valid = r0 < s.M;
+      const int64_t r = valid ? r0 : s.M - 1;
+      const RayIn ray = load_ray(s.orig, s.dir, s.tnear, s.tfar, r, R);
+      if (hf == 0) {   // the pixel feature v_i: columns [0, 32)
+        float v[kGsC];
+#pragma unroll
+        for (int k4 = 0; k4 < kGsC / 4; ++k4) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(s.feat + r * kGsC) + k4);
+          v[4 * k4] = t.x, v[4 * k4 + 1] = t.y, v[4 * k4 + 2] = t.z, v[4 * k4 + 3] = t.w;
+        }
+        store32<3>(At, L::A_PIECE, rt, 0, kGsKA, v);
+      } else {         // direnc(d_i): columns [64, 96)
+        write_direnc(At, L::A_PIECE, rt, kGsC + kGsKp, kGsKA, ray.d, a.dir_freqs);
+      }
+      for (int j = 0; j <= R; ++j) {
+        double x[3];
+        sample_point(ray, j, s.contract, x);
+        write_taps<KIND, kGsKp>(taps + rt * NPL, x, s.dims);
+        if (!valid) {
+#pragma unroll
+          for (int p = 0; p < NPL; ++p) taps[rt * NPL + p].x = __int_as_float(-1);
+        }
+        __syncwarp();
+        // h_prior -> columns [32, 64) (byte offset 4 core-matrix columns), fused with step j-1's splat
+        if (SW == 0 && pending)
+          coop_gather<KIND, kGsKp, kGsKA, 3, true>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, theta,
+                                                   ptaps, dhs, it0, it1, weight);
+        else
+          coop_gather<KIND, kGsKp, kGsKA, 3>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, nullptr,
+                                             nullptr, nullptr, it0, it1);
+        pending = false;
+        to_tensor_core();
+        if (gt == 0) {
+          tc::fence_after_sync();
+          mma_split6(tZ, a_addr, L::A_PIECE, kGsKA, w0_addr, L::W0_PIECE, kGsKA, kGsKA / 16, id_z);
+          tc::mma_commit(bar);
+        }
+        mma_done();
+        {   // a1 = relu(z + b0), this half's 32 hidden units
+          float z[32];
+          tc::tmem_ld<32>(tZ + tq + (uint32_t)(hf * 32), z);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) z[i] = fmaxf(z[i] + fp[hf * 32 + i], 0.0f);
+          store32<3>(A1t, L::A1_PIECE, rt, hf * 32, kGsH, z);
+        }
+        to_tensor_core();
+        if (gt == 0) {
+          tc::fence_after_sync();
+          mma_split6(tV, a1_addr, L::A1_PIECE, kGsH, w1_addr, L::W1_PIECE, kGsH, kGsH / 16, id_v);
+          tc::mma_commit(bar);
+        }
+        mma_done();
+        if (SW > 0 && staged) {   // dhs / ptaps still hold the previous step's staging
+          tc::mbar_wait(bar_dr, dphase);
+          dphase ^= 1;
+        }
+        {   // v~ = V~ + b1 (this half's 16 channels) -> fp32 staging
+          float v[16];
+          tc::tmem_ld<16>(tV + tq + (uint32_t)(hf * 16), v);
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4)
+            *reinterpret_cast<float4*>(dhs + rt * (kGsK + 4) + hf * 16 + 4 * k4) =
+                make_float4(v[4 * k4] + fp[kGsH + hf * 16 + 4 * k4], v[4 * k4 + 1] + fp[kGsH + hf * 16 + 4 * k4 + 1],
+                            v[4 * k4 + 2] + fp[kGsH + hf * 16 + 4 * k4 + 2], v[4 * k4 + 3] + fp[kGsH + hf * 16 + 4 * k4 + 3]);
+        }
+        if (hf == 0) {
+#pragma unroll
+          for (int p = 0; p < NPL; ++p) ptaps[rt * NPL + p] = taps[rt * NPL + p];
+        }
+        pending = true;
+        if constexpr (SW > 0) {
+          tc::mbar_arrive(bar_st);
+          staged = true;
+        }
+        tc::fence_before_sync();
+        tc::named_bar(1, 256);
+      }
+    }
+    if (SW == 0 && pending) coop_scatter<KIND, kGsK>(theta, ptaps, s.dims, dhs, wq * 32, lane, it0, it1, weight);
+  }   // compute warps
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -351,7 +393,7 @@ __global__ void __launch_bounds__(256, 1) lp_splat_mlp_bwd_kernel(const SplatMlp
 
   const int64_t ntiles = (s.M + 127) / 128;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * 128 + rt;
+    const int64_t r0 = tile * 128 + ray_slot<kGsKp>(rt);
     const bool valid = r0 < s.M;
     const int64_t r = valid ? r0 : s.M - 1;
     const RayIn ray = load_ray(s.orig, s.dir, s.tnear, s.tfar, r, R);

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tc2_kernel(const KernelArgs
 
   const int64_t ntiles = (a.M + 127) / 128;
   for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
-    const int64_t r0 = tile * 128 + rt;
+    const int64_t r0 = tile * 128 + ray_slot<K>(rt);
     const bool valid = r0 < a.M;
     const int64_t r = valid ? r0 : a.M - 1;
     const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
 
     const int64_t ntiles = (a.M + 127) / 128;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int64_t r0 = tile * 128 + rt;
+      const int64_t r0 = tile * 128 + ray_slot<K>(rt);
       const bool valid = r0 < a.M;
       const int64_t r = valid ? r0 : a.M - 1;   // tail rows march a real ray with zero upstream
       const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);

@@ -146,14 +146,27 @@ __device__ __forceinline__ void record_corners(const float4 rec, int p, const Gr
   }
 }
 
-// Row (ray of the 128-ray tile) a lane serves in cooperative iteration `it`. A warp's
-// 32 rays are an 8x4-pixel block in raster order (workload `pixel_of`); with K = 32
-// (4 rays per iteration) an iteration takes a 2x2-pixel quad, whose corner sets
-// overlap most (window scatter below); otherwise consecutive rows.
+// Row (tile slot) a lane serves in cooperative iteration `it`: consecutive slots, so the
+// RPI rows of an iteration fall in distinct rows of a core matrix and its H-tile stores
+// spread over the shared-memory banks.
 template <int RPI>
 __device__ __forceinline__ int coop_row(int row0, int it, int sub) {
-  if constexpr (RPI == 4) return row0 + ((it >> 2) * 2 + (sub >> 1)) * 8 + (it & 3) * 2 + (sub & 1);
-  else return row0 + it * RPI + sub;
+  return row0 + it * RPI + sub;
+}
+
+// Ray of tile slot rt (offset within the 128-ray tile). A warp's 32 rays are an
+// 8x4-pixel block in raster order (workload `pixel_of`); with K = 32 (4 rays per
+// cooperative iteration) slots 4i..4i+3 of the block take its 2x2-pixel quad i, whose
+// corner sets overlap most (L1 reuse within an iteration; window_scatter_plane). The
+// permutation stays inside each 32-ray block, so tail tiles keep their valid rays.
+template <int K>
+__device__ __forceinline__ int ray_slot(int rt) {
+  if constexpr (K == 32) {
+    const int b = rt & ~31, it = (rt & 31) >> 2, s = rt & 3;
+    return b + ((it >> 2) * 2 + (s >> 1)) * 8 + (it & 3) * 2 + (s & 1);
+  } else {
+    return rt;
+  }
 }
 
 #ifndef LP_WINDOW_SCATTER
@@ -433,7 +446,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
 
   const int64_t ntiles = (a.M + 127) / 128;
   for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
-    const int64_t r0 = tile * 128 + gt;
+    const int64_t r0 = tile * 128 + ray_slot<K>(gt);
     const bool valid = r0 < a.M;
     const int64_t r = valid ? r0 : a.M - 1;
     const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
@@ -638,7 +651,7 @@ __global__ void __launch_bounds__(128 * T * G + 32 * bwd_scatter_warps<T>(), 1) 
 
     const int64_t ntiles = (a.M + 127) / 128;
     for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
-      const int64_t r0 = tile * 128 + rt;
+      const int64_t r0 = tile * 128 + ray_slot<K>(rt);
       const bool valid = r0 < a.M;
       const int64_t r = valid ? r0 : a.M - 1;   // tail rows march a real ray with zero upstream
       const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);

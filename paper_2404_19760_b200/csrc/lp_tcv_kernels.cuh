@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tcv_kernel(const KernelArgs
 
   const int64_t ntiles = (a.M + 127) / 128;
   for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < ntiles; tile += (int64_t)gridDim.x * G) {
-    const int64_t r0 = tile * 128 + rt;
+    const int64_t r0 = tile * 128 + ray_slot<K>(rt);
     const bool valid = r0 < a.M;
     const int64_t r = valid ? r0 : a.M - 1;
     const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwdvScatterWarps, 1) lp_bwd_tcv_ke
 
     const int64_t ntiles = (a.M + 127) / 128;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int64_t r0 = tile * 128 + rt;
+      const int64_t r0 = tile * 128 + ray_slot<K>(rt);
       const bool valid = r0 < a.M;
       const int64_t r = valid ? r0 : a.M - 1;
       const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
