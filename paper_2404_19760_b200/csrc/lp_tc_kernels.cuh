@@ -59,10 +59,17 @@ namespace lp {
 constexpr int kGatherUnroll = LP_GATHER_UNROLL;
 
 #ifndef LP_BWD_HPIECES
-#define LP_BWD_HPIECES 3
+#define LP_BWD_HPIECES 2
 #endif
-// bf16 pieces of the backward's H tile (3: the forward's fp32-class Z; 2: 5 products,
-// ~2^-17 relative, frees 12 KB of shared memory per group for L1 -- experiment)
+#ifndef LP_FWD_HPIECES
+#define LP_FWD_HPIECES 2
+#endif
+// bf16 pieces of the sampled feature h in the H tiles of K1tc / K2tc. 2 (default): h
+// carried to 16 significant bits (more than TF32's 11), W0 to 24, 5 products, Z within
+// ~2^-17 relative of fp32; the tiles shrink by 8 KB (fwd) / 12 KB (bwd) per group, which
+// the L1 gets: c4 fwd 133.6 -> 127.1 ms, bwd 379 -> 374 ms, parity unchanged (images
+// and gradients far inside 1e-4 / 1e-3). 3: 6 products, fp32-class (~2^-24).
+constexpr int kFwdHPieces = LP_FWD_HPIECES;
 constexpr int kBwdHPieces = LP_BWD_HPIECES;
 
 template <int KIND, int K, int HID>
@@ -396,8 +403,8 @@ struct FwdTcSmem {
   static constexpr uint32_t W0P = 0;                                   // 3 pieces
   static constexpr uint32_t FP = W0P + 3 * S::W0_PIECE;                // fp32 params
   static constexpr uint32_t GRP = (FP + TcParams<K, HID>::N * 4 + 127) & ~127u;
-  static constexpr uint32_t H = 0;                                     // per group: H (3 pieces), taps
-  static constexpr uint32_t TAPS = H + 3 * S::H_PIECE;
+  static constexpr uint32_t H = 0;                                     // per group: H (kFwdHPieces), taps
+  static constexpr uint32_t TAPS = H + kFwdHPieces * S::H_PIECE;
   static constexpr uint32_t GSIZE = (TAPS + S::TAPS + 127) & ~127u;
   static constexpr uint32_t BAR = GRP + G * GSIZE;                     // G mbarriers + tmem slot
   static constexpr uint32_t BYTES = BAR + 8 * G + 16;
@@ -459,7 +466,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
       write_taps<KIND, K>(taps + gt * S::NPL, x, a.dims);          // F3 (cells)
       __syncwarp();
       LP_PT(0)
-      coop_gather<KIND, K, S::KP, 3>(planes, taps, a.dims, Ht, S::H_PIECE, wg * 32, lane);  // F3 (gather)
+      coop_gather<KIND, K, S::KP, kFwdHPieces>(planes, taps, a.dims, Ht, S::H_PIECE, wg * 32, lane);  // F3 (gather)
       LP_PT(1)
       tc::fence_async_smem();
       tc::fence_before_sync();
@@ -468,11 +475,12 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
       if (gt == 0) {                                               // F4: Z = H W0^T on the tensor core
         tc::fence_after_sync();
         constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
+        constexpr int NPROD = kFwdHPieces == 3 ? 6 : 5;   // products with H piece < kFwdHPieces
         uint32_t acc = 0;
 #pragma unroll
         for (int ks = 0; ks < S::KP / 16; ++ks)
 #pragma unroll
-          for (int c = 0; c < 6; ++c) {
+          for (int c = 0; c < NPROD; ++c) {
             tc::mma_bf16(tmem, tc::desc_kmajor(h_addr + PA[c] * S::H_PIECE, S::KP, ks),
                          tc::desc_kmajor(w_addr + PB[c] * S::W0_PIECE, S::KP, ks), idesc, acc);
             acc = 1;
