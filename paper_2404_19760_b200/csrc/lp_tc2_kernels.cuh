@@ -77,14 +77,23 @@ __device__ __forceinline__ void stage_tc2_weights(uint8_t* w0p, uint8_t* w1p, fl
   if (threadIdx.x < 4) fp[F::BO + threadIdx.x] = g[P::BO + threadIdx.x];
 }
 
-// 6 piece products of a 3-piece x 3-piece K-major contraction (forward-type)
+#ifndef LP_TC2_PIECES
+#define LP_TC2_PIECES 2
+#endif
+// bf16 pieces of the activation operands (h, a1) of the forward-type contractions in
+// K1tc2 / K2tc2; the weights keep 3. 2: 16 significant bits, 5 products (as K1tc/K2tc).
+constexpr int kTc2Pieces = LP_TC2_PIECES;
+
+// piece products of a kTc2Pieces-piece x 3-piece K-major contraction (forward-type):
+// 6 for 3 x 3 (fp32-class), 5 for 2 x 3
 __device__ __forceinline__ void mma_split6(uint32_t d, uint32_t a, uint32_t a_piece, int CA, uint32_t b,
                                            uint32_t b_piece, int CB, int nks, uint32_t idesc) {
   constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
+  constexpr int NPROD = kTc2Pieces == 3 ? 6 : 5;
   uint32_t acc = 0;
   for (int ks = 0; ks < nks; ++ks)
 #pragma unroll
-    for (int c = 0; c < 6; ++c) {
+    for (int c = 0; c < NPROD; ++c) {
       tc::mma_bf16(d, tc::desc_kmajor(a + PA[c] * a_piece, CA, ks), tc::desc_kmajor(b + PB[c] * b_piece, CB, ks),
                    idesc, acc);
       acc = 1;
@@ -96,8 +105,8 @@ template <int KIND, int K, int HID, int G>
 struct Fwd2Smem : Tc2Shape<KIND, K, HID> {
   using T = Tc2Shape<KIND, K, HID>;
   static constexpr uint32_t A_PIECE = 128 * HID * 2;
-  static constexpr uint32_t X = 0;   // H tile (3 x H_PIECE), overlaid by the A1 tile (3 x A_PIECE)
-  static constexpr uint32_t XSZ = 3 * (T::H_PIECE > A_PIECE ? T::H_PIECE : A_PIECE);
+  static constexpr uint32_t X = 0;   // H tile (kTc2Pieces x H_PIECE), overlaid by the A1 tile
+  static constexpr uint32_t XSZ = kTc2Pieces * (T::H_PIECE > A_PIECE ? T::H_PIECE : A_PIECE);
   static constexpr uint32_t TAPS = X + XSZ;            // [2 halves][128][NPL]
   static constexpr uint32_t XO = TAPS + 2 * T::TAPS;   // [2 halves][128] float4 partial outputs
   static constexpr uint32_t GSIZE = (XO + 2 * 128 * 16 + 127) & ~127u;
@@ -166,7 +175,7 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tc2_kernel(const KernelArgs
       sample_point(ray, j, a.contract, x);                                                // F2
       write_taps<KIND, K>(taps + rt * NPL, x, a.dims);                     // F3 (cells)
       __syncwarp();
-      coop_gather<KIND, K, KP, 3>(planes, taps, a.dims, X, L::H_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
+      coop_gather<KIND, K, KP, kTc2Pieces>(planes, taps, a.dims, X, L::H_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
                                   it0, it1);                               // F3 (gather)
       tc::fence_async_smem();
       tc::fence_before_sync();
@@ -187,7 +196,7 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tc2_kernel(const KernelArgs
           float a1[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) a1[u] = fmaxf(z[8 * c + u] + b0[8 * c + u], 0.0f);
-          tc::store8<3>(X, L::A_PIECE, rt, hf * HH + 8 * c, HID, a1);
+          tc::store8<kTc2Pieces>(X, L::A_PIECE, rt, hf * HH + 8 * c, HID, a1);
         }
       }
       tc::fence_before_sync();
@@ -257,7 +266,7 @@ struct Bwd2Smem : Tc2Shape<KIND, K, HID> {
   static constexpr uint32_t A1_PIECE = 128 * T::HC1 * 2;
   static constexpr uint32_t DP = 128 * 2 * HID * 2;
   static constexpr uint32_t H = T::GRP;                          // [128][HC] x 3 (ones column at KP)
-  static constexpr uint32_t A1 = H + 3 * T::HB_PIECE;            // [A1 | 1 | DO] [128][HC1] x 3; piece 2: ptaps
+  static constexpr uint32_t A1 = H + kTc2Pieces * T::HB_PIECE;   // [A1 | 1 | DO] [128][HC1] x 3; piece 2: ptaps
   static constexpr uint32_t D = A1 + 3 * A1_PIECE;               // [D2 | A2] x 2, then D1, then fp32 dH
   static constexpr uint32_t TAPS = D + 2 * DP;                   // [2 halves][128][NPL]
   static constexpr uint32_t XO = TAPS + 2 * T::TAPS;             // [2 halves][128] float4
@@ -406,10 +415,10 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
         write_taps<KIND, K>(taps + rt * NPL, x, a.dims);
         __syncwarp();
         if (SW == 0 && pending)   // warp-uniform
-          coop_gather<KIND, K, HC, 3, true>(planes, taps, a.dims, Ht, L::HB_PIECE, wq * 32, lane, gplanes, ptaps, dhs,
+          coop_gather<KIND, K, HC, kTc2Pieces, true>(planes, taps, a.dims, Ht, L::HB_PIECE, wq * 32, lane, gplanes, ptaps, dhs,
                                             it0, it1);
         else
-          coop_gather<KIND, K, HC, 3>(planes, taps, a.dims, Ht, L::HB_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
+          coop_gather<KIND, K, HC, kTc2Pieces>(planes, taps, a.dims, Ht, L::HB_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
                                       it0, it1);
         pending = false;
         to_tensor_core();
@@ -436,7 +445,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
               mask1 |= (zz > 0.0f ? 1u : 0u) << (8 * c + u);
               a1[u] = fmaxf(zz, 0.0f);
             }
-            tc::store8<3>(A1t, L::A1_PIECE, rt, hf * HH + 8 * c, HC1, a1);
+            tc::store8<kTc2Pieces>(A1t, L::A1_PIECE, rt, hf * HH + 8 * c, HC1, a1);
           }
         }
         to_tensor_core();
