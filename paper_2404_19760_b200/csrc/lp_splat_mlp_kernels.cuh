@@ -93,8 +93,8 @@ struct GsFwdSmem : GsLayout {
   static constexpr uint32_t A_PIECE = 128 * kGsKA * 2;
   static constexpr uint32_t A1_PIECE = 128 * kGsH * 2;
   static constexpr uint32_t A = GRP;
-  static constexpr uint32_t A1 = A + 3 * A_PIECE;
-  static constexpr uint32_t DHS = A1 + 3 * A1_PIECE;           // fp32 v~ rows [128][K + 4]
+  static constexpr uint32_t A1 = A + kTc2Pieces * A_PIECE;      // activation operands: kTc2Pieces bf16 pieces
+  static constexpr uint32_t DHS = A1 + kTc2Pieces * A1_PIECE;           // fp32 v~ rows [128][K + 4]
   static constexpr uint32_t PTAPS = DHS + 128 * (kGsK + 4) * 4;
   static constexpr uint32_t TAPS = PTAPS + 128 * NPL * 16;     // [2 halves][128][NPL]
   static constexpr uint32_t BAR = (TAPS + 2 * 128 * NPL * 16 + 127) & ~127u;   // MMA, tmem slot, staged, drained
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256 + 32 * kSplatScatterWarps, 1) lp_splat_mlp
           const float4 t = __ldg(reinterpret_cast<const float4*>(s.feat + r * kGsC) + k4);
           v[4 * k4] = t.x, v[4 * k4 + 1] = t.y, v[4 * k4 + 2] = t.z, v[4 * k4 + 3] = t.w;
         }
-        store32<3>(At, L::A_PIECE, rt, 0, kGsKA, v);
+        store32<kTc2Pieces>(At, L::A_PIECE, rt, 0, kGsKA, v);
       } else {         // direnc(d_i): columns [64, 96)
         write_direnc(At, L::A_PIECE, rt, kGsC + kGsKp, kGsKA, ray.d, a.dir_freqs);
       }
@@ -212,10 +212,10 @@ __global__ void __launch_bounds__(256 + 32 * kSplatScatterWarps, 1) lp_splat_mlp
         __syncwarp();
         // h_prior -> columns [32, 64) (byte offset 4 core-matrix columns), fused with step j-1's splat
         if (SW == 0 && pending)
-          coop_gather<KIND, kGsKp, kGsKA, 3, true>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, theta,
+          coop_gather<KIND, kGsKp, kGsKA, kTc2Pieces, true>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, theta,
                                                    ptaps, dhs, it0, it1, weight);
         else
-          coop_gather<KIND, kGsKp, kGsKA, 3>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, nullptr,
+          coop_gather<KIND, kGsKp, kGsKA, kTc2Pieces>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, nullptr,
                                              nullptr, nullptr, it0, it1);
         pending = false;
         to_tensor_core();
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256 + 32 * kSplatScatterWarps, 1) lp_splat_mlp
           tc::tmem_ld<32>(tZ + tq + (uint32_t)(hf * 32), z);
 #pragma unroll
           for (int i = 0; i < 32; ++i) z[i] = fmaxf(z[i] + fp[hf * 32 + i], 0.0f);
-          store32<3>(A1t, L::A1_PIECE, rt, hf * 32, kGsH, z);
+          store32<kTc2Pieces>(A1t, L::A1_PIECE, rt, hf * 32, kGsH, z);
         }
         to_tensor_core();
         if (gt == 0) {
@@ -321,7 +321,7 @@ struct GsBwdSmem : GsLayout {
   static constexpr uint32_t A1_PIECE = 128 * A1C * 2;
   static constexpr uint32_t X_PIECE = 128 * 64 * 2;             // DV, then D1, then dh staging
   static constexpr uint32_t A = GRP;
-  static constexpr uint32_t A1 = A + 3 * A_PIECE;
+  static constexpr uint32_t A1 = A + kTc2Pieces * A_PIECE;
   static constexpr uint32_t X = A1 + 2 * A1_PIECE;
   static constexpr uint32_t PTAPS = X + 128 * (kGsKp + 4) * 4;  // inside X, after the fp32 staging
   static constexpr uint32_t TAPS = X + 2 * X_PIECE;
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(256, 1) lp_splat_mlp_bwd_kernel(const SplatMlp
         const float4 t = __ldg(reinterpret_cast<const float4*>(s.feat + r * kGsC) + k4);
         v[4 * k4] = t.x, v[4 * k4 + 1] = t.y, v[4 * k4 + 2] = t.z, v[4 * k4 + 3] = t.w;
       }
-      store32<3>(At, L::A_PIECE, rt, 0, L::AC, v);
+      store32<kTc2Pieces>(At, L::A_PIECE, rt, 0, L::AC, v);
     } else {
       write_direnc(At, L::A_PIECE, rt, kGsC + kGsKp, L::AC, ray.d, a.dir_freqs);
     }
@@ -421,10 +421,10 @@ __global__ void __launch_bounds__(256, 1) lp_splat_mlp_bwd_kernel(const SplatMlp
       }
       __syncwarp();
       if (pending)   // h_prior, fused with the prior-gradient scatter of step q+1
-        coop_gather<KIND, kGsKp, L::AC, 3, true>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, gprior,
+        coop_gather<KIND, kGsKp, L::AC, kTc2Pieces, true>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, gprior,
                                                  ptaps, dhs, it0, it1);
       else
-        coop_gather<KIND, kGsKp, L::AC, 3>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, nullptr,
+        coop_gather<KIND, kGsKp, L::AC, kTc2Pieces>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, nullptr,
                                            nullptr, nullptr, it0, it1);
       pending = false;
       tc::named_bar(1, 256);   // the staging in X has been read by every warp before DV overwrites it

@@ -109,6 +109,13 @@ __device__ __forceinline__ void stage_tcv_weights(uint8_t* wp, float* fp, const 
 
 // direnc(d) of this thread's ray into columns [KP, KP + E) of row `row` of an A tile
 // (3 bf16 pieces): per axis k, per frequency 2^i, (sin(pi 2^i d_k), cos(pi 2^i d_k)).
+#ifndef LP_TCV_PIECES
+#define LP_TCV_PIECES 2
+#endif
+// bf16 pieces of the [h | direnc(d)] operand of Z = [H | E] W'^T (the weights keep 3):
+// 2 = 16 significant bits, 5 products (as K1tc / K2tc)
+constexpr int kTcvPieces = LP_TCV_PIECES;
+
 __device__ __forceinline__ void write_direnc(uint8_t* tile, uint32_t piece, int row, int col0, int C, const float d[3],
                                              int F) {
   float e[kDirEP];
@@ -123,15 +130,15 @@ __device__ __forceinline__ void write_direnc(uint8_t* tile, uint32_t piece, int 
       e[2 * (k * F + i) + 1] = (float)c;
     }
 #pragma unroll
-  for (int c8 = 0; c8 < kDirEP / 8; ++c8) tc::store8<3>(tile, piece, row, col0 + 8 * c8, C, e + 8 * c8);
+  for (int c8 = 0; c8 < kDirEP / 8; ++c8) tc::store8<kTcvPieces>(tile, piece, row, col0 + 8 * c8, C, e + 8 * c8);
 }
 
 // ================================================================= K1tcv forward
 template <int KIND, int K, int HID, int G>
 struct FwdTcvSmem : TcvShape<KIND, K, HID> {
   using T = TcvShape<KIND, K, HID>;
-  static constexpr uint32_t X = 0;                       // [h | e] tile, 3 pieces
-  static constexpr uint32_t TAPS = X + 3 * T::XF_PIECE;  // [2 halves][128][NPL]
+  static constexpr uint32_t X = 0;                       // [h | e] tile, kTcvPieces pieces
+  static constexpr uint32_t TAPS = X + kTcvPieces * T::XF_PIECE;  // [2 halves][128][NPL]
   static constexpr uint32_t XO = TAPS + 2 * T::TAPS;     // [2 halves][128] float4
   static constexpr uint32_t GSIZE = (XO + 2 * 128 * 16 + 127) & ~127u;
   static constexpr uint32_t BAR = T::GRP + G * GSIZE;
@@ -197,7 +204,7 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tcv_kernel(const KernelArgs
       sample_point(ray, j, a.contract, x);                                 // F2
       write_taps<KIND, K>(taps + rt * NPL, x, a.dims);                     // F3 (cells)
       __syncwarp();
-      coop_gather<KIND, K, KV, 3>(planes, taps, a.dims, X, L::XF_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
+      coop_gather<KIND, K, KV, kTcvPieces>(planes, taps, a.dims, X, L::XF_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
                                   it0, it1);                               // F3 (gather)
       tc::fence_async_smem();
       tc::fence_before_sync();
@@ -205,11 +212,12 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tcv_kernel(const KernelArgs
       if (gt == 0) {                                                       // F4: Z = [H | E] W'^T
         tc::fence_after_sync();
         constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
+        constexpr int NPROD = kTcvPieces == 3 ? 6 : 5;
         uint32_t acc = 0;
 #pragma unroll
         for (int ks = 0; ks < KV / 16; ++ks)
 #pragma unroll
-          for (int c = 0; c < 6; ++c) {
+          for (int c = 0; c < NPROD; ++c) {
             tc::mma_bf16(tZ, tc::desc_kmajor(x_addr + PA[c] * L::XF_PIECE, KV, ks),
                          tc::desc_kmajor(w_addr + PB[c] * L::W_PIECE, KV, ks), idesc, acc);
             acc = 1;
@@ -279,7 +287,7 @@ template <int KIND, int K, int HID>
 struct BwdTcvSmem : TcvShape<KIND, K, HID> {
   using T = TcvShape<KIND, K, HID>;
   static constexpr uint32_t H = T::GRP;                      // [h | e | 1 | dout], 3 pieces
-  static constexpr uint32_t D = H + 3 * T::XB_PIECE;         // D' then A', 2 pieces [128][MP]
+  static constexpr uint32_t D = H + kTcvPieces * T::XB_PIECE;  // D' then A', 2 pieces [128][MP]
   static constexpr uint32_t DHS = D + 2 * T::D_PIECE;        // fp32 dH rows [128][K + 4]
   static constexpr uint32_t PTAPS = DHS + 128 * (K + 4) * 4; // previous step's tap records
   static constexpr uint32_t TAPS = PTAPS + T::TAPS;          // [2 halves][128][NPL]
@@ -413,21 +421,22 @@ __global__ void __launch_bounds__(256 + 32 * kBwdvScatterWarps, 1) lp_bwd_tcv_ke
         write_taps<KIND, K>(taps + rt * NPL, x, a.dims);
         __syncwarp();
         if (SW == 0 && pending)
-          coop_gather<KIND, K, HCB, 3, true>(planes, taps, a.dims, Ht, L::XB_PIECE, wq * 32, lane, gplanes, ptaps, dhs,
+          coop_gather<KIND, K, HCB, kTcvPieces, true>(planes, taps, a.dims, Ht, L::XB_PIECE, wq * 32, lane, gplanes, ptaps, dhs,
                                              it0, it1);
         else
-          coop_gather<KIND, K, HCB, 3>(planes, taps, a.dims, Ht, L::XB_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
+          coop_gather<KIND, K, HCB, kTcvPieces>(planes, taps, a.dims, Ht, L::XB_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
                                        it0, it1);
         pending = false;
         to_tensor_core();
         if (gt == 0) {                   // Z = [H | E] W'^T
           tc::fence_after_sync();
           constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
+          constexpr int NPROD = kTcvPieces == 3 ? 6 : 5;
           uint32_t acc = 0;
 #pragma unroll
           for (int ks = 0; ks < KV / 16; ++ks)
 #pragma unroll
-            for (int c = 0; c < 6; ++c) {
+            for (int c = 0; c < NPROD; ++c) {
               tc::mma_bf16(tZ, tc::desc_kmajor(h_addr + PA[c] * L::XB_PIECE, HCB, ks),
                            tc::desc_kmajor(w_addr + PB[c] * L::W_PIECE, KV, ks), id_z, acc);
               acc = 1;
