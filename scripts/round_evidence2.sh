@@ -3,6 +3,9 @@
 # cache-warm traffic (c4), every other config's bench line.
 TAG=${1:-r1f}
 mkdir -p gpurun_out
+# measured parity errors (printed by the tests) for the record
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -s -k "parity_subset or view_dependent or density_regimes" \
+    > gpurun_out/parity_${TAG}.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_${TAG}.json 2> gpurun_out/bench_ref_${TAG}.err
 for C in c4 c4p; do
