@@ -78,10 +78,11 @@ __device__ __forceinline__ void stage_tc2_weights(uint8_t* w0p, uint8_t* w1p, fl
 }
 
 #ifndef LP_TC2_PIECES
-#define LP_TC2_PIECES 2
+#define LP_TC2_PIECES 3
 #endif
 // bf16 pieces of the activation operands (h, a1) of the forward-type contractions in
-// K1tc2 / K2tc2; the weights keep 3. 2: 16 significant bits, 5 products (as K1tc/K2tc).
+// K1tc2 / K2tc2 (the weights keep 3). 3: fp32-class (default); 2: 16 significant bits,
+// 5 products -- c4p +6%, but more ReLU decisions flip against the oracle (experiment).
 constexpr int kTc2Pieces = LP_TC2_PIECES;
 
 // piece products of a kTc2Pieces-piece x 3-piece K-major contraction (forward-type):

@@ -110,10 +110,10 @@ __device__ __forceinline__ void stage_tcv_weights(uint8_t* wp, float* fp, const 
 // direnc(d) of this thread's ray into columns [KP, KP + E) of row `row` of an A tile
 // (3 bf16 pieces): per axis k, per frequency 2^i, (sin(pi 2^i d_k), cos(pi 2^i d_k)).
 #ifndef LP_TCV_PIECES
-#define LP_TCV_PIECES 2
+#define LP_TCV_PIECES 3
 #endif
 // bf16 pieces of the [h | direnc(d)] operand of Z = [H | E] W'^T (the weights keep 3):
-// 2 = 16 significant bits, 5 products (as K1tc / K2tc)
+// 3 = fp32-class (default); 2 = 16 significant bits, 5 products (experiment, c4v +9%)
 constexpr int kTcvPieces = LP_TCV_PIECES;
 
 __device__ __forceinline__ void write_direnc(uint8_t* tile, uint32_t piece, int row, int col0, int C, const float d[3],
