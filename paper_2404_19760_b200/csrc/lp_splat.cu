@@ -199,7 +199,7 @@ lp_status run_gs(const lp::SplatMlpArgs& a, cudaStream_t s) {
   static cudaError_t err = cudaSuccess;
   auto kernel = FWD ? lp::lp_splat_mlp_fwd_kernel<KIND> : lp::lp_splat_mlp_bwd_kernel<KIND>;
   const size_t smem = FWD ? lp::GsFwdSmem<KIND>::BYTES : lp::GsBwdSmem<KIND>::BYTES;
-  const int threads = FWD ? 256 + 32 * lp::kSplatScatterWarps : 256;
+  const int threads = 256 + 32 * (FWD ? lp::kSplatScatterWarps : lp::kSplatBwdScatterWarps);
   std::call_once(once, [&] {
     int dev = 0, sms = 0, occ = 0;
     err = cudaGetDevice(&dev);

@@ -325,14 +325,22 @@ struct GsBwdSmem : GsLayout {
   static constexpr uint32_t X = A1 + 2 * A1_PIECE;
   static constexpr uint32_t PTAPS = X + 128 * (kGsKp + 4) * 4;  // inside X, after the fp32 staging
   static constexpr uint32_t TAPS = X + 2 * X_PIECE;
-  static constexpr uint32_t BAR = (TAPS + 2 * 128 * NPL * 16 + 127) & ~127u;
-  static constexpr uint32_t BYTES = BAR + 16;
+  static constexpr uint32_t BAR = (TAPS + 2 * 128 * NPL * 16 + 127) & ~127u;   // MMA, tmem slot, staged, drained
+  static constexpr uint32_t BYTES = BAR + 32;
   static_assert(128 * (kGsKp + 4) * 4 + 128 * NPL * 16 <= 2 * X_PIECE, "staging fits X");
 };
 
+// scatter warps of the g_s backward (the prior-gradient reductions); the staging lives in
+// X, which the next step's g/theta_weight gather overwrites, so they drain it during the
+// next step's taps and prior gather
+#ifndef LP_SPLAT_BWD_SW
+#define LP_SPLAT_BWD_SW 4
+#endif
+constexpr int kSplatBwdScatterWarps = LP_SPLAT_BWD_SW;
+
 // TMEM: S0 [0,64) Z -> dA1 -> dA; dW1|db1 [64,136) (M = 64, rows < 32 real); dW0|db0 [136,240)
 template <int KIND>
-__global__ void __launch_bounds__(256, 1) lp_splat_mlp_bwd_kernel(const SplatMlpArgs a) {
+__global__ void __launch_bounds__(256 + 32 * kSplatBwdScatterWarps, 1) lp_splat_mlp_bwd_kernel(const SplatMlpArgs a) {
   using L = GsBwdSmem<KIND>;
   constexpr int NPL = L::NPL, KC = kGsKp / 4;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -344,6 +352,10 @@ __global__ void __launch_bounds__(256, 1) lp_splat_mlp_bwd_kernel(const SplatMlp
   const float* fp = reinterpret_cast<const float*>(smem + L::FP);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::BAR);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 8);
+  uint64_t* bar_st = reinterpret_cast<uint64_t*>(smem + L::BAR + 16);   // 256 compute threads
+  uint64_t* bar_dr = reinterpret_cast<uint64_t*>(smem + L::BAR + 24);   // the scatter warps
+  constexpr int SW = kSplatBwdScatterWarps;
+  static_assert(SW == 0 || 4 % SW == 0, "scatter warps");
   const int gt = threadIdx.x, hf = gt >> 7, rt = gt & 127, wq = (gt >> 5) & 3, lane = gt & 31;
   float4* taps = reinterpret_cast<float4*>(smem + L::TAPS) + hf * 128 * NPL;
   const SplatArgs& s = a.s;
@@ -353,203 +365,235 @@ __global__ void __launch_bounds__(256, 1) lp_splat_mlp_bwd_kernel(const SplatMlp
     *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
   __syncthreads();
   stage_gs_weights(smem, a.params, E);
-  if (threadIdx.x == 0) tc::mbar_init(bar, 1);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(bar, 1);
+    tc::mbar_init(bar_st, 256);
+    tc::mbar_init(bar_dr, SW > 0 ? SW : 1);
+  }
   if (threadIdx.x < 32) tc::tmem_alloc(tslot, 256);
-  if (hf == 0) *reinterpret_cast<__nv_bfloat16*>(At + tc::cm_off(rt, kGsKA, L::AC)) = __float2bfloat16_rn(1.0f);
-  else *reinterpret_cast<__nv_bfloat16*>(A1t + tc::cm_off(rt, kGsH, L::A1C)) = __float2bfloat16_rn(1.0f);
+  if (threadIdx.x >= 256) {
+  } else if (hf == 0) {
+    *reinterpret_cast<__nv_bfloat16*>(At + tc::cm_off(rt, kGsKA, L::AC)) = __float2bfloat16_rn(1.0f);
+  } else {
+    *reinterpret_cast<__nv_bfloat16*>(A1t + tc::cm_off(rt, kGsH, L::A1C)) = __float2bfloat16_rn(1.0f);
+  }
   tc::fence_async_smem();
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
-  const uint32_t tS = *tslot, tW1 = *tslot + 64, tW0 = *tslot + 136;
-  const uint32_t tq = (uint32_t)(wq * 32) << 16;
-  const int it0 = hf * (KC / 2), it1 = it0 + KC / 2;
-  const uint32_t a_addr = tc::smem_u32(At), a1_addr = tc::smem_u32(A1t), x_addr = tc::smem_u32(Xt);
-  const uint32_t w0_addr = tc::smem_u32(smem + L::W0P), w1_addr = tc::smem_u32(smem + L::W1P);
-  const uint32_t id_z = tc::idesc_bf16(128, kGsH, 0, 0);
-  const uint32_t id_da1 = tc::idesc_bf16(128, kGsH, 0, 1);
-  const uint32_t id_w1 = tc::idesc_bf16(64, L::A1C, 1, 1);
-  const uint32_t id_da = tc::idesc_bf16(128, kGsC + kGsKp, 0, 1);
-  const uint32_t id_w0 = tc::idesc_bf16(64, L::AC, 1, 1);
-  constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
-  const float* prior[3] = {a.prior[0], a.prior[1], a.prior[2]};
-  float* gprior[3] = {a.gprior[0], a.gprior[1], a.gprior[2]};
-  const float* gout[3] = {s.gout[0], s.gout[1], s.gout[2]};
-  const float* wgt[3] = {s.weight[0], s.weight[1], s.weight[2]};
-  uint32_t phase = 0, wacc1 = 0, wacc0 = 0;
-  bool pending = false;
-  const int R = s.S - 1;
-  auto to_tensor_core = [&]() {
-    tc::fence_async_smem();
-    tc::fence_before_sync();
-    tc::named_bar(1, 256);
-  };
-  auto mma_done = [&]() {
-    tc::mbar_wait(bar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
-  };
-
-  const int64_t ntiles = (s.M + 127) / 128;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * 128 + ray_slot<kGsKp>(rt);
-    const bool valid = r0 < s.M;
-    const int64_t r = valid ? r0 : s.M - 1;
-    const RayIn ray = load_ray(s.orig, s.dir, s.tnear, s.tfar, r, R);
-    if (hf == 0) {
-      float v[kGsC];
-#pragma unroll
-      for (int k4 = 0; k4 < kGsC / 4; ++k4) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(s.feat + r * kGsC) + k4);
-        v[4 * k4] = t.x, v[4 * k4 + 1] = t.y, v[4 * k4 + 2] = t.z, v[4 * k4 + 3] = t.w;
-      }
-      store32<kTc2Pieces>(At, L::A_PIECE, rt, 0, L::AC, v);
-    } else {
-      write_direnc(At, L::A_PIECE, rt, kGsC + kGsKp, L::AC, ray.d, a.dir_freqs);
+  if constexpr (SW > 0) {
+    if (threadIdx.x >= 256) {   // ---- scatter warps: prior-gradient reductions of every staged step
+      const int sw = (threadIdx.x - 256) / 32, sl = threadIdx.x & 31;
+      float* sgp[3] = {a.gprior[0], a.gprior[1], a.gprior[2]};
+      uint32_t ph = 0;
+      const int64_t nt = (s.M + 127) / 128;
+      for (int64_t tile = blockIdx.x; tile < nt; tile += gridDim.x)
+        for (int q = 0; q < s.S; ++q) {
+          tc::mbar_wait(bar_st, ph);
+          ph ^= 1;
+          for (int rb = sw; rb < 4; rb += SW) coop_scatter<KIND, kGsKp>(sgp, ptaps, s.dims, dhs, rb * 32, sl);
+          __syncwarp();
+          if (sl == 0) tc::mbar_arrive(bar_dr);
+        }
     }
-    float gv[kGsC];   // dL/dv_i of this ray (half 0)
-#pragma unroll
-    for (int k = 0; k < kGsC; ++k) gv[k] = 0.0f;
-    for (int q = R; q >= 0; --q) {
-      double x[3];
-      sample_point(ray, q, s.contract, x);
-      write_taps<KIND, kGsKp>(taps + rt * NPL, x, s.dims);
-      if (!valid) {
-#pragma unroll
-        for (int p = 0; p < NPL; ++p) taps[rt * NPL + p].x = __int_as_float(-1);
-      }
-      __syncwarp();
-      if (pending)   // h_prior, fused with the prior-gradient scatter of step q+1
-        coop_gather<KIND, kGsKp, L::AC, kTc2Pieces, true>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, gprior,
-                                                 ptaps, dhs, it0, it1);
-      else
-        coop_gather<KIND, kGsKp, L::AC, kTc2Pieces>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, nullptr,
-                                           nullptr, nullptr, it0, it1);
-      pending = false;
-      tc::named_bar(1, 256);   // the staging in X has been read by every warp before DV overwrites it
-      coop_gather_gnorm<KIND, kGsK>(gout, wgt, taps, s.dims, Xt, L::X_PIECE, 64, wq * 32, lane, it0, it1);
-      to_tensor_core();
-      if (gt == 0) {
-        tc::fence_after_sync();
-        mma_split6(tS, a_addr, L::A_PIECE, L::AC, w0_addr, L::W0_PIECE, kGsKA, kGsKA / 16, id_z);
-        tc::mma_commit(bar);
-      }
-      mma_done();
-      uint32_t mask = 0;
-      {
-        float z[32];
-        tc::tmem_ld<32>(tS + tq + (uint32_t)(hf * 32), z);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float zz = z[i] + fp[hf * 32 + i];
-          mask |= (zz > 0.0f ? 1u : 0u) << i;
-          z[i] = fmaxf(zz, 0.0f);
-        }
-        store32<2>(A1t, L::A1_PIECE, rt, hf * 32, L::A1C, z);
-      }
-      to_tensor_core();
-      if (gt == 0) {
-        tc::fence_after_sync();
-        // dA1 = DV W1   (B = W1 [K][H] viewed MN-major: MN = hidden, K = channels)
-#pragma unroll
-        for (int ks = 0; ks < kGsK / 16; ++ks)
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            tc::mma_bf16(tS, tc::desc_kmajor(x_addr + QA[c] * L::X_PIECE, 64, ks),
-                         tc::desc_mnmajor(w1_addr + QB[c] * L::W1_PIECE, kGsH, ks), id_da1, (ks | c) != 0);
-        // dW1 | db1 += DV^T [A1 | 1]   (M = 64: rows >= 32 unused)
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            tc::mma_bf16(tW1, tc::desc_mnmajor(x_addr + QA[c] * L::X_PIECE, 64, ks),
-                         tc::desc_mnmajor(a1_addr + QB[c] * L::A1_PIECE, L::A1C, ks), id_w1, wacc1);
-            wacc1 = 1;
-          }
-        tc::mma_commit(bar);
-      }
-      mma_done();
-      {   // delta1 = ReLU'(z) dA1 -> D1 (over the consumed DV)
-        float d[32];
-        tc::tmem_ld<32>(tS + tq + (uint32_t)(hf * 32), d);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) d[i] = (mask >> i) & 1u ? d[i] : 0.0f;
-        store32<2>(Xt, L::X_PIECE, rt, hf * 32, 64, d);
-      }
-      to_tensor_core();
-      if (gt == 0) {
-        tc::fence_after_sync();
-        // dA = D1 W0 over the v and prior columns (B = W0 [H][KA] MN-major, N = 64)
-#pragma unroll
-        for (int ks = 0; ks < kGsH / 16; ++ks)
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            tc::mma_bf16(tS, tc::desc_kmajor(x_addr + QA[c] * L::X_PIECE, 64, ks),
-                         tc::desc_mnmajor(w0_addr + QB[c] * L::W0_PIECE, kGsKA, ks), id_da, (ks | c) != 0);
-        // dW0 | db0 += D1^T [A | 1]
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            tc::mma_bf16(tW0, tc::desc_mnmajor(x_addr + QA[c] * L::X_PIECE, 64, ks),
-                         tc::desc_mnmajor(a_addr + QB[c] * L::A_PIECE, L::AC, ks), id_w0, wacc0);
-            wacc0 = 1;
-          }
-        tc::mma_commit(bar);
-      }
-      mma_done();
-      {
-        float d[32];
-        tc::tmem_ld<32>(tS + tq + (uint32_t)(hf * 32), d);
-        if (hf == 0) {        // dL/dv_i += dA[:, 0:32]
-#pragma unroll
-          for (int k = 0; k < kGsC; ++k) gv[k] += d[k];
-        } else {              // prior gradient rows -> fp32 staging (scattered by the next step's gather)
-#pragma unroll
-          for (int k4 = 0; k4 < kGsKp / 4; ++k4)
-            *reinterpret_cast<float4*>(dhs + rt * (kGsKp + 4) + 4 * k4) =
-                make_float4(d[4 * k4], d[4 * k4 + 1], d[4 * k4 + 2], d[4 * k4 + 3]);
-        }
-      }
-      if (hf == 1) {
-#pragma unroll
-        for (int p = 0; p < NPL; ++p) ptaps[rt * NPL + p] = taps[rt * NPL + p];
-      }
-      pending = true;
+  }
+  if (SW == 0 || threadIdx.x < 256) {   // ---- compute warps
+    const uint32_t tS = *tslot, tW1 = *tslot + 64, tW0 = *tslot + 136;
+    const uint32_t tq = (uint32_t)(wq * 32) << 16;
+    const int it0 = hf * (KC / 2), it1 = it0 + KC / 2;
+    const uint32_t a_addr = tc::smem_u32(At), a1_addr = tc::smem_u32(A1t), x_addr = tc::smem_u32(Xt);
+    const uint32_t w0_addr = tc::smem_u32(smem + L::W0P), w1_addr = tc::smem_u32(smem + L::W1P);
+    const uint32_t id_z = tc::idesc_bf16(128, kGsH, 0, 0);
+    const uint32_t id_da1 = tc::idesc_bf16(128, kGsH, 0, 1);
+    const uint32_t id_w1 = tc::idesc_bf16(64, L::A1C, 1, 1);
+    const uint32_t id_da = tc::idesc_bf16(128, kGsC + kGsKp, 0, 1);
+    const uint32_t id_w0 = tc::idesc_bf16(64, L::AC, 1, 1);
+    constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
+    const float* prior[3] = {a.prior[0], a.prior[1], a.prior[2]};
+    float* gprior[3] = {a.gprior[0], a.gprior[1], a.gprior[2]};
+    const float* gout[3] = {s.gout[0], s.gout[1], s.gout[2]};
+    const float* wgt[3] = {s.weight[0], s.weight[1], s.weight[2]};
+    uint32_t phase = 0, wacc1 = 0, wacc0 = 0;
+    bool pending = false;
+    uint32_t dphase = 0;
+    const int R = s.S - 1;
+    auto to_tensor_core = [&]() {
+      tc::fence_async_smem();
       tc::fence_before_sync();
       tc::named_bar(1, 256);
-    }
-    if (hf == 0 && valid) {
-#pragma unroll
-      for (int k4 = 0; k4 < kGsC / 4; ++k4)
-        reinterpret_cast<float4*>(s.gfeat + r * kGsC)[k4] =
-            make_float4(gv[4 * k4], gv[4 * k4 + 1], gv[4 * k4 + 2], gv[4 * k4 + 3]);
-    }
-  }
-  if (pending) coop_scatter<KIND, kGsKp>(gprior, ptaps, s.dims, dhs, wq * 32, lane, it0, it1);
+    };
+    auto mma_done = [&]() {
+      tc::mbar_wait(bar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+    };
 
-  // flush: M = 64 accumulators, row i in TMEM lane (i/16)*32 + i%16
-  tc::fence_after_sync();
-  const bool had_tiles = (int64_t)blockIdx.x < ntiles;
-  const int row = 16 * wq + lane;
-  const int oW1 = kGsH * nin + kGsH;
-  if (hf == 0) {
-    float w[L::AC];
-    tc::tmem_ld<L::AC>(tW0 + tq, w);
-    if (had_tiles && lane < 16) {
-      for (int c = 0; c < nin; ++c) atomicAdd(a.gparams + row * nin + c, w[c]);
-      atomicAdd(a.gparams + kGsH * nin + row, w[kGsKA]);   // ones column: db0
-    }
-  } else {
-    float w[L::A1C];
-    tc::tmem_ld<L::A1C>(tW1 + tq, w);
-    if (had_tiles && lane < 16 && row < kGsK) {
+    const int64_t ntiles = (s.M + 127) / 128;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t r0 = tile * 128 + ray_slot<kGsKp>(rt);
+      const bool valid = r0 < s.M;
+      const int64_t r = valid ? r0 : s.M - 1;
+      const RayIn ray = load_ray(s.orig, s.dir, s.tnear, s.tfar, r, R);
+      if (hf == 0) {
+        float v[kGsC];
 #pragma unroll
-      for (int c = 0; c < kGsH; ++c) atomicAdd(a.gparams + oW1 + row * kGsH + c, w[c]);
-      atomicAdd(a.gparams + oW1 + kGsK * kGsH + row, w[kGsH]);   // ones column: db1
+        for (int k4 = 0; k4 < kGsC / 4; ++k4) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(s.feat + r * kGsC) + k4);
+          v[4 * k4] = t.x, v[4 * k4 + 1] = t.y, v[4 * k4 + 2] = t.z, v[4 * k4 + 3] = t.w;
+        }
+        store32<kTc2Pieces>(At, L::A_PIECE, rt, 0, L::AC, v);
+      } else {
+        write_direnc(At, L::A_PIECE, rt, kGsC + kGsKp, L::AC, ray.d, a.dir_freqs);
+      }
+      float gv[kGsC];   // dL/dv_i of this ray (half 0)
+#pragma unroll
+      for (int k = 0; k < kGsC; ++k) gv[k] = 0.0f;
+      for (int q = R; q >= 0; --q) {
+        double x[3];
+        sample_point(ray, q, s.contract, x);
+        write_taps<KIND, kGsKp>(taps + rt * NPL, x, s.dims);
+        if (!valid) {
+#pragma unroll
+          for (int p = 0; p < NPL; ++p) taps[rt * NPL + p].x = __int_as_float(-1);
+        }
+        __syncwarp();
+        if (SW == 0 && pending)   // h_prior, fused with the prior-gradient scatter of step q+1
+          coop_gather<KIND, kGsKp, L::AC, kTc2Pieces, true>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, gprior,
+                                                   ptaps, dhs, it0, it1);
+        else
+          coop_gather<KIND, kGsKp, L::AC, kTc2Pieces>(prior, taps, s.dims, At + 4 * 128, L::A_PIECE, wq * 32, lane, nullptr,
+                                             nullptr, nullptr, it0, it1);
+        if (SW > 0 && pending) {   // the scatter warps have read the staging in X before DV overwrites it
+          tc::mbar_wait(bar_dr, dphase);
+          dphase ^= 1;
+        }
+        pending = false;
+        tc::named_bar(1, 256);   // the staging in X has been read by every warp before DV overwrites it
+        coop_gather_gnorm<KIND, kGsK>(gout, wgt, taps, s.dims, Xt, L::X_PIECE, 64, wq * 32, lane, it0, it1);
+        to_tensor_core();
+        if (gt == 0) {
+          tc::fence_after_sync();
+          mma_split6(tS, a_addr, L::A_PIECE, L::AC, w0_addr, L::W0_PIECE, kGsKA, kGsKA / 16, id_z);
+          tc::mma_commit(bar);
+        }
+        mma_done();
+        uint32_t mask = 0;
+        {
+          float z[32];
+          tc::tmem_ld<32>(tS + tq + (uint32_t)(hf * 32), z);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float zz = z[i] + fp[hf * 32 + i];
+            mask |= (zz > 0.0f ? 1u : 0u) << i;
+            z[i] = fmaxf(zz, 0.0f);
+          }
+          store32<2>(A1t, L::A1_PIECE, rt, hf * 32, L::A1C, z);
+        }
+        to_tensor_core();
+        if (gt == 0) {
+          tc::fence_after_sync();
+          // dA1 = DV W1   (B = W1 [K][H] viewed MN-major: MN = hidden, K = channels)
+#pragma unroll
+          for (int ks = 0; ks < kGsK / 16; ++ks)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              tc::mma_bf16(tS, tc::desc_kmajor(x_addr + QA[c] * L::X_PIECE, 64, ks),
+                           tc::desc_mnmajor(w1_addr + QB[c] * L::W1_PIECE, kGsH, ks), id_da1, (ks | c) != 0);
+          // dW1 | db1 += DV^T [A1 | 1]   (M = 64: rows >= 32 unused)
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              tc::mma_bf16(tW1, tc::desc_mnmajor(x_addr + QA[c] * L::X_PIECE, 64, ks),
+                           tc::desc_mnmajor(a1_addr + QB[c] * L::A1_PIECE, L::A1C, ks), id_w1, wacc1);
+              wacc1 = 1;
+            }
+          tc::mma_commit(bar);
+        }
+        mma_done();
+        {   // delta1 = ReLU'(z) dA1 -> D1 (over the consumed DV)
+          float d[32];
+          tc::tmem_ld<32>(tS + tq + (uint32_t)(hf * 32), d);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) d[i] = (mask >> i) & 1u ? d[i] : 0.0f;
+          store32<2>(Xt, L::X_PIECE, rt, hf * 32, 64, d);
+        }
+        to_tensor_core();
+        if (gt == 0) {
+          tc::fence_after_sync();
+          // dA = D1 W0 over the v and prior columns (B = W0 [H][KA] MN-major, N = 64)
+#pragma unroll
+          for (int ks = 0; ks < kGsH / 16; ++ks)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              tc::mma_bf16(tS, tc::desc_kmajor(x_addr + QA[c] * L::X_PIECE, 64, ks),
+                           tc::desc_mnmajor(w0_addr + QB[c] * L::W0_PIECE, kGsKA, ks), id_da, (ks | c) != 0);
+          // dW0 | db0 += D1^T [A | 1]
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              tc::mma_bf16(tW0, tc::desc_mnmajor(x_addr + QA[c] * L::X_PIECE, 64, ks),
+                           tc::desc_mnmajor(a_addr + QB[c] * L::A_PIECE, L::AC, ks), id_w0, wacc0);
+              wacc0 = 1;
+            }
+          tc::mma_commit(bar);
+        }
+        mma_done();
+        {
+          float d[32];
+          tc::tmem_ld<32>(tS + tq + (uint32_t)(hf * 32), d);
+          if (hf == 0) {        // dL/dv_i += dA[:, 0:32]
+#pragma unroll
+            for (int k = 0; k < kGsC; ++k) gv[k] += d[k];
+          } else {              // prior gradient rows -> fp32 staging (scattered by the next step's gather)
+#pragma unroll
+            for (int k4 = 0; k4 < kGsKp / 4; ++k4)
+              *reinterpret_cast<float4*>(dhs + rt * (kGsKp + 4) + 4 * k4) =
+                  make_float4(d[4 * k4], d[4 * k4 + 1], d[4 * k4 + 2], d[4 * k4 + 3]);
+          }
+        }
+        if (hf == 1) {
+#pragma unroll
+          for (int p = 0; p < NPL; ++p) ptaps[rt * NPL + p] = taps[rt * NPL + p];
+        }
+        pending = true;
+        if constexpr (SW > 0) tc::mbar_arrive(bar_st);
+        tc::fence_before_sync();
+        tc::named_bar(1, 256);
+      }
+      if (hf == 0 && valid) {
+#pragma unroll
+        for (int k4 = 0; k4 < kGsC / 4; ++k4)
+          reinterpret_cast<float4*>(s.gfeat + r * kGsC)[k4] =
+              make_float4(gv[4 * k4], gv[4 * k4 + 1], gv[4 * k4 + 2], gv[4 * k4 + 3]);
+      }
     }
-  }
+    if (SW == 0 && pending) coop_scatter<KIND, kGsKp>(gprior, ptaps, s.dims, dhs, wq * 32, lane, it0, it1);
+
+    // flush: M = 64 accumulators, row i in TMEM lane (i/16)*32 + i%16
+    tc::fence_after_sync();
+    const bool had_tiles = (int64_t)blockIdx.x < ntiles;
+    const int row = 16 * wq + lane;
+    const int oW1 = kGsH * nin + kGsH;
+    if (hf == 0) {
+      float w[L::AC];
+      tc::tmem_ld<L::AC>(tW0 + tq, w);
+      if (had_tiles && lane < 16) {
+        for (int c = 0; c < nin; ++c) atomicAdd(a.gparams + row * nin + c, w[c]);
+        atomicAdd(a.gparams + kGsH * nin + row, w[kGsKA]);   // ones column: db0
+      }
+    } else {
+      float w[L::A1C];
+      tc::tmem_ld<L::A1C>(tW1 + tq, w);
+      if (had_tiles && lane < 16 && row < kGsK) {
+#pragma unroll
+        for (int c = 0; c < kGsH; ++c) atomicAdd(a.gparams + oW1 + row * kGsH + c, w[c]);
+        atomicAdd(a.gparams + oW1 + kGsK * kGsH + row, w[kGsH]);   // ones column: db1
+      }
+    }
+  }   // compute warps
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 32) {
