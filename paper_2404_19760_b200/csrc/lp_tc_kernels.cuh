@@ -161,6 +161,9 @@ __device__ __forceinline__ int coop_row(int row0, int it, int sub) {
   return row0 + it * RPI + sub;
 }
 
+#ifndef LP_RAY_SLOT16
+#define LP_RAY_SLOT16 1
+#endif
 // Ray of tile slot rt (offset within the 128-ray tile). A warp's 32 rays are an
 // 8x4-pixel block in raster order (workload `pixel_of`); with K = 32 (4 rays per
 // cooperative iteration) slots 4i..4i+3 of the block take its 2x2-pixel quad i, whose
@@ -171,6 +174,9 @@ __device__ __forceinline__ int ray_slot(int rt) {
   if constexpr (K == 32) {
     const int b = rt & ~31, it = (rt & 31) >> 2, s = rt & 3;
     return b + ((it >> 2) * 2 + (s >> 1)) * 8 + (it & 3) * 2 + (s & 1);
+  } else if constexpr (K == 16 && LP_RAY_SLOT16) {   // 8 rays per iteration: 4x2-pixel blocks
+    const int b = rt & ~31, it = (rt & 31) >> 3, s = rt & 7;
+    return b + ((it >> 1) * 2 + (s >> 2)) * 8 + (it & 1) * 4 + (s & 3);
   } else {
     return rt;
   }
