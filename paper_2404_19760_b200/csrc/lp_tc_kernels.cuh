@@ -31,7 +31,7 @@
 #include "lp_tc.cuh"
 
 #ifndef LP_GATHER_UNROLL
-#define LP_GATHER_UNROLL 1
+#define LP_GATHER_UNROLL 2
 #endif
 
 #ifdef LP_PHASES
