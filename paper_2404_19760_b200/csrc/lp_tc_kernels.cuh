@@ -258,7 +258,7 @@ __device__ __forceinline__ bool window_scatter_plane(float* gpl, const float4* p
 // merged per quad where their corners overlap (window_scatter_plane): the L2
 // reductions of step q+1 overlap the corner loads of step q (B6 || F3).
 // Iterations [it0, it1) of the KC = K/4 per warp (two warps may split one row block).
-template <int KIND, int K, int C, int NP, bool SCATTER = false, bool PAIR = true>
+template <int KIND, int K, int C, int NP, bool SCATTER = false, bool PAIR = true, int UNROLL = kGatherUnroll>
 __device__ __forceinline__ void coop_gather(const float* const* planes, const float4* taps, const GridDims& g,
                                             uint8_t* Htile, uint32_t piece_stride, int row0, int lane,
                                             float* const* gplanes = nullptr, const float4* ptaps = nullptr,
@@ -273,7 +273,7 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
   // (PAIR; measured: c4 fwd -1.6%, c4p bwd -1.7%; off for K1tcv/K2tcv, +5% there).
   float pacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
   int prow = 0;
-#pragma unroll kGatherUnroll
+#pragma unroll UNROLL
   for (int it = it0; it < it1; ++it) {
     const int row = coop_row<RPI>(row0, it, sub);
     float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};

@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tcv_kernel(const KernelArgs
       sample_point(ray, j, a.contract, x);                                 // F2
       write_taps<KIND, K>(taps + rt * NPL, x, a.dims);                     // F3 (cells)
       __syncwarp();
-      coop_gather<KIND, K, KV, kTcvPieces, false, false>(planes, taps, a.dims, X, L::XF_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
+      coop_gather<KIND, K, KV, kTcvPieces, false, false, 1>(planes, taps, a.dims, X, L::XF_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
                                   it0, it1);                               // F3 (gather)
       tc::fence_async_smem();
       tc::fence_before_sync();
@@ -421,10 +421,10 @@ __global__ void __launch_bounds__(256 + 32 * kBwdvScatterWarps, 1) lp_bwd_tcv_ke
         write_taps<KIND, K>(taps + rt * NPL, x, a.dims);
         __syncwarp();
         if (SW == 0 && pending)
-          coop_gather<KIND, K, HCB, kTcvPieces, true, false>(planes, taps, a.dims, Ht, L::XB_PIECE, wq * 32, lane, gplanes, ptaps, dhs,
+          coop_gather<KIND, K, HCB, kTcvPieces, true, false, 1>(planes, taps, a.dims, Ht, L::XB_PIECE, wq * 32, lane, gplanes, ptaps, dhs,
                                              it0, it1);
         else
-          coop_gather<KIND, K, HCB, kTcvPieces, false, false>(planes, taps, a.dims, Ht, L::XB_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
+          coop_gather<KIND, K, HCB, kTcvPieces, false, false, 1>(planes, taps, a.dims, Ht, L::XB_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
                                        it0, it1);
         pending = false;
         to_tensor_core();
