@@ -185,6 +185,12 @@ __device__ __forceinline__ int ray_slot(int rt) {
 #ifndef LP_WINDOW_SCATTER
 #define LP_WINDOW_SCATTER 0
 #endif
+#ifndef LP_SCATTER_WINDOW   // the same merge in the scatter warps' coop_scatter (experiment)
+#define LP_SCATTER_WINDOW 0
+#endif
+#ifndef LP_SCATTER_PAIR     // coop_scatter merges the shared corners of horizontal ray pairs
+#define LP_SCATTER_PAIR 0
+#endif
 
 // B6 for one triplane plane and the 4 rays of a cooperative iteration (K = 32),
 // merged over shared corners. If the inside rays' cells span at most 3 x 3 cells,
@@ -364,13 +370,55 @@ __device__ __forceinline__ void coop_scatter(float* const* gplanes, const float4
     const float4 d = *reinterpret_cast<const float4*>(dhs + row * (K + 4) + 4 * ch);
 #pragma unroll
     for (int p = 0; p < NPL; ++p) {
+      if constexpr (KIND == 0 && RPI == 4 && LP_SCATTER_WINDOW) {   // experiment: merge the quad's corners
+        if (!wplanes) {
+          int rows[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) rows[t] = coop_row<RPI>(row0, it, t);
+          const int sa = (p == 0 ? g.W : p == 1 ? g.D : g.H) * K;
+          if (window_scatter_plane<K>(gplanes[p] + 4 * ch, taps, dhs + 4 * ch, rows, p, sub, sa)) continue;
+        }
+      }
       const float4 rec = taps[row * NPL + p];
       if (__float_as_int(rec.x) < 0) continue;
       Corners<KIND, K> c;
       record_corners<KIND, K>(rec, p, g, c);
       float* pl = gplanes[p] + 4 * ch;
+      if constexpr (KIND == 0 && RPI == 4 && LP_SCATTER_PAIR) {
+        if (!wplanes) {   // merge with the horizontal neighbour of the 2x2 quad (slot sub ^ 1)
+          const int prow = coop_row<RPI>(row0, it, sub ^ 1);
+          const float4 d2 = *reinterpret_cast<const float4*>(dhs + prow * (K + 4) + 4 * ch);
+          const float4 rec2 = taps[prow * NPL + p];
+          const int base2 = __float_as_int(rec2.x);
+          const int nb = (p == 0 ? g.W : p == 1 ? g.D : g.H);   // vertices per row of this plane
+          const bool owner = (sub & 1) == 0;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            // vertex offset of this corner from the partner's corner (0, 0): the partner
+            // has it iff dv is one of its corners' 0, 1, nb, nb + 1
+            const int dv = (c.off[cc] - base2) / K;
+            const bool shared = base2 >= 0 && (dv == 0 || dv == 1 || dv == nb || dv == nb + 1);
+            if (shared && !owner) continue;   // the owner lane reduces this line
+            const float w = c.w[cc];
+            float4 v = make_float4(w * d.x, w * d.y, w * d.z, w * d.w);
+            if (shared) {
+              const int a2 = dv >= nb ? 1 : 0, b2 = dv - a2 * nb;
+              const float w2 = (a2 ? rec2.y : 1.0f - rec2.y) * (b2 ? rec2.z : 1.0f - rec2.z);
+              v.x = fmaf(w2, d2.x, v.x);
+              v.y = fmaf(w2, d2.y, v.y);
+              v.z = fmaf(w2, d2.z, v.z);
+              v.w = fmaf(w2, d2.w, v.w);
+            }
+            atomicAdd(reinterpret_cast<float4*>(pl + c.off[cc]), v);
+          }
+          continue;
+        }
+      }
 #pragma unroll
       for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) {
+#ifdef LP_ABL_SKIPRED   // ablation (timing only, wrong results): bit (p * 4 + cc) set = reduction skipped
+        if ((LP_ABL_SKIPRED >> (p * 4 + cc)) & 1) continue;
+#endif
         const float w = c.w[cc];
         atomicAdd(reinterpret_cast<float4*>(pl + c.off[cc]), make_float4(w * d.x, w * d.y, w * d.z, w * d.w));
       }
