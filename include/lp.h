@@ -75,7 +75,8 @@ typedef enum { LP_CONTRACT_NONE = 0, LP_CONTRACT_PER_AXIS = 1, LP_CONTRACT_RADIA
  *             h = trilinear sample.
  * Requirements: H, W, D >= 2; every data[] pointer 16-byte aligned;
  * elements per plane/volume < 2^31. Compiled K values: 8, 16, 32.
- * contraction / contract_scale: see lp_contraction; scale a in (0, 2]
+ * contraction / contract_scale: see lp_contraction; scale a in (0, 2) (SPEC S:
+ *   ContractConfig: contracted points stay strictly inside the cube)
  * (ignored for LP_CONTRACT_NONE). */
 typedef struct {
   int32_t kind;           /* lp_grid_kind */
@@ -143,9 +144,16 @@ lp_status lp_render_backward(const lp_grid* grid, const lp_mlp* mlp, const lp_ra
  * rays_host, bg_host, grad_out_host, grad_tau_host (may be NULL) are HOST
  * pointers (pinned memory recommended); grid, mlp, grad_data and grad_params
  * are device-resident. The call copies the ray batch and upstream gradients to
- * `workspace` (device, >= lp_fwd_bwd_host_workspace_bytes(M, C) bytes),
- * runs forward and backward, copies out/tau back to out_host / tau_host
- * (HOST, [M][C] and [M]) and synchronises `stream` before returning. */
+ * `workspace` (device, 256-byte aligned, >= lp_fwd_bwd_host_workspace_bytes(M, C)
+ * bytes), runs forward and backward, copies out/tau back to out_host / tau_host
+ * (HOST, [M][C] and [M]) and synchronises `stream` before returning.
+ * Pipelined for M >= 4 Mi rays: the forward runs in 4 ray chunks, each
+ * starting when its rays have landed (the upstream gradients copy under the
+ * forward, out/tau copy back under the later chunks and the backward), on
+ * `stream` plus two copy streams the library creates once per device. Every
+ * argument is validated before the first copy; if a copy or launch fails
+ * midway, all three streams are synchronised before the error returns, so no
+ * copy still reads or writes the caller's host buffers. Calls serialise. */
 size_t lp_fwd_bwd_host_workspace_bytes(int64_t n_rays, int32_t C);
 lp_status lp_render_fwd_bwd_host(const lp_grid* grid, const lp_mlp* mlp, const lp_rays* rays_host,
                                  const float* bg_host, const float* grad_out_host, const float* grad_tau_host,

@@ -308,11 +308,23 @@ def render_forward_threaded(field: Field, rays: Rays, bg=None, threads: int = 1,
     return (out, tau) if depth is None else (out, tau, depth)
 
 
+def backward_buffers(field: Field, threads: int):
+    """Per-thread private fp64 gradient buffers ([grid planes], params) for
+    render_backward_threaded(parts=...)."""
+    return [([np.zeros_like(a) for a in field.grid], np.zeros_like(field.params)) for _ in range(threads)]
+
+
 def render_backward_threaded(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, threads: int = 1,
-                             grad_depth=None):
-    """Backward with per-thread private gradient buffers, summed in thread order."""
+                             grad_depth=None, parts=None):
+    """Backward with per-thread private gradient buffers, summed in thread order.
+    With `parts` (backward_buffers(field, threads), caller-owned) the gradients
+    accumulate into those buffers and nothing is summed or returned (timing
+    loops: no per-call allocation of grid-sized buffers)."""
     bounds = np.linspace(0, rays.n, threads + 1).astype(np.int64)
-    parts = [([np.zeros_like(a) for a in field.grid], np.zeros_like(field.params)) for _ in range(threads)]
+    keep = parts is not None
+    if not keep:
+        parts = backward_buffers(field, threads)
+    assert len(parts) == threads
     ts = [threading.Thread(target=render_backward,
                            kwargs=dict(field=field, rays=rays, grad_out=grad_out, grad_tau=grad_tau, bg=bg,
                                        r0=int(bounds[i]), r1=int(bounds[i + 1]), grads=parts[i],
@@ -322,6 +334,8 @@ def render_backward_threaded(field: Field, rays: Rays, grad_out, grad_tau=None, 
         t.start()
     for t in ts:
         t.join()
+    if keep:
+        return None
     gg = [sum(p[0][k] for p in parts) for k in range(len(field.grid))]
     gp = sum(p[1] for p in parts)
     return gg, gp

@@ -67,8 +67,8 @@ lp_status validate(const lp_grid* g, const lp_mlp* m, const lp_rays* r, Inst* in
   if (g->K < 1) return fail(LP_ERR_INVALID_ARG, "K must be >= 1");
   if (g->contraction < LP_CONTRACT_NONE || g->contraction > LP_CONTRACT_RADIAL)
     return fail(LP_ERR_INVALID_ARG, "bad contraction mode %d", g->contraction);
-  if (g->contraction != LP_CONTRACT_NONE && !(g->contract_scale > 0.0f && g->contract_scale <= 2.0f))
-    return fail(LP_ERR_INVALID_ARG, "contract_scale must be in (0, 2] (got %g)", (double)g->contract_scale);
+  if (g->contraction != LP_CONTRACT_NONE && !(g->contract_scale > 0.0f && g->contract_scale < 2.0f))
+    return fail(LP_ERR_INVALID_ARG, "contract_scale must be in (0, 2) (got %g)", (double)g->contract_scale);
   const int nplanes = g->kind == LP_GRID_TRIPLANE ? 3 : 1;
   for (int i = 0; i < nplanes; ++i) {
     if (!g->data[i]) return fail(LP_ERR_INVALID_ARG, "grid data[%d] is null", i);
@@ -180,6 +180,55 @@ lp::KernelArgs make_args(const lp_grid* g, const lp_mlp* m, const lp_rays* r, co
   return a;
 }
 
+lp_status check_grad_buffers(const lp_grid* grid, float* const grad_data[3], const float* grad_params) {
+  if (!grad_data || !grad_params) return fail(LP_ERR_INVALID_ARG, "null gradient buffers");
+  const int nplanes = grid->kind == LP_GRID_TRIPLANE ? 3 : 1;
+  for (int i = 0; i < nplanes; ++i) {
+    if (!grad_data[i]) return fail(LP_ERR_INVALID_ARG, "grad_data[%d] is null", i);
+    if (!aligned16(grad_data[i])) return fail(LP_ERR_MISALIGNED, "grad_data[%d] not 16-byte aligned", i);
+  }
+  return LP_OK;
+}
+
+// Copy streams and events of lp_render_fwd_bwd_host, created once per device
+// (no device memory); calls serialise on one mutex (each call synchronises anyway).
+constexpr int kHostChunks = 4;
+struct HostPipe {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_start, ev_grad, ev_end, ev_in[kHostChunks], ev_fwd[kHostChunks];
+  bool ready = false;
+};
+
+std::mutex& host_entry_mutex() {
+  static std::mutex m;
+  return m;
+}
+
+lp_status host_pipe(HostPipe** out) {   // caller holds host_entry_mutex()
+  static HostPipe pipes[LaunchShape::kMaxDevices];
+  int dev = 0;
+  lp_status st = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  if (st != LP_OK) return st;
+  if (dev < 0 || dev >= LaunchShape::kMaxDevices) return fail(LP_ERR_UNSUPPORTED, "device ordinal %d", dev);
+  HostPipe& p = pipes[dev];
+  if (!p.ready) {
+    const unsigned f = cudaEventDisableTiming;
+    cudaError_t e = cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_start, f);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_grad, f);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_end, f);
+    for (int i = 0; i < kHostChunks && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&p.ev_in[i], f);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_fwd[i], f);
+    }
+    if (e != cudaSuccess) return cuda_check(e, "fwd_bwd_host streams/events");
+    p.ready = true;
+  }
+  *out = &p;
+  return LP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -207,14 +256,10 @@ lp_status lp_render_backward(const lp_grid* grid, const lp_mlp* mlp, const lp_ra
   Inst in;
   lp_status st = validate(grid, mlp, rays, &in);
   if (st != LP_OK) return st;
-  if (!grad_data || !grad_params) return fail(LP_ERR_INVALID_ARG, "null gradient buffers");
-  const int nplanes = grid->kind == LP_GRID_TRIPLANE ? 3 : 1;
-  for (int i = 0; i < nplanes; ++i) {
-    if (!grad_data[i]) return fail(LP_ERR_INVALID_ARG, "grad_data[%d] is null", i);
-    if (!aligned16(grad_data[i])) return fail(LP_ERR_MISALIGNED, "grad_data[%d] not 16-byte aligned", i);
-  }
+  if ((st = check_grad_buffers(grid, grad_data, grad_params)) != LP_OK) return st;
   if (rays->n_rays > 0 && (!tau || !grad_out)) return fail(LP_ERR_INVALID_ARG, "null tau/grad_out");
   lp::KernelArgs a = make_args(grid, mlp, rays, bg);
+  const int nplanes = grid->kind == LP_GRID_TRIPLANE ? 3 : 1;
   for (int i = 0; i < 3; ++i) a.ggrid[i] = i < nplanes ? grad_data[i] : nullptr;
   a.gparams = grad_params;
   a.tau = const_cast<float*>(tau);
@@ -235,14 +280,18 @@ lp_status lp_render_fwd_bwd_host(const lp_grid* grid, const lp_mlp* mlp, const l
                                  const float* bg_host, const float* grad_out_host, const float* grad_tau_host,
                                  float* out_host, float* tau_host, float* const grad_data[3], float* grad_params,
                                  void* workspace, size_t workspace_bytes, void* stream) {
+  // ---- every check before the first enqueue: nothing is copied or launched on error
   Inst in;
   lp_status st = validate(grid, mlp, rays_host, &in);
   if (st != LP_OK) return st;
+  if ((st = check_grad_buffers(grid, grad_data, grad_params)) != LP_OK) return st;
   const int C = mlp->widths[mlp->n_layers] - 1;
   const int64_t M = rays_host->n_rays;
   if (!workspace || workspace_bytes < lp_fwd_bwd_host_workspace_bytes(M, C))
     return fail(LP_ERR_INVALID_ARG, "workspace too small (need %zu bytes)", lp_fwd_bwd_host_workspace_bytes(M, C));
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0) return fail(LP_ERR_MISALIGNED, "workspace not 256-byte aligned");
   if (M > 0 && (!grad_out_host || !out_host || !tau_host)) return fail(LP_ERR_INVALID_ARG, "null host buffers");
+  if (M == 0) return LP_OK;
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   char* w = static_cast<char*>(workspace);
   float* d_o = reinterpret_cast<float*>(w);   w += al(M * 12);
@@ -254,32 +303,77 @@ lp_status lp_render_fwd_bwd_host(const lp_grid* grid, const lp_mlp* mlp, const l
   float* d_tau = reinterpret_cast<float*>(w); w += al(M * 4);
   float* d_gt = reinterpret_cast<float*>(w);  w += al(M * 4);
   float* d_bg = reinterpret_cast<float*>(w);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const auto H2D = cudaMemcpyHostToDevice;
-  lp_status e;
-  if ((e = cuda_check(cudaMemcpyAsync(d_o, rays_host->origins, M * 12, H2D, s), "H2D origins")) != LP_OK) return e;
-  if ((e = cuda_check(cudaMemcpyAsync(d_d, rays_host->dirs, M * 12, H2D, s), "H2D dirs")) != LP_OK) return e;
-  if ((e = cuda_check(cudaMemcpyAsync(d_n, rays_host->t_near, M * 4, H2D, s), "H2D near")) != LP_OK) return e;
-  if ((e = cuda_check(cudaMemcpyAsync(d_f, rays_host->t_far, M * 4, H2D, s), "H2D far")) != LP_OK) return e;
-  if ((e = cuda_check(cudaMemcpyAsync(d_go, grad_out_host, M * C * 4, H2D, s), "H2D grad_out")) != LP_OK) return e;
-  if (grad_tau_host &&
-      (e = cuda_check(cudaMemcpyAsync(d_gt, grad_tau_host, M * 4, H2D, s), "H2D grad_tau")) != LP_OK)
-    return e;
-  if (bg_host && (e = cuda_check(cudaMemcpyAsync(d_bg, bg_host, C * 4, H2D, s), "H2D bg")) != LP_OK) return e;
-  lp_rays dr = *rays_host;
-  dr.origins = d_o;
-  dr.dirs = d_d;
-  dr.t_near = d_n;
-  dr.t_far = d_f;
   const float* dbg = bg_host ? d_bg : nullptr;
-  if ((e = lp_render_forward(grid, mlp, &dr, dbg, d_out, d_tau, nullptr, stream)) != LP_OK) return e;
-  if ((e = lp_render_backward(grid, mlp, &dr, dbg, d_tau, d_go, grad_tau_host ? d_gt : nullptr, nullptr, grad_data,
-                              grad_params, stream)) != LP_OK)
-    return e;
-  const auto D2H = cudaMemcpyDeviceToHost;
-  if ((e = cuda_check(cudaMemcpyAsync(out_host, d_out, M * C * 4, D2H, s), "D2H out")) != LP_OK) return e;
-  if ((e = cuda_check(cudaMemcpyAsync(tau_host, d_tau, M * 4, D2H, s), "D2H tau")) != LP_OK) return e;
-  return cuda_check(cudaStreamSynchronize(s), "stream sync");
+
+  // ---- pipelined over NCH ray chunks on the caller's stream `s` and two copy streams:
+  //   h2d: bg, rays chunk 0..NCH-1 (event each), then grad_out / grad_tau
+  //   s:   forward of chunk i after its rays land; backward over all M after grad_out lands
+  //   d2h: out / tau of chunk i after its forward (overlaps the later chunks and the backward)
+  // Exposed copies: the first rays chunk only. Rays are independent, so the chunked
+  // forward computes exactly what one launch would.
+  std::lock_guard<std::mutex> lock(host_entry_mutex());
+  HostPipe* hp = nullptr;
+  if ((st = host_pipe(&hp)) != LP_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t min_chunk = 1 << 20;   // below ~1M rays one chunk (the kernel tails would dominate)
+  const int NCH = (int)(M >= kHostChunks * min_chunk ? kHostChunks : 1);
+  const int64_t per = ((M + NCH - 1) / NCH + 127) / 128 * 128;   // whole 128-ray tiles per chunk
+  const auto H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
+  cudaError_t ce = cudaSuccess;
+  auto ok = [&](cudaError_t e) { if (ce == cudaSuccess) ce = e; return ce == cudaSuccess; };
+  lp_status kst = LP_OK;
+  ok(cudaEventRecord(hp->ev_start, s));                  // after the caller's earlier work on s
+  ok(cudaStreamWaitEvent(hp->h2d, hp->ev_start, 0));
+  ok(cudaStreamWaitEvent(hp->d2h, hp->ev_start, 0));
+  if (bg_host) ok(cudaMemcpyAsync(d_bg, bg_host, C * 4, H2D, hp->h2d));
+  for (int i = 0; i < NCH && ce == cudaSuccess; ++i) {
+    const int64_t r0 = i * per, n = r0 + per < M ? per : M - r0;
+    if (n <= 0) break;
+    ok(cudaMemcpyAsync(d_o + 3 * r0, rays_host->origins + 3 * r0, n * 12, H2D, hp->h2d));
+    ok(cudaMemcpyAsync(d_d + 3 * r0, rays_host->dirs + 3 * r0, n * 12, H2D, hp->h2d));
+    ok(cudaMemcpyAsync(d_n + r0, rays_host->t_near + r0, n * 4, H2D, hp->h2d));
+    ok(cudaMemcpyAsync(d_f + r0, rays_host->t_far + r0, n * 4, H2D, hp->h2d));
+    ok(cudaEventRecord(hp->ev_in[i], hp->h2d));
+  }
+  ok(cudaMemcpyAsync(d_go, grad_out_host, M * C * 4, H2D, hp->h2d));
+  if (grad_tau_host) ok(cudaMemcpyAsync(d_gt, grad_tau_host, M * 4, H2D, hp->h2d));
+  ok(cudaEventRecord(hp->ev_grad, hp->h2d));
+  for (int i = 0; i < NCH && ce == cudaSuccess && kst == LP_OK; ++i) {
+    const int64_t r0 = i * per, n = r0 + per < M ? per : M - r0;
+    if (n <= 0) break;
+    if (!ok(cudaStreamWaitEvent(s, hp->ev_in[i], 0))) break;
+    lp_rays dr = *rays_host;
+    dr.n_rays = n;
+    dr.origins = d_o + 3 * r0;
+    dr.dirs = d_d + 3 * r0;
+    dr.t_near = d_n + r0;
+    dr.t_far = d_f + r0;
+    if ((kst = lp_render_forward(grid, mlp, &dr, dbg, d_out + C * r0, d_tau + r0, nullptr, stream)) != LP_OK) break;
+    ok(cudaEventRecord(hp->ev_fwd[i], s));
+    ok(cudaStreamWaitEvent(hp->d2h, hp->ev_fwd[i], 0));
+    ok(cudaMemcpyAsync(out_host + C * r0, d_out + C * r0, n * C * 4, D2H, hp->d2h));
+    ok(cudaMemcpyAsync(tau_host + r0, d_tau + r0, n * 4, D2H, hp->d2h));
+  }
+  if (ce == cudaSuccess && kst == LP_OK && ok(cudaStreamWaitEvent(s, hp->ev_grad, 0))) {
+    lp_rays dr = *rays_host;
+    dr.origins = d_o;
+    dr.dirs = d_d;
+    dr.t_near = d_n;
+    dr.t_far = d_f;
+    kst = lp_render_backward(grid, mlp, &dr, dbg, d_tau, d_go, grad_tau_host ? d_gt : nullptr, nullptr, grad_data,
+                             grad_params, stream);
+  }
+  // join the copy streams into s (also on failure: no copy may still be reading caller memory)
+  const cudaError_t e1 = cudaEventRecord(hp->ev_end, hp->d2h);
+  const cudaError_t e2 = e1 == cudaSuccess ? cudaStreamWaitEvent(s, hp->ev_end, 0) : e1;
+  const cudaError_t e3 = cudaStreamSynchronize(hp->h2d);
+  const cudaError_t e4 = cudaStreamSynchronize(hp->d2h);
+  const cudaError_t e5 = cudaStreamSynchronize(s);
+  if (kst != LP_OK) return kst;
+  if (ce != cudaSuccess) return cuda_check(ce, "fwd_bwd_host enqueue");
+  for (cudaError_t e : {e1, e2, e3, e4, e5})
+    if (e != cudaSuccess) return cuda_check(e, "fwd_bwd_host sync");
+  return LP_OK;
 }
 
 lp_status lp_set_l2_persist(float hit_ratio) {

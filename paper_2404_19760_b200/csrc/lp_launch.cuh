@@ -1,48 +1,20 @@
 // lp_launch.cuh -- persistent launch of one kernel instance (included only by
 // the generated per-instance translation units under csrc/inst/).
 #pragma once
-#include <cstdlib>
-#include <mutex>
-
 #include "lp_internal.h"
 #include "lp_tc2_kernels.cuh"
 #include "lp_tcv_kernels.cuh"
 
 namespace lpi {
 
-// Per (kernel, device) persistent grid size = SMs x resident CTAs.
-struct LaunchShape {
-  std::once_flag once;
-  int ctas = 0;
-  cudaError_t err = cudaSuccess;
-};
-
 // Launch a persistent kernel whose CTAs each march `groups` tiles of 128 rays at a time.
 template <typename KernelT>
 lp_status launch(KernelT kernel, LaunchShape& shape, size_t smem, int threads, int groups, int64_t M,
                  const lp::KernelArgs& args, const L2Window& win, cudaStream_t stream) {
-  std::call_once(shape.once, [&] {
-    int dev = 0, sms = 0, occ = 0;
-    shape.err = cudaGetDevice(&dev);
-    if (shape.err == cudaSuccess) shape.err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (shape.err == cudaSuccess)
-      shape.err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (shape.err == cudaSuccess)
-      shape.err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
-    if (shape.err == cudaSuccess && occ < 1) shape.err = cudaErrorInvalidConfiguration;
-    shape.ctas = sms * occ;
-  });
-  if (shape.err != cudaSuccess) return cuda_check(shape.err, "kernel setup");
-  if (M == 0) return LP_OK;
   const int64_t tiles = (M + 127) / 128;
-  const int64_t need = (tiles + groups - 1) / groups;
-  int ctas = shape.ctas;
-  static const int cap = [] {   // LP_MAX_CTAS: cap the persistent grid (experiments only)
-    const char* e = getenv("LP_MAX_CTAS");
-    return e ? atoi(e) : 0;
-  }();
-  if (cap > 0 && cap < ctas) ctas = cap;
-  const int grid = (int)(need < ctas ? need : ctas);
+  int grid = 0;
+  lp_status st = persistent_grid(kernel, shape, smem, threads, (tiles + groups - 1) / groups, grid);
+  if (st != LP_OK || grid == 0) return st;
 
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);

@@ -2,8 +2,6 @@
 // instance dispatch and persistent launches of lp_splat_kernels.cuh.
 #include <cuda_runtime.h>
 
-#include <mutex>
-
 #include "../../include/lp.h"
 #include "lp_internal.h"
 #include "lp_splat_mlp_kernels.cuh"
@@ -11,33 +9,19 @@
 namespace {
 using namespace lpi;
 
-struct Shape {
-  std::once_flag once;
-  int blocks = 0;
-  cudaError_t err = cudaSuccess;
-};
-
 template <typename KernelT>
-lp_status launch_persistent(KernelT kernel, Shape& sh, int threads, int64_t work_blocks, const lp::SplatArgs& a,
+lp_status launch_persistent(KernelT kernel, LaunchShape& sh, int threads, int64_t work_blocks, const lp::SplatArgs& a,
                             cudaStream_t s) {
-  std::call_once(sh.once, [&] {
-    int dev = 0, sms = 0, occ = 0;
-    sh.err = cudaGetDevice(&dev);
-    if (sh.err == cudaSuccess) sh.err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sh.err == cudaSuccess) sh.err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0);
-    if (sh.err == cudaSuccess && occ < 1) sh.err = cudaErrorInvalidConfiguration;
-    sh.blocks = sms * occ;
-  });
-  if (sh.err != cudaSuccess) return cuda_check(sh.err, "splat kernel setup");
-  if (work_blocks <= 0) return LP_OK;
-  const int grid = (int)(work_blocks < sh.blocks ? work_blocks : sh.blocks);
+  int grid = 0;
+  lp_status st = persistent_grid(kernel, sh, 0, threads, work_blocks, grid);
+  if (st != LP_OK || grid == 0) return st;
   kernel<<<grid, threads, 0, s>>>(a);
   return cuda_check(cudaGetLastError(), "splat kernel launch");
 }
 
 template <bool FWD, int KIND, int K>
 lp_status run(const lp::SplatArgs& a, cudaStream_t s) {
-  static Shape sh;
+  static LaunchShape sh;
   constexpr int WARPS = lp::kSplatThreads / 32;
   const int64_t blocks = ((a.M + 31) / 32 + WARPS - 1) / WARPS;
   if constexpr (FWD) return launch_persistent(lp::lp_splat_fwd_kernel<KIND, K>, sh, lp::kSplatThreads, blocks, a, s);
@@ -68,8 +52,8 @@ lp_status validate(const lp_grid* g, const lp_rays* r) {
   if (g->K != 8 && g->K != 16 && g->K != 32) return fail(LP_ERR_UNSUPPORTED, "splat: K must be 8, 16 or 32 (got %d)", g->K);
   if (g->contraction < LP_CONTRACT_NONE || g->contraction > LP_CONTRACT_RADIAL)
     return fail(LP_ERR_INVALID_ARG, "bad contraction mode %d", g->contraction);
-  if (g->contraction != LP_CONTRACT_NONE && !(g->contract_scale > 0.0f && g->contract_scale <= 2.0f))
-    return fail(LP_ERR_INVALID_ARG, "contract_scale must be in (0, 2]");
+  if (g->contraction != LP_CONTRACT_NONE && !(g->contract_scale > 0.0f && g->contract_scale < 2.0f))
+    return fail(LP_ERR_INVALID_ARG, "contract_scale must be in (0, 2)");
   const int np = g->kind == LP_GRID_TRIPLANE ? 3 : 1;
   for (int i = 0; i < np; ++i)
     if (plane_cells(g, i) * g->K >= (1LL << 31)) return fail(LP_ERR_UNSUPPORTED, "grid plane/volume has >= 2^31 elements");
@@ -194,25 +178,14 @@ lp_status validate_gs(const lp_grid* grid, const lp_splat_mlp* gs) {
 
 template <bool FWD, int KIND>
 lp_status run_gs(const lp::SplatMlpArgs& a, cudaStream_t s) {
-  static std::once_flag once;
-  static int blocks = 0;
-  static cudaError_t err = cudaSuccess;
+  static LaunchShape sh;
   auto kernel = FWD ? lp::lp_splat_mlp_fwd_kernel<KIND> : lp::lp_splat_mlp_bwd_kernel<KIND>;
   const size_t smem = FWD ? lp::GsFwdSmem<KIND>::BYTES : lp::GsBwdSmem<KIND>::BYTES;
   const int threads = 256 + 32 * (FWD ? lp::kSplatScatterWarps : lp::kSplatBwdScatterWarps);
-  std::call_once(once, [&] {
-    int dev = 0, sms = 0, occ = 0;
-    err = cudaGetDevice(&dev);
-    if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (err == cudaSuccess) err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
-    if (err == cudaSuccess && occ < 1) err = cudaErrorInvalidConfiguration;
-    blocks = sms * occ;
-  });
-  if (err != cudaSuccess) return cuda_check(err, "g_s splat kernel setup");
-  const int64_t tiles = (a.s.M + 127) / 128;
-  if (tiles == 0) return LP_OK;
-  kernel<<<(int)(tiles < blocks ? tiles : blocks), threads, smem, s>>>(a);
+  int grid = 0;
+  lp_status st = persistent_grid(kernel, sh, smem, threads, (a.s.M + 127) / 128, grid);
+  if (st != LP_OK || grid == 0) return st;
+  kernel<<<grid, threads, smem, s>>>(a);
   return cuda_check(cudaGetLastError(), "g_s splat kernel launch");
 }
 

@@ -100,15 +100,17 @@ __global__ void __launch_bounds__(kSplatThreads) lp_splat_fwd_kernel(const Splat
 }
 
 // out = theta / theta_weight per cell, 0 where theta_weight == 0 (reading R27).
+// May run in place (out == theta): theta and out are not restrict-qualified and
+// theta is read with plain loads; each element is read, then written, by one thread.
 template <int K>
-__global__ void __launch_bounds__(256) lp_splat_normalize_kernel(const float* __restrict__ theta,
+__global__ void __launch_bounds__(256) lp_splat_normalize_kernel(const float* theta,
                                                                  const float* __restrict__ weight,
-                                                                 float* __restrict__ out, int64_t ncells) {
+                                                                 float* out, int64_t ncells) {
   constexpr int KC = K / 4;
   const int64_t n = ncells * KC;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float w = __ldg(weight + i / KC);
-    const float4 t = __ldg(reinterpret_cast<const float4*>(theta) + i);
+    const float4 t = reinterpret_cast<const float4*>(theta)[i];
     const float s = w > 0.0f ? 1.0f / w : 0.0f;
     float4 o = make_float4(t.x * s, t.y * s, t.z * s, t.w * s);
     if (!(w > 0.0f)) o = make_float4(0.f, 0.f, 0.f, 0.f);

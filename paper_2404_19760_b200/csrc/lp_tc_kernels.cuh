@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(128 * T * G + 32 * bwd_scatter_warps<T>(), 1) 
   stage_tc_weights<K, HID, S::KP>(w0p, fp, a.params);
   // per group: Z done, dH/dW done (tcgen05.commit), staged (128 compute threads),
   // drained (the group's scatter warps)
-  if (threadIdx.x < 4 * G) tc::mbar_init(&bars[threadIdx.x], threadIdx.x % 4 == 2 ? 128 : threadIdx.x % 4 == 3 ? SWG : 1);
+  if (threadIdx.x < 4 * G) tc::mbar_init(&bars[threadIdx.x], threadIdx.x % 4 == 2 ? 128 : threadIdx.x % 4 == 3 ? (SWG > 0 ? SWG : 1) : 1);
   if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
   tc::fence_async_smem();
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

@@ -43,8 +43,17 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _same_device(device, **tensors):
+    for name, t in tensors.items():
+        if t is not None and t.device != device:
+            raise ValueError(f"{name} is on {t.device}, expected {device} (one device per call)")
+
+
+def _launch(device, fn, *args):
+    """One ABI call with `device` current, enqueued on that device's current
+    stream (tensors on cuda:N launch on cuda:N, not on the current device)."""
+    with torch.cuda.device(device):
+        _lib.check(fn(*args, ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
 
 
 @dataclass
@@ -124,9 +133,11 @@ def render_forward(field: Field, origins, dirs, near, far, n_samples: int, bg=No
         depth = torch.empty((M,), device=origins.device, dtype=torch.float32)
     if depth is not None:
         _req(depth, "depth", (M,))
+    _same_device(origins.device, dirs=dirs, near=near, far=far, bg=bg, out=out, tau=tau, depth=depth,
+                 params=field.params, **{f"planes{i}": p for i, p in enumerate(field.planes)})
     g, m = field.c_grid(), field.c_mlp()
-    _lib.check(_lib.lib.lp_render_forward(ctypes.byref(g), ctypes.byref(m), ctypes.byref(rays), _ptr(bg),
-                                          _ptr(out), _ptr(tau), _ptr(depth), _stream()))
+    _launch(origins.device, _lib.lib.lp_render_forward, ctypes.byref(g), ctypes.byref(m), ctypes.byref(rays), _ptr(bg),
+            _ptr(out), _ptr(tau), _ptr(depth))
     return (out, tau) if depth is None else (out, tau, depth)
 
 
@@ -150,11 +161,15 @@ def render_backward(field: Field, origins, dirs, near, far, n_samples: int, tau,
     for i, (gp, p) in enumerate(zip(grad_planes, field.planes)):
         _req(gp, f"grad_planes[{i}]", p.shape)
     _req(grad_params, "grad_params", field.params.shape)
+    _same_device(origins.device, dirs=dirs, near=near, far=far, bg=bg, tau=tau, grad_out=grad_out,
+                 grad_tau=grad_tau, grad_depth=grad_depth, params=field.params, grad_params=grad_params,
+                 **{f"planes{i}": p for i, p in enumerate(field.planes)},
+                 **{f"grad_planes{i}": p for i, p in enumerate(grad_planes)})
     g, m = field.c_grid(), field.c_mlp()
     gptr = _lib.ptr_array3([t.data_ptr() for t in grad_planes])
-    _lib.check(_lib.lib.lp_render_backward(ctypes.byref(g), ctypes.byref(m), ctypes.byref(rays), _ptr(bg),
-                                           _ptr(tau), _ptr(grad_out), _ptr(grad_tau), _ptr(grad_depth), gptr,
-                                           _ptr(grad_params), _stream()))
+    _launch(origins.device, _lib.lib.lp_render_backward, ctypes.byref(g), ctypes.byref(m), ctypes.byref(rays), _ptr(bg),
+            _ptr(tau), _ptr(grad_out), _ptr(grad_tau), _ptr(grad_depth), gptr,
+            _ptr(grad_params))
     return grad_planes, grad_params
 
 
@@ -199,10 +214,15 @@ def fwd_bwd_host(field: Field, origins_h, dirs_h, near_h, far_h, n_samples: int,
     """End-to-end step through lp_render_fwd_bwd_host: host (pinned) inputs,
     host outputs, device-resident field and gradients. Synchronises."""
     M = origins_h.shape[0]
-    for name, t in (("origins", origins_h), ("dirs", dirs_h), ("near", near_h), ("far", far_h),
-                    ("grad_out", grad_out_h)):
-        if t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous():
-            raise ValueError(f"{name} must be a contiguous float32 host tensor")
+    C = field.C
+    for name, t, shape in (("origins", origins_h, (M, 3)), ("dirs", dirs_h, (M, 3)), ("near", near_h, (M,)),
+                           ("far", far_h, (M,)), ("grad_out", grad_out_h, (M, C)), ("grad_tau", grad_tau_h, (M,)),
+                           ("bg", bg_h, (C,)), ("out", out_h, (M, C)), ("tau", tau_h, (M,))):
+        if t is None and name in ("grad_tau", "bg", "out", "tau"):
+            continue
+        if not isinstance(t, torch.Tensor) or t.device.type != "cpu" or t.dtype != torch.float32 \
+                or not t.is_contiguous() or tuple(t.shape) != shape:
+            raise ValueError(f"{name} must be a contiguous float32 host tensor of shape {shape}")
     rays = _lib.make_rays(M, origins_h.data_ptr(), dirs_h.data_ptr(), near_h.data_ptr(), far_h.data_ptr(),
                           int(n_samples))
     if out_h is None:
@@ -218,10 +238,10 @@ def fwd_bwd_host(field: Field, origins_h, dirs_h, near_h, far_h, n_samples: int,
         grad_params = torch.zeros_like(field.params)
     g, m = field.c_grid(), field.c_mlp()
     gptr = _lib.ptr_array3([t.data_ptr() for t in grad_planes])
-    _lib.check(_lib.lib.lp_render_fwd_bwd_host(
-        ctypes.byref(g), ctypes.byref(m), ctypes.byref(rays), _ptr(bg_h), _ptr(grad_out_h), _ptr(grad_tau_h),
-        _ptr(out_h), _ptr(tau_h), gptr, _ptr(grad_params), ctypes.c_void_p(workspace.data_ptr()),
-        ctypes.c_size_t(workspace.numel()), _stream()))
+    _launch(field.params.device, _lib.lib.lp_render_fwd_bwd_host,
+            ctypes.byref(g), ctypes.byref(m), ctypes.byref(rays), _ptr(bg_h), _ptr(grad_out_h), _ptr(grad_tau_h),
+            _ptr(out_h), _ptr(tau_h), gptr, _ptr(grad_params), ctypes.c_void_p(workspace.data_ptr()),
+            ctypes.c_size_t(workspace.numel()))
     return out_h, tau_h, grad_planes, grad_params, workspace
 
 

@@ -18,7 +18,7 @@ from typing import List, Optional, Tuple
 import torch
 
 from . import _lib
-from .render import CONTRACT_NONE, TRIPLANE, VOXEL, _c_rays, _ptr, _req, _stream
+from .render import CONTRACT_NONE, TRIPLANE, VOXEL, _c_rays, _ptr, _launch, _req
 
 
 @dataclass
@@ -64,9 +64,8 @@ def splat_forward(grid: SplatGrid, origins, dirs, near, far, n_samples: int, fea
     theta = grid.zeros(origins.device) if theta is None else theta
     weight = grid.zeros(origins.device, 1) if weight is None else weight
     g = grid.c_grid()
-    _lib.check(_lib.lib.lp_splat_forward(ctypes.byref(g), ctypes.byref(rays), _ptr(features),
-                                         _planes(grid, theta, "theta"), _planes(grid, weight, "weight", 1),
-                                         _stream()))
+    _launch(origins.device, _lib.lib.lp_splat_forward, ctypes.byref(g), ctypes.byref(rays), _ptr(features),
+            _planes(grid, theta, "theta"), _planes(grid, weight, "weight", 1))
     return theta, weight
 
 
@@ -74,9 +73,8 @@ def splat_normalize(grid: SplatGrid, theta, weight, out=None):
     """theta / theta_weight per cell (0 where no weight landed)."""
     out = [torch.empty_like(t) for t in theta] if out is None else out
     g = grid.c_grid()
-    _lib.check(_lib.lib.lp_splat_normalize(ctypes.byref(g), _planes(grid, theta, "theta"),
-                                           _planes(grid, weight, "weight", 1), _planes(grid, out, "out"),
-                                           _stream()))
+    _launch(theta[0].device, _lib.lib.lp_splat_normalize, ctypes.byref(g), _planes(grid, theta, "theta"),
+            _planes(grid, weight, "weight", 1), _planes(grid, out, "out"))
     return out
 
 
@@ -89,8 +87,8 @@ def splat_backward(grid: SplatGrid, origins, dirs, near, far, n_samples: int, gr
         else grad_features
     _req(gf, "grad_features", (M, grid.K))
     g = grid.c_grid()
-    _lib.check(_lib.lib.lp_splat_backward(ctypes.byref(g), ctypes.byref(rays), _planes(grid, grad_out, "grad_out"),
-                                          _planes(grid, weight, "weight", 1), _ptr(gf), _stream()))
+    _launch(origins.device, _lib.lib.lp_splat_backward, ctypes.byref(g), ctypes.byref(rays), _planes(grid, grad_out, "grad_out"),
+            _planes(grid, weight, "weight", 1), _ptr(gf))
     return gf
 
 
@@ -156,9 +154,8 @@ def splat_forward_mlp(grid: SplatGrid, origins, dirs, near, far, n_samples: int,
     theta = grid.zeros(origins.device) if theta is None else theta
     weight = grid.zeros(origins.device, 1) if weight is None else weight
     g, m = grid.c_grid(), gs.c_struct(grid)
-    _lib.check(_lib.lib.lp_splat_forward_mlp(ctypes.byref(g), ctypes.byref(rays), _ptr(features), ctypes.byref(m),
-                                             _planes(grid, theta, "theta"), _planes(grid, weight, "weight", 1),
-                                             _stream()))
+    _launch(origins.device, _lib.lib.lp_splat_forward_mlp, ctypes.byref(g), ctypes.byref(rays), _ptr(features), ctypes.byref(m),
+            _planes(grid, theta, "theta"), _planes(grid, weight, "weight", 1))
     return theta, weight
 
 
@@ -174,9 +171,9 @@ def splat_backward_mlp(grid: SplatGrid, origins, dirs, near, far, n_samples: int
     gpa = torch.zeros_like(gs.params) if grad_params is None else grad_params
     Kp = int(gs.prior[0].shape[-1])
     g, m = grid.c_grid(), gs.c_struct(grid)
-    _lib.check(_lib.lib.lp_splat_backward_mlp(ctypes.byref(g), ctypes.byref(rays), _ptr(features), ctypes.byref(m),
-                                              _planes(grid, grad_out, "grad_out"), _planes(grid, weight, "weight", 1),
-                                              _ptr(gf), _planes(grid, gpr, "grad_prior", Kp), _ptr(gpa), _stream()))
+    _launch(origins.device, _lib.lib.lp_splat_backward_mlp, ctypes.byref(g), ctypes.byref(rays), _ptr(features), ctypes.byref(m),
+            _planes(grid, grad_out, "grad_out"), _planes(grid, weight, "weight", 1),
+            _ptr(gf), _planes(grid, gpr, "grad_prior", Kp), _ptr(gpa))
     return gf, gpr, gpa
 
 

@@ -61,10 +61,31 @@ def test_validation_errors(L):
     g, m, r = _args(L)
     g.contraction = 3                              # unknown contraction mode
     assert _fwd(L, g, m, r) == L.LP_ERR_INVALID_ARG
-    g.contraction, g.contract_scale = L.LP_CONTRACT_PER_AXIS, 2.5   # scale a outside (0, 2]
+    g.contraction, g.contract_scale = L.LP_CONTRACT_PER_AXIS, 2.5   # scale a outside (0, 2)
     assert _fwd(L, g, m, r) == L.LP_ERR_INVALID_ARG and "contract_scale" in L.lib.lp_last_error().decode()
 
 
 def test_workspace_size(L):
     n = L.lib.lp_fwd_bwd_host_workspace_bytes(1000, 3)
     assert n >= 1000 * (12 + 12 + 4 + 4 + 12 + 12 + 4 + 4)
+
+
+def test_fwd_bwd_host_validates_before_enqueue(L):
+    """lp_render_fwd_bwd_host rejects null gradient buffers, a short or
+    misaligned workspace and null host buffers host-side (no CUDA call)."""
+    g, m, r = _args(L)
+    p = ctypes.c_void_p(0x2000)
+    need = L.lib.lp_fwd_bwd_host_workspace_bytes(4, 3)
+    ws = ctypes.c_void_p(0x10000)
+    gptr = L.ptr_array3([0x4000, 0x4000, 0x4000])
+    f = L.lib.lp_render_fwd_bwd_host
+    call = lambda gd, gp, w, n, outh: f(ctypes.byref(g), ctypes.byref(m), ctypes.byref(r), None, p, None, outh, p,
+                                       gd, gp, w, ctypes.c_size_t(n), None)
+    assert call(None, p, ws, need, p) == L.LP_ERR_INVALID_ARG
+    assert call(L.ptr_array3([0x4004, 0x4000, 0x4000]), p, ws, need, p) == L.LP_ERR_MISALIGNED
+    assert call(gptr, None, ws, need, p) == L.LP_ERR_INVALID_ARG
+    assert call(gptr, p, ws, need - 1, p) == L.LP_ERR_INVALID_ARG
+    assert call(gptr, p, ctypes.c_void_p(0x10010), need, p) == L.LP_ERR_MISALIGNED
+    assert call(gptr, p, ws, need, None) == L.LP_ERR_INVALID_ARG
+    g.contraction, g.contract_scale = L.LP_CONTRACT_PER_AXIS, 2.0   # a = 2 collapses the background: rejected
+    assert call(gptr, p, ws, need, p) == L.LP_ERR_INVALID_ARG
