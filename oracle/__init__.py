@@ -59,8 +59,6 @@ def lib():
                                               P, P, P, P, i32, P, P, P, P, P, P, P, i32, P, i32, f64, i32]
             L.lpo_trace.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, P, P, f64, f64, i32,
                                     P, P, P, P, P, i32, f64, i32]
-            L.lpo_render_min_preact.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
-                                                P, P, P, P, i32, P, i32, f64, i32]
             L.lpo_render_relu_slack.argtypes = [i32, i32, i32, i32, i32, P, P, P, i32, P, P, i64, i64,
                                                 P, P, P, P, i32, P, P, P, f64, P, P, P, P, P, i32, f64, i32]
             L.lpo_contract.argtypes = [i32, f64, i64, P, P]
@@ -69,17 +67,18 @@ def lib():
             L.lpo_splat_normalize.argtypes = [i64, i32, P, P, P]
             L.lpo_splat_rays_mlp.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, i32, P, P, i32, i32, i64, i64,
                                              P, P, P, P, i32, P, P, P, P, P, P, P, i32, f64]
-            L.lpo_splat_mlp_min_preact.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, i32, P, P, i32, i32, i64,
-                                                   i64, P, P, P, P, i32, P, P, i32, f64]
+            L.lpo_splat_mlp_relu_slack.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, i32, P, P, i32, i32, i64,
+                                                   i64, P, P, P, P, i32, P, P, P, P, P, P, P, f64, P, P, P, P, P,
+                                                   i32, f64]
             L.lpo_splat_rays_mlp_backward.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, i32, P, P, i32, i32,
                                                       i64, i64, P, P, P, P, i32, P, P, P, P, P, P, P, P, P, P, P,
                                                       P, i32, f64]
             L.lpo_splat_rays_backward.argtypes = [i32, i32, i32, i32, i32, i64, i64, P, P, P, P, i32, P, P, P,
                                                   P, P, P, P, i32, f64]
-            for f in (L.lpo_render_relu_slack, L.lpo_render_min_preact, L.lpo_sample, L.lpo_splat, L.lpo_mlp_forward, L.lpo_mlp_backward,
+            for f in (L.lpo_render_relu_slack, L.lpo_sample, L.lpo_splat, L.lpo_mlp_forward, L.lpo_mlp_backward,
                       L.lpo_render_forward, L.lpo_render_backward, L.lpo_trace, L.lpo_contract,
                       L.lpo_splat_rays, L.lpo_splat_normalize, L.lpo_splat_rays_backward,
-                      L.lpo_splat_rays_mlp, L.lpo_splat_rays_mlp_backward, L.lpo_splat_mlp_min_preact):
+                      L.lpo_splat_rays_mlp, L.lpo_splat_rays_mlp_backward, L.lpo_splat_mlp_relu_slack):
                 f.restype = ctypes.c_int
             _lib = L
     return _lib
@@ -229,16 +228,6 @@ def render_backward(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, 
                                    *field._scene())
     assert rc == 0
     return gg, gpar
-
-
-def min_preact(field: Field, rays: Rays) -> np.ndarray:
-    """Per ray: min over samples / hidden units of |z| / (sum |W a| + |b|) (see lp_oracle.cpp)."""
-    out = np.zeros(rays.n)
-    rc = lib().lpo_render_min_preact(*field._geom(), *field._planes(), field.n_layers, _p(field.widths),
-                                     _p(field.params), 0, rays.n, _p(rays.o), _p(rays.d), _p(rays.near),
-                                     _p(rays.far), rays.S, _p(out), *field._scene())
-    assert rc == 0
-    return out
 
 
 def relu_slack(field: Field, rays: Rays, grad_out, grad_tau=None, bg=None, band: float = 2e-5,
@@ -473,12 +462,21 @@ def splat_backward_mlp(spec: GridSpec, rays: Rays, features, g: SplatMlp, grad_o
     return gv, gpr, gpar
 
 
-def splat_mlp_min_preact(spec: GridSpec, rays: Rays, features, g: SplatMlp) -> np.ndarray:
-    """Per ray: min |z| / scale over g_s's hidden units (lp_oracle.cpp)."""
+def splat_mlp_relu_slack(spec: GridSpec, rays: Rays, features, g: SplatMlp, grad_out, theta_weight,
+                         band: float = 2e-5):
+    """Elementwise bound of how much the g_s Splatter's gradients (features,
+    prior, params) may change when a g_s ReLU decision with |z| < band * scale
+    flips (lp_oracle.cpp lpo_splat_mlp_relu_slack). Returns (slack_features,
+    slack_prior planes, slack_params)."""
     v = _d(features).reshape(rays.n, g.C_in)
-    out = np.zeros(rays.n)
-    rc = lib().lpo_splat_mlp_min_preact(*spec._geom(), *g._args(), 0, rays.n, _p(rays.o), _p(rays.d),
-                                        _p(rays.near), _p(rays.far), rays.S, _p(v), _p(out), spec.contraction,
+    sv = np.zeros((rays.n, g.C_in))
+    spr = [np.zeros_like(a) for a in g.prior]
+    spar = np.zeros_like(g.params)
+    go = [_d(a) for a in grad_out]
+    w = [_d(a) for a in theta_weight]
+    rc = lib().lpo_splat_mlp_relu_slack(*spec._geom(), *g._args(), 0, rays.n, _p(rays.o), _p(rays.d),
+                                        _p(rays.near), _p(rays.far), rays.S, _p(v), *_ptr3(go), *_ptr3(w),
+                                        float(band), _p(sv), *_ptr3(spr), _p(spar), spec.contraction,
                                         spec.contract_a)
     assert rc == 0
-    return out
+    return sv, spr, spar

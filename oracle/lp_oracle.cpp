@@ -869,20 +869,31 @@ int lpo_splat_rays_mlp_backward(int kind, int H, int W, int D, int K, int Kp, co
   return 0;
 }
 
-// Per ray: min over in-cube samples and hidden units of g_s of |z| / (sum_k |W_ik u_k| + |b_i|)
-// (the ReLU-decision conditioning used by the GPU parity tests to leave out rays whose
-// ReLU'(z) is decided within rounding).
-int lpo_splat_mlp_min_preact(int kind, int H, int W, int D, int K, int Kp, const double* q0, const double* q1,
+// Slack bound for ambiguous ReLU decisions of g_s (the parity metric's
+// allowance, as lpo_render_relu_slack for the renderer; DESIGN.md "Parity
+// metric"): for every in-cube sample and g_s hidden unit with |z| < band *
+// (sum_k |W_ik u_k| + |b_i|), mlp_slack bounds the change of the g_s parameter
+// gradient and of dL/du when the decision flips; the u-part splits into the
+// feature slack of the ray (first C_in entries, accumulated over its samples)
+// and the prior slack (next K_p entries, pushed with the prior's sampling
+// weights, which are >= 0). Accumulates (+=) into slack_features[M][C_in],
+// slack_prior planes and slack_params.
+int lpo_splat_mlp_relu_slack(int kind, int H, int W, int D, int K, int Kp, const double* q0, const double* q1,
                              const double* q2, int n_layers, const int* widths, const double* params, int C_in,
                              int F_dir, int64_t r0, int64_t r1, const double* origins, const double* dirs,
-                             const double* nearv, const double* farv, int S, const double* features, double* min_rel,
-                             int contraction, double contract_a) {
+                             const double* nearv, const double* farv, int S, const double* features,
+                             const double* g0, const double* g1, const double* g2, const double* w0,
+                             const double* w1, const double* w2, double band, double* slack_features, double* sp0,
+                             double* sp1, double* sp2, double* slack_params, int contraction, double contract_a) {
   if (widths[0] != C_in + Kp + 6 * F_dir || widths[n_layers] != K || S < 2) return 1;
   SplatMlp m = make_splat_mlp(kind, H, W, D, K, Kp, q0, q1, q2, n_layers, widths, params, C_in, F_dir, contraction,
                               contract_a);
+  const double* gg[3] = {g0, g1, g2};
+  const double* wg[3] = {w0, w1, w2};
+  double* spr[3] = {sp0, sp1, sp2};
   const int R = S - 1;
   std::vector<Tap> taps, ptaps;
-  std::vector<double> u, e(6 * F_dir);
+  std::vector<double> u, e(6 * F_dir), dv(K), du_slack(widths[0]);
   MlpTrace tr;
   for (int64_t r = r0; r < r1; ++r) {
     const double* o = origins + 3 * r;
@@ -890,29 +901,25 @@ int lpo_splat_mlp_min_preact(int kind, int H, int W, int D, int K, int Kp, const
     direnc(d, F_dir, e.data());
     double span = farv[r] - nearv[r];
     double delta = (span > 0.0 ? span : 0.0) / (double)R;
-    double best = INFINITY;
     for (int j = 0; j < S; ++j) {
       double t = nearv[r] + (double)j * delta;
       double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
       contract(m.F, x);
       sample_taps(m.F, x, taps);
       if (taps.empty()) continue;
+      for (int k = 0; k < K; ++k) dv[k] = 0.0;
+      for (const Tap& tp : taps) {
+        double wc = wg[tp.plane][tp.cell];
+        if (!(wc > 0.0)) continue;
+        const double* g = gg[tp.plane] + tp.cell * K;
+        for (int k = 0; k < K; ++k) dv[k] += tp.w * (g[k] / wc);
+      }
       splat_mlp_input(m, features + r * C_in, x, e.data(), ptaps, u);
       mlp_forward(m.Fm, u.data(), tr);
-      const double* p = params;
-      for (int l = 0; l < n_layers - 1; ++l) {
-        int fin = widths[l], fout = widths[l + 1];
-        const double* Wl = p;
-        const double* bl = p + (int64_t)fout * fin;
-        p = bl + fout;
-        for (int i = 0; i < fout; ++i) {
-          double sc = std::fabs(bl[i]);
-          for (int k = 0; k < fin; ++k) sc += std::fabs(Wl[(int64_t)i * fin + k] * tr.a[l][k]);
-          if (sc > 0.0 && std::fabs(tr.z[l][i]) / sc < best) best = std::fabs(tr.z[l][i]) / sc;
-        }
-      }
+      mlp_slack(m.Fm, tr, dv.data(), band, slack_params, du_slack.data());
+      for (int k = 0; k < C_in; ++k) slack_features[r * C_in + k] += du_slack[k];
+      scatter(m.Fp, ptaps, du_slack.data() + C_in, spr);
     }
-    min_rel[r - r0] = best;
   }
   return 0;
 }
@@ -934,55 +941,6 @@ int lpo_trace(int kind, int H, int W, int D, int K, const double* p0, const doub
     T[j] = rt.T[j];
     w[j] = rt.w[j];
     for (int k = 0; k < C; ++k) c[j * C + k] = rt.c[j][k];
-  }
-  return 0;
-}
-
-// Conditioning of the ReLU decisions along each ray [r0, r1): the minimum over
-// samples and hidden units of |z| / (sum_k |W_ik a_k| + |b_i|). A hidden
-// pre-activation within rounding of 0 makes ReLU'(z) (reading R7,
-// ReLU'(0) = 0) a decision that fp32 and fp64 evaluations may take
-// differently; both are correct roundings, so parity tests exclude such rays
-// from gradient comparison.
-int lpo_render_min_preact(int kind, int H, int W, int D, int K, const double* p0, const double* p1, const double* p2,
-                          int n_layers, const int* widths, const double* params, int64_t r0, int64_t r1,
-                          const double* origins, const double* dirs, const double* nearv, const double* farv, int S,
-                          double* min_rel, int contraction, double contract_a, int dir_freqs) {
-  if (check(kind, H, W, D, K, n_layers, widths, S)) return 1;
-  Field F = make_field(kind, H, W, D, K, p0, p1, p2, n_layers, widths, params, contraction, contract_a,
-                       dir_freqs);
-  RayTrace rt;
-  for (int64_t r = r0; r < r1; ++r) {
-    trace_ray(F, origins + 3 * r, dirs + 3 * r, nearv[r], farv[r], S, rt);
-    double best = INFINITY;
-    auto scan = [&](const Field& N, const std::vector<MlpTrace>& trs) {
-      for (int j = 0; j < S; ++j) {
-        const double* p = N.params;
-        for (int l = 0; l < n_layers - 1; ++l) {
-          int fin = N.widths[l], fout = N.widths[l + 1];
-          const double* Wl = p;
-          const double* bl = p + (int64_t)fout * fin;
-          p = bl + fout;
-          for (int i = 0; i < fout; ++i) {
-            double sc = std::fabs(bl[i]);
-            for (int k = 0; k < fin; ++k) sc += std::fabs(Wl[(int64_t)i * fin + k] * trs[j].a[l][k]);
-            if (sc > 0.0) {
-              double q = std::fabs(trs[j].z[l][i]) / sc;
-              if (q < best) best = q;
-            }
-          }
-        }
-      }
-    };
-    if (dir_freqs > 0) {
-      Field Fs, Fv;
-      split_nets(F, Fs, Fv);
-      scan(Fs, rt.mlp);
-      scan(Fv, rt.mlpv);
-    } else {
-      scan(F, rt.mlp);
-    }
-    min_rel[r - r0] = best;
   }
   return 0;
 }

@@ -141,51 +141,60 @@ def test_splat_edge_cases(torch_cuda):
 
 
 # ---------------------------------------------------------------- g_s (Eq. 2)
-GS_CASES = [(wl.VOXEL, 24, {}), (wl.TRIPLANE, 40, {}), (wl.TRIPLANE, 32, dict(contraction=1, contract_a=0.9))]
+# every ray compared at the benchmark's 160 points per ray; grid resolution
+# 24-40 for the quick cases, the benchmark's 160 (triplane) / 128 (voxel) for one each
+GS_CASES = [(wl.VOXEL, 24, 768, {}), (wl.TRIPLANE, 40, 768, {}),
+            (wl.TRIPLANE, 32, 768, dict(contraction=1, contract_a=0.9)),
+            (wl.TRIPLANE, 160, 512, {}), (wl.VOXEL, 128, 256, {})]
 RELU_BAND = 2e-5
 
 
-@pytest.mark.parametrize("kind,res,over", GS_CASES)
-def test_splat_mlp_parity(torch_cuda, kind, res, over):
+@pytest.mark.parametrize("kind,res,n,over", GS_CASES)
+def test_splat_mlp_parity(torch_cuda, kind, res, n, over):
     """Forward (theta, theta_weight, normalised) and all gradients (features, prior, g_s
-    params) of the g_s Splatter vs the oracle. Rays with a g_s ReLU decision within
-    RELU_BAND of 0 (relative) are left out of the comparison."""
+    params) of the g_s Splatter vs the oracle, on every ray. Gradients: the metric
+    subtracts the oracle's bound for g_s ReLU decisions within RELU_BAND of 0
+    (oracle.splat_mlp_relu_slack); the raw (slack-free)
+    errors are asserted too."""
     import paper_2404_19760_b200 as lpb
+    from tests.helpers import rel_inf_slack
     torch = torch_cuda
-    cfg = wl.get_config("s1" if kind == wl.VOXEL else "s2", res=res, S=48, **over)
+    cfg = wl.get_config("s1" if kind == wl.VOXEL else "s2", res=res, S=160, **over)
     spec = _spec(cfg)
     F = 4
     widths = (32 + 32 + 6 * F, 64, 32)
     params = wl.make_mlp(widths, seed=120, hidden_bias_scale=0.2)
     prior = [wl.counter_uniform(121 + i, np.arange(int(np.prod(s)), dtype=np.uint64), -1, 1).reshape(s)
              for i, s in enumerate(spec.shapes(32))]
-    idx = wl.subset_indices(cfg, 768)
+    idx = wl.subset_indices(cfg, n)
     rays = wl.make_rays(cfg, idx)
     v = wl.make_features(idx, 32)
     g = oracle.SplatMlp(prior, widths, params, 32, F)
-    keep = oracle.splat_mlp_min_preact(spec, oracle.Rays(*rays, cfg.S), v, g) > RELU_BAND
-    assert keep.mean() > 0.5
-    rays = tuple(a[keep] for a in rays)
-    v = v[keep]
     R = oracle.Rays(*rays, cfg.S)
     ref_out, ref_th, ref_wt = oracle.splat_forward_mlp(spec, R, v, g)
     gout = wl.make_grid_grad(spec.shapes())
     ref_gv, ref_gpr, ref_gpa = oracle.splat_backward_mlp(spec, R, v, g, gout, ref_wt)
+    sv, spr, spa = oracle.splat_mlp_relu_slack(spec, R, v, g, gout, ref_wt, band=RELU_BAND)
 
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     grid = lpb.SplatGrid(cfg.kind, (cfg.res,) * 3, 32, cfg.contraction, cfg.contract_a)
     gs = lpb.SplatMlp(T(params), [T(p) for p in prior], 32, F, 64)
-    o, d, n, f = (T(a) for a in rays)
-    th, wt = lpb.splat_forward_mlp(grid, o, d, n, f, cfg.S, T(v), gs)
+    o, d, nr, fr = (T(a) for a in rays)
+    th, wt = lpb.splat_forward_mlp(grid, o, d, nr, fr, cfg.S, T(v), gs)
     out = lpb.splat_normalize(grid, th, wt)
-    gv, gpr, gpa = lpb.splat_backward_mlp(grid, o, d, n, f, cfg.S, T(v), gs, [T(x) for x in gout], wt)
+    gv, gpr, gpa = lpb.splat_backward_mlp(grid, o, d, nr, fr, cfg.S, T(v), gs, [T(x) for x in gout], wt)
     torch.cuda.synchronize()
+    gv, gpa, gpr = gv.cpu().numpy(), gpa.cpu().numpy(), [a.cpu().numpy() for a in gpr]
     errs = dict(out=max(rel_inf(a.cpu().numpy(), b) for a, b in zip(out, ref_out)),
                 theta=max(rel_inf(a.cpu().numpy(), b) for a, b in zip(th, ref_th)),
                 weight=max(rel_inf(a.cpu().numpy(), b) for a, b in zip(wt, ref_wt)),
-                gfeat=rel_inf(gv.cpu().numpy(), ref_gv),
-                gprior=max(rel_inf(a.cpu().numpy(), b) for a, b in zip(gpr, ref_gpr)),
-                gparams=rel_inf(gpa.cpu().numpy(), ref_gpa))
+                gfeat=rel_inf_slack(gv, ref_gv, sv),
+                gprior=max(rel_inf_slack(a, b, s) for a, b, s in zip(gpr, ref_gpr, spr)),
+                gparams=rel_inf_slack(gpa, ref_gpa, spa),
+                raw_gfeat=rel_inf(gv, ref_gv), raw_gprior=max(rel_inf(a, b) for a, b in zip(gpr, ref_gpr)),
+                raw_gparams=rel_inf(gpa, ref_gpa),
+                ambiguous_rays=int(np.count_nonzero(sv.max(axis=1) > 0)), rays=len(idx))
     print(errs)
     assert errs["out"] < 1e-4 and errs["theta"] < 1e-4 and errs["weight"] < 1e-4, errs
-    assert errs["gfeat"] < 1e-3 and errs["gprior"] < 1e-3 and errs["gparams"] < 1e-3, errs
+    for k in ("gfeat", "gprior", "gparams", "raw_gfeat", "raw_gprior", "raw_gparams"):
+        assert errs[k] < 1e-3, (k, errs)

@@ -395,7 +395,7 @@ def test_view_dependent_matches_torch_autograd():
     assert rel_inf(gp, params.grad.numpy()) < 1e-10
 
 
-def test_view_dependent_relu_slack_runs_and_bounds():
+def test_view_dependent_relu_slack_is_zero_without_ambiguity():
     """relu_slack on a view-dependent field: buffers sized for both networks, slack >= 0,
     and zero slack when no pre-activation is ambiguous (band = 0)."""
     F, _ = _vd_field(wl.TRIPLANE, (4, 5, 6))
@@ -406,4 +406,58 @@ def test_view_dependent_relu_slack_runs_and_bounds():
     assert sp.shape == F.params.shape and np.all(sp >= 0) and all(np.all(g >= 0) for g in sg)
     sg0, sp0 = oracle.relu_slack(F, rays, p, band=0.0)
     assert float(np.abs(sp0).sum()) == 0.0
-    assert np.all(np.isfinite(oracle.min_preact(F, rays)))
+
+
+def _direnc(d, F):
+    """direnc per S:146 in the order pinned by test_direnc_through_a_probe_network:
+    per axis k, per frequency 2^i: sin(pi 2^i d_k), cos(pi 2^i d_k)."""
+    e = []
+    for k in range(3):
+        for i in range(F):
+            e += [math.sin(math.pi * 2.0 ** i * d[k]), math.cos(math.pi * 2.0 ** i * d[k])]
+    return np.array(e)
+
+
+@pytest.mark.parametrize("net", ["sigma", "color"])
+def test_view_dependent_relu_slack_bounds_a_flipped_decision(net):
+    """The two-network slack (R29) bounds the gradient jump of a flipped decision in
+    either network: put hidden unit 1 of g_sigma (or g_v, whose input is
+    [h ; direnc(d)]) exactly at z = 0 on one sample, evaluate the oracle gradients
+    with its bias nudged to either side (the forward does not move, ReLU'
+    flips), and check |g+ - g-| <= slack elementwise."""
+    K, hid, Fq = 3, 5, 2
+    Fd, _ = _vd_field(wl.TRIPLANE, (4, 5, 6), K=K, hid=hid, F=Fq)
+    o, d, near, far = tiny_rays(2, inside_start=True)
+    S = 7
+    rays = oracle.Rays(o[:1], d[:1], near[:1], far[:1], S)
+    p = np.array([[0.7, -0.4, 0.9]])
+    gt = np.array([0.3])
+    bg = np.array([0.1, 0.2, 0.3])
+    Dl = (float(far[0]) - float(near[0])) / (S - 1)
+    x = o[0].astype(np.float64) + (float(near[0]) + 3 * Dl) * d[0].astype(np.float64)
+    h = oracle.sample(Fd, x[None])[0]
+    nsig = hid * K + hid + hid + 1
+    if net == "sigma":
+        W0, b_at, u = Fd.params[:hid * K].reshape(hid, K), hid * K, h
+    else:
+        E = 6 * Fq
+        W0 = Fd.params[nsig:nsig + hid * (K + E)].reshape(hid, K + E)
+        b_at, u = nsig + hid * (K + E), np.concatenate([h, _direnc(d[0].astype(np.float64), Fq)])
+    unit = 1
+    Fd.params[b_at + unit] -= float(W0[unit] @ u + Fd.params[b_at + unit])      # z = 0 at sample 3
+    base = Fd.params[b_at + unit]
+    res = []
+    for eps in (+1e-11, -1e-11):
+        Fd.params[b_at + unit] = base + eps
+        res.append(oracle.render_backward(Fd, rays, p, gt, bg))
+    Fd.params[b_at + unit] = base
+    sg, sp = oracle.relu_slack(Fd, rays, p, gt, bg, band=1e-9)
+    jump_p = np.abs(res[0][1] - res[1][1])
+    assert jump_p.max() > 1e-6, "the flip must change the gradient"
+    assert np.all(jump_p <= sp + 1e-9)
+    for a, b, s_ in zip(res[0][0], res[1][0], sg):
+        assert np.abs(a - b).max() > 0 or net == "sigma"
+        assert np.all(np.abs(a - b) <= s_ + 1e-9)
+    # the slack names the flipped network: the other network's parameters get none
+    other = slice(nsig, None) if net == "sigma" else slice(0, nsig)
+    assert float(np.abs(sp[other]).sum()) == 0.0

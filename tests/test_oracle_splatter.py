@@ -257,3 +257,49 @@ def test_gs_backward_matches_finite_differences(kind):
             fdq[i] = (lp - lm) / (2 * eps)
         assert rel_inf(gpr[pi_].reshape(-1), fdq) < 1e-6
     assert np.max(np.abs(gv)) > 1e-3 and max(np.max(np.abs(a)) for a in gpr) > 1e-3
+
+
+@pytest.mark.parametrize("kind", [wl.TRIPLANE, wl.VOXEL])
+def test_gs_relu_slack_bounds_a_flipped_decision(kind):
+    """The g_s slack (parity metric allowance) bounds the jump of the features,
+    prior and parameter gradients when one g_s ReLU decision flips: hidden
+    unit 2 is put exactly at z = 0 on one sample (u = [v ; h_prior(x) ;
+    direnc(d)]), the gradients are evaluated with its bias nudged to either
+    side, and |g+ - g-| <= slack elementwise; band 0 gives zero slack."""
+    spec = _spec(kind, K=3)
+    o, d, near, far = tiny_rays(2, inside_start=True)
+    S = 6
+    rays = oracle.Rays(o[:1], d[:1], near[:1], far[:1], S)
+    C_in, Kp, F, hid = 2, 2, 1, 5
+    widths = (C_in + Kp + 6 * F, hid, spec.K)
+    params = wl.make_mlp(widths, seed=97, hidden_bias_scale=0.3).astype(np.float64)
+    prior = _prior(spec, Kp)
+    v = np.array([[0.6, -0.8]])
+    gout = [wl.counter_uniform(99 + i, np.arange(int(np.prod(s)), dtype=np.uint64), -1, 1).reshape(s).astype(np.float64)
+            for i, s in enumerate(spec.shapes())]
+    Dl = (float(far[0]) - float(near[0])) / (S - 1)
+    x = o[0].astype(np.float64) + (float(near[0]) + 2 * Dl) * d[0].astype(np.float64)
+    Fp = oracle.Field(spec.kind, prior, (Kp, 2), np.zeros(Kp * 2 + 2))
+    dd = d[0].astype(np.float64)
+    e = [f(np.pi * dd[k]) for k in range(3) for f in (np.sin, np.cos)]          # F = 1: sin, cos per axis
+    u = np.concatenate([v[0], oracle.sample(Fp, x[None])[0], e])
+    In = widths[0]
+    W0, b_at, unit = params[:hid * In].reshape(hid, In), hid * In, 2
+    params[b_at + unit] -= float(W0[unit] @ u + params[b_at + unit])
+    base = params[b_at + unit]
+    g0 = oracle.SplatMlp(prior, widths, params, C_in, F)
+    _, _, wt = oracle.splat_forward_mlp(spec, rays, v, g0)
+    res = []
+    for eps in (+1e-11, -1e-11):
+        pp = params.copy()
+        pp[b_at + unit] = base + eps
+        res.append(oracle.splat_backward_mlp(spec, rays, v, oracle.SplatMlp(prior, widths, pp, C_in, F), gout, wt))
+    sv, spr, spar = oracle.splat_mlp_relu_slack(spec, rays, v, g0, gout, wt, band=1e-9)
+    jv, jpar = np.abs(res[0][0] - res[1][0]), np.abs(res[0][2] - res[1][2])
+    assert jpar.max() > 1e-6 and jv.max() > 1e-6, "the flip must change the gradients"
+    assert np.all(jv <= sv + 1e-9) and np.all(jpar <= spar + 1e-9)
+    for a, b, s_ in zip(res[0][1], res[1][1], spr):
+        assert np.all(np.abs(a - b) <= s_ + 1e-9)
+    assert max(float(np.abs(a - b).max()) for a, b in zip(res[0][1], res[1][1])) > 1e-8
+    z = oracle.splat_mlp_relu_slack(spec, rays, v, g0, gout, wt, band=0.0)
+    assert float(np.abs(z[0]).sum() + sum(np.abs(a).sum() for a in z[1]) + np.abs(z[2]).sum()) == 0.0
