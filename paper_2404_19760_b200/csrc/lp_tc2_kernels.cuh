@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
     const float* b0 = fp + F::B0 + hf * HH;
     const float* b1 = fp + F::B1 + hf * HH;
     const float4* wot = reinterpret_cast<const float4*>(fp + F::WOT) + hf * HH;
+    LP_PT_DECL
 
     auto mma_done = [&]() {
       tc::mbar_wait(bar, phase);
@@ -415,6 +416,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
         sample_point(ray, q, a.contract, x);
         write_taps<KIND, K>(taps + rt * NPL, x, a.dims);
         __syncwarp();
+        LP_PT(0)
         if (SW == 0 && pending)   // warp-uniform
           coop_gather<KIND, K, HC, kTc2Pieces, true>(planes, taps, a.dims, Ht, L::HB_PIECE, wq * 32, lane, gplanes, ptaps, dhs,
                                             it0, it1);
@@ -422,6 +424,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
           coop_gather<KIND, K, HC, kTc2Pieces>(planes, taps, a.dims, Ht, L::HB_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
                                       it0, it1);
         pending = false;
+        LP_PT(1)
         to_tensor_core();
         if (gt == 0) {
           tc::fence_after_sync();
@@ -429,10 +432,12 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
           tc::mma_commit(bar);
         }
         mma_done();
+        LP_PT(2)
         if (SW > 0 && staged) {   // A1 piece 2 and the D region still hold the previous step's staging
           tc::mbar_wait(bar_dr, dphase);
           dphase ^= 1;
         }
+        LP_PT(7)
         uint32_t mask1 = 0;   // ReLU'(z1) of this half's hidden units
         {
           float z[HH];
@@ -449,6 +454,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
             tc::store8<kTc2Pieces>(A1t, L::A1_PIECE, rt, hf * HH + 8 * c, HC1, a1);
           }
         }
+        LP_PT(3)
         to_tensor_core();
         if (gt == 0) {
           tc::fence_after_sync();
@@ -456,6 +462,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
           tc::mma_commit(bar);
         }
         mma_done();
+        LP_PT(4)
         float a2[HH];
         {
           tc::tmem_ld<HH>(tS1 + tq + hf * HH, a2);
@@ -526,6 +533,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
           tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, 2 * HID, d2);
           tc::store8<2>(Dt, L::DP, rt, HID + hf * HH + 8 * c, 2 * HID, a2 + 8 * c);
         }
+        LP_PT(3)
         to_tensor_core();
         if (gt == 0) {
           tc::fence_after_sync();
@@ -548,6 +556,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
           tc::mma_commit(bar);
         }
         mma_done();
+        LP_PT(4)
         {   // delta1 = ReLU'(z1) dA1 -> D1 (over D2, consumed)
           float da[HH];
           tc::tmem_ld<HH>(tS0 + tq + hf * HH, da);
@@ -559,6 +568,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
             tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, 2 * HID, d1);
           }
         }
+        LP_PT(3)
         to_tensor_core();
         if (gt == 0) {
           tc::fence_after_sync();
@@ -580,6 +590,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
           tc::mma_commit(bar);
         }
         mma_done();
+        LP_PT(4)
         // ---- B6: this half's dH channels -> fp32 staging; scattered by the next step's gather
         {
           constexpr int HK = KP / 2;
@@ -602,8 +613,10 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
         }
         tc::fence_before_sync();
         tc::named_bar(1, 256);
+        LP_PT(3)
       }
     }
+    LP_PT_FLUSH(1)
     if (SW == 0 && pending) coop_scatter<KIND, K>(gplanes, ptaps, a.dims, dhs, wq * 32, lane, it0, it1);
 
     // ---- B7: flush the gradient partials (TMEM accumulators + register bias sums)

@@ -10,7 +10,8 @@ cfg = wl.get_config(sys.argv[1] if len(sys.argv) > 1 else "c4")
 M = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 20
 o, d, n, f = wl.make_rays(cfg, start=0, count=M)
 T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
-field = lpb.Field(cfg.kind, [T(g) for g in wl.make_grid(cfg)], cfg.widths, T(wl.make_params(cfg)))
+field = lpb.Field(cfg.kind, [T(g) for g in wl.make_grid(cfg)], cfg.widths, T(wl.make_params(cfg)),
+                  cfg.contraction, cfg.contract_a, cfg.dir_freqs)
 o, d, n, f = T(o), T(d), T(n), T(f)
 go = T(wl.make_grad_out(np.arange(M), cfg.C))
 fn = _lib.lib.lp_debug_phase_cycles
@@ -26,6 +27,8 @@ torch.cuda.synchronize(); fn(buf, 0)
 v = np.array(list(buf), dtype=np.float64).reshape(2, 8)
 names = [["taps", "gather", "bar", "mma-issue", "mma-wait", "epilogue", "-", "-"],
          ["taps", "gather", "bar1", "mma1-wait", "epilogue", "bar2+mma2-wait", "scatter", "drained-wait"]]
+if len(cfg.widths) == 4 and not cfg.dir_freqs:   # K2tc2 (lp_tc2_kernels.cuh LP_PT slots)
+    names[1] = ["taps", "gather", "bar+Z1-wait", "epilogues", "bar+MMA2/3/4-wait", "-", "-", "drained-wait"]
 for k, nm in enumerate(("fwd", "bwd")):
     tot = v[k].sum()
     print(nm, f"{(e0.elapsed_time(e1) if k == 0 else e1.elapsed_time(e2)):.2f} ms",
