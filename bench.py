@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU work for the oracle baseline")
+    ap.add_argument("--l2-persist", type=float, default=0.0,
+                    help="hit ratio of an L2 persisting access-policy window on theta (lp_set_l2_persist; 0 = off)")
     return ap.parse_args()
 
 
@@ -315,6 +317,8 @@ def run_ours(args):
     from paper_2404_19760_b200.dist import FlatGrads, allreduce_grads, shard_range
 
     cfg = wl.get_config(args.config)
+    if args.l2_persist > 0:
+        lpb.set_l2_persist(args.l2_persist)
     M_all = cfg.n_rays
     lo, hi = shard_range(M_all, rank, world)
     M = hi - lo
@@ -483,6 +487,8 @@ def run_ours(args):
         "clocks": clk_sum,
         "gpu_launches": 2 * args.steps,
     }
+    if args.l2_persist > 0:
+        line["config"]["l2_persist_hit_ratio"] = args.l2_persist
     if e2e:
         line["e2e"] = e2e
     if not args.no_cpu_baseline and world == 1:

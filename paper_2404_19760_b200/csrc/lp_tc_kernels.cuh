@@ -167,7 +167,7 @@ __device__ __forceinline__ int coop_row(int row0, int it, int sub) {
 // Ray of tile slot rt (offset within the 128-ray tile). A warp's 32 rays are an
 // 8x4-pixel block in raster order (workload `pixel_of`); with K = 32 (4 rays per
 // cooperative iteration) slots 4i..4i+3 of the block take its 2x2-pixel quad i, whose
-// corner sets overlap most (L1 reuse within an iteration; window_scatter_plane). The
+// corner sets overlap most (L1 reuse within an iteration). The
 // permutation stays inside each 32-ray block, so tail tiles keep their valid rays.
 template <int K>
 __device__ __forceinline__ int ray_slot(int rt) {
@@ -182,87 +182,16 @@ __device__ __forceinline__ int ray_slot(int rt) {
   }
 }
 
-#ifndef LP_WINDOW_SCATTER
-#define LP_WINDOW_SCATTER 0
+#ifndef LP_SCATTER_UNIFORM  // coop_scatter: one reduction per line when all rays of an instruction share a cell
+#define LP_SCATTER_UNIFORM 0
 #endif
-#ifndef LP_SCATTER_WINDOW   // the same merge in the scatter warps' coop_scatter (experiment)
-#define LP_SCATTER_WINDOW 0
-#endif
-#ifndef LP_SCATTER_PAIR     // coop_scatter merges the shared corners of horizontal ray pairs
-#define LP_SCATTER_PAIR 0
-#endif
-
-// B6 for one triplane plane and the 4 rays of a cooperative iteration (K = 32),
-// merged over shared corners. If the inside rays' cells span at most 3 x 3 cells,
-// the union of their corners lies in a 4 x 4 vertex window anchored at the minimum
-// cell (amin, bmin); lane (sub, ch) owns window column bmin + sub and, for each row
-// amin + k, sums w_t(vertex) dh_t over the rays t (the bilinear weight factors per
-// axis), then issues one 16-byte reduction per touched vertex. The reductions of a
-// quad drop to the number of distinct corner lines (c4: ~55% of 4 per ray, c3:
-// ~33%). Returns false (nothing issued) when the cells do not fit the window; the
-// caller then reduces each ray's own corners. Sums are reassociated (fp32), as the
-// atomics already are.
-template <int K>
-__device__ __forceinline__ bool window_scatter_plane(float* gpl, const float4* ptaps, const float* dhs,
-                                                     const int (&rows)[4], int p, int sub, int sa) {
-  constexpr int NPL = 3;
-  // all shared-memory reads first (broadcast records, the rays' dh chunks): with two
-  // warps per scheduler the merge must be short dependent chains over 4 independent rays
-  float4 pr[4], d[4];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) pr[t] = ptaps[rows[t] * NPL + p];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) d[t] = *reinterpret_cast<const float4*>(dhs + rows[t] * (K + 4));
-  int ia[4], ib[4];
-  bool in[4];
-  int amin = 1 << 30, amax = -1, bmin = 1 << 30, bmax = -1;
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int pk = __float_as_int(pr[t].w);
-    in[t] = __float_as_int(pr[t].x) >= 0;
-    ia[t] = pk >> 16;
-    ib[t] = pk & 0xffff;
-    amin = min(amin, in[t] ? ia[t] : 1 << 30);
-    amax = max(amax, in[t] ? ia[t] : -1);
-    bmin = min(bmin, in[t] ? ib[t] : 1 << 30);
-    bmax = max(bmax, in[t] ? ib[t] : -1);
-  }
-  if (amax < 0) return true;                                    // no ray inside: nothing to reduce
-  if (amax - amin > 2 || bmax - bmin > 2) return false;         // warp-uniform
-  float4 acc[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) acc[k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-  unsigned touched = 0;
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int ca = ia[t] - amin, cb = sub - (ib[t] - bmin);   // ca in [0, 2]; this lane's column touched iff cb in {0, 1}
-    const float fa = pr[t].y, fb = pr[t].z;
-    const float m0 = (in[t] && cb == 0) ? 1.0f : 0.0f, m1 = (in[t] && cb == 1) ? 1.0f : 0.0f;
-    const float wb = fmaf(m1, fb, m0 * (1.0f - fb));
-    touched |= (m0 + m1 != 0.0f ? 3u : 0u) << ca;
-    const float4 e = make_float4(wb * d[t].x, wb * d[t].y, wb * d[t].z, wb * d[t].w);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float c = (ca == k ? 1.0f - fa : 0.0f) + (ca == k - 1 ? fa : 0.0f);
-      acc[k].x = fmaf(c, e.x, acc[k].x);
-      acc[k].y = fmaf(c, e.y, acc[k].y);
-      acc[k].z = fmaf(c, e.z, acc[k].z);
-      acc[k].w = fmaf(c, e.w, acc[k].w);
-    }
-  }
-  float* col = gpl + (amin * sa + (bmin + sub) * K);
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if ((touched >> k) & 1u) atomicAdd(reinterpret_cast<float4*>(col + k * sa), acc[k]);
-  return true;
-}
 
 // Warp-cooperative gather of the warp's 32 rays: lane = (ray RPI-subgroup, chunk).
 // Writes h into rows [row0, row0 + 32) of the H tile (NP bf16 pieces).
 // With SCATTER, each iteration also issues the grid-gradient reductions of the
-// previous march step for the same lane slot (records `ptaps`, dh rows `dhs`),
-// merged per quad where their corners overlap (window_scatter_plane): the L2
-// reductions of step q+1 overlap the corner loads of step q (B6 || F3).
+// previous march step for the same lane slot (records `ptaps`, dh rows `dhs`):
+// the L2 reductions of step q+1 overlap the corner loads of step q (B6 || F3;
+// the fused-scatter mode, SW = 0).
 // Iterations [it0, it1) of the KC = K/4 per warp (two warps may split one row block).
 template <int KIND, int K, int C, int NP, bool SCATTER = false, bool PAIR = true, int UNROLL = kGatherUnroll>
 __device__ __forceinline__ void coop_gather(const float* const* planes, const float4* taps, const GridDims& g,
@@ -292,17 +221,7 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
       float4 v[Corners<KIND, K>::N];
 #pragma unroll
       for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) v[cc] = __ldg(reinterpret_cast<const float4*>(pl + c.off[cc]));
-      bool merged = false;
-      if constexpr (SCATTER && KIND == 0 && RPI == 4 && LP_WINDOW_SCATTER) {
-        if (!wplanes) {
-          int rows[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) rows[t] = coop_row<RPI>(row0, it, t);
-          const int sa = (p == 0 ? g.W : p == 1 ? g.D : g.H) * K;
-          merged = window_scatter_plane<K>(gplanes[p] + 4 * ch, ptaps, dhs + 4 * ch, rows, p, sub, sa);
-        }
-      }
-      if constexpr (SCATTER) if (!merged) {
+      if constexpr (SCATTER) {
         const float4 prec = ptaps[row * NPL + p];
         if (__float_as_int(prec.x) >= 0) {
           const float4 d = *reinterpret_cast<const float4*>(dhs + row * (K + 4) + 4 * ch);
@@ -311,9 +230,6 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
           float* gpl = gplanes[p] + 4 * ch;
 #pragma unroll
           for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) {
-#ifdef LP_ABL_SKIPRED   // ablation (timing only, wrong results): bit (p * 4 + cc) set = reduction skipped
-            if ((LP_ABL_SKIPRED >> (p * 4 + cc)) & 1) continue;
-#endif
             const float w = pc.w[cc];
             atomicAdd(reinterpret_cast<float4*>(gpl + pc.off[cc]), make_float4(w * d.x, w * d.y, w * d.z, w * d.w));
           }
@@ -370,55 +286,37 @@ __device__ __forceinline__ void coop_scatter(float* const* gplanes, const float4
     const float4 d = *reinterpret_cast<const float4*>(dhs + row * (K + 4) + 4 * ch);
 #pragma unroll
     for (int p = 0; p < NPL; ++p) {
-      if constexpr (KIND == 0 && RPI == 4 && LP_SCATTER_WINDOW) {   // experiment: merge the quad's corners
-        if (!wplanes) {
-          int rows[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) rows[t] = coop_row<RPI>(row0, it, t);
-          const int sa = (p == 0 ? g.W : p == 1 ? g.D : g.H) * K;
-          if (window_scatter_plane<K>(gplanes[p] + 4 * ch, taps, dhs + 4 * ch, rows, p, sub, sa)) continue;
-        }
-      }
       const float4 rec = taps[row * NPL + p];
-      if (__float_as_int(rec.x) < 0) continue;
-      Corners<KIND, K> c;
-      record_corners<KIND, K>(rec, p, g, c);
-      float* pl = gplanes[p] + 4 * ch;
-      if constexpr (KIND == 0 && RPI == 4 && LP_SCATTER_PAIR) {
-        if (!wplanes) {   // merge with the horizontal neighbour of the 2x2 quad (slot sub ^ 1)
-          const int prow = coop_row<RPI>(row0, it, sub ^ 1);
-          const float4 d2 = *reinterpret_cast<const float4*>(dhs + prow * (K + 4) + 4 * ch);
-          const float4 rec2 = taps[prow * NPL + p];
-          const int base2 = __float_as_int(rec2.x);
-          const int nb = (p == 0 ? g.W : p == 1 ? g.D : g.H);   // vertices per row of this plane
-          const bool owner = (sub & 1) == 0;
+#if LP_SCATTER_UNIFORM
+      if (!wplanes) {   // N1 experiment: all RPI rays of this instruction in one cell -> reduce once
+        const int base = __float_as_int(rec.x);
+        if (__all_sync(0xffffffffu, base >= 0 && base == __shfl_sync(0xffffffffu, base, 0))) {
+          Corners<KIND, K> c;
+          record_corners<KIND, K>(rec, p, g, c);
+          float* pl = gplanes[p] + 4 * ch;
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            // vertex offset of this corner from the partner's corner (0, 0): the partner
-            // has it iff dv is one of its corners' 0, 1, nb, nb + 1
-            const int dv = (c.off[cc] - base2) / K;
-            const bool shared = base2 >= 0 && (dv == 0 || dv == 1 || dv == nb || dv == nb + 1);
-            if (shared && !owner) continue;   // the owner lane reduces this line
+          for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) {
             const float w = c.w[cc];
             float4 v = make_float4(w * d.x, w * d.y, w * d.z, w * d.w);
-            if (shared) {
-              const int a2 = dv >= nb ? 1 : 0, b2 = dv - a2 * nb;
-              const float w2 = (a2 ? rec2.y : 1.0f - rec2.y) * (b2 ? rec2.z : 1.0f - rec2.z);
-              v.x = fmaf(w2, d2.x, v.x);
-              v.y = fmaf(w2, d2.y, v.y);
-              v.z = fmaf(w2, d2.z, v.z);
-              v.w = fmaf(w2, d2.w, v.w);
+#pragma unroll
+            for (int off = KC; off < 32; off <<= 1) {   // sum over the rays (lanes of equal chunk)
+              v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+              v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+              v.z += __shfl_xor_sync(0xffffffffu, v.z, off);
+              v.w += __shfl_xor_sync(0xffffffffu, v.w, off);
             }
-            atomicAdd(reinterpret_cast<float4*>(pl + c.off[cc]), v);
+            if (sub == 0) atomicAdd(reinterpret_cast<float4*>(pl + c.off[cc]), v);
           }
           continue;
         }
       }
+#endif
+      if (__float_as_int(rec.x) < 0) continue;
+      Corners<KIND, K> c;
+      record_corners<KIND, K>(rec, p, g, c);
+      float* pl = gplanes[p] + 4 * ch;
 #pragma unroll
       for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) {
-#ifdef LP_ABL_SKIPRED   // ablation (timing only, wrong results): bit (p * 4 + cc) set = reduction skipped
-        if ((LP_ABL_SKIPRED >> (p * 4 + cc)) & 1) continue;
-#endif
         const float w = c.w[cc];
         atomicAdd(reinterpret_cast<float4*>(pl + c.off[cc]), make_float4(w * d.x, w * d.y, w * d.z, w * d.w));
       }
@@ -764,7 +662,6 @@ __global__ void __launch_bounds__(128 * T * G + 32 * bwd_scatter_warps<T>(), 1) 
         write_taps<KIND, K>(taps + rt * S::NPL, x, a.dims);
         __syncwarp();
         LP_PT(0)
-#ifndef LP_ABL_NOGATHER
         if (SW == 0 && pending)   // warp-uniform
           coop_gather<KIND, K, S::HC, kBwdHPieces, true>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, gplanes, ptaps, dhs,
                                                it0, it1);
@@ -772,7 +669,6 @@ __global__ void __launch_bounds__(128 * T * G + 32 * bwd_scatter_warps<T>(), 1) 
           coop_gather<KIND, K, S::HC, kBwdHPieces>(planes, taps, a.dims, Ht, S::HB_PIECE, wg * 32, lane, nullptr, nullptr,
                                          nullptr, it0, it1);
         pending = false;
-#endif
         LP_PT(1)
         tc::fence_async_smem();
         tc::fence_before_sync();
@@ -918,9 +814,7 @@ __global__ void __launch_bounds__(128 * T * G + 32 * bwd_scatter_warps<T>(), 1) 
 #pragma unroll
           for (int pp = 0; pp < S::NPL; ++pp) ptaps[rt * S::NPL + pp] = taps[rt * S::NPL + pp];
         }
-#ifndef LP_ABL_NOSCATTER   // ablation hooks (timing experiments only; results are wrong when set)
         pending = true;
-#endif
         if constexpr (SW > 0) {
           tc::mbar_arrive(bar_st);
           staged = true;

@@ -4,6 +4,13 @@
 //   gran <bytes> <MB>: A with <bytes>-granules (corner vectors of K = bytes/4 channels,
 //   bytes/16 lanes each) at random granule-aligned offsets of a <MB> buffer -- the
 //   ceilings of the K = 16 voxel grid (c2: 64 B into 128 MB) and of the 2 GiB c5 grid
+//   seq: A on sequential lines (warp w reduces a contiguous run of lines): is the
+//   random-line rate the ceiling, or do conflicts of random lines cost throughput?
+//   gather <window_lines>: the forward's load side -- 8 lanes x LDG.128 per 128-B
+//   line, 4 lines per warp instruction, 4 instructions in flight per lane, lines
+//   drawn at random from a per-warp window of <window_lines> lines (small window:
+//   every load hits L1 -> the L1 line-gather ceiling; 0 = random over the 24 MB
+//   buffer -> L1 misses served by L2, the L2->SM gather ceiling)
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
@@ -52,6 +59,78 @@ __global__ void redG(float* g, const long long* offs, int n_per_warp, int lanes_
   }
 }
 
+__global__ void redSeq(float* g, int nl_per_warp) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int sub = lane >> 3, ch = lane & 7;
+  const size_t base = (size_t)warp * nl_per_warp;
+  for (int i = 0; i < nl_per_warp; i += 4) {
+    float4 v = make_float4(1.f, 1.f, 1.f, 1.f);
+    atomicAdd(reinterpret_cast<float4*>(g + (base + i + sub) * 32 + 4 * ch), v);
+  }
+}
+
+__global__ void gatherK(const float* __restrict__ g, const int* lines, int nl_per_warp, float* sink) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int* L = lines + (size_t)warp * nl_per_warp;
+  const int sub = lane >> 3, ch = lane & 7;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = 0; i < nl_per_warp; i += 16) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(g + (size_t)L[i + 4 * u + sub] * 32 + 4 * ch));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+    }
+  }
+  if (acc.x + acc.y + acc.z + acc.w == 12345.f) sink[0] = acc.x;
+}
+
+static int gather_mode(int window) {
+  const int nlines = 24 * 1024 * 1024 / 128;
+  const int blocks = 148 * 4, threads = 256, warps = blocks * threads / 32, per = 4096;
+  float *g, *sink; int* lines;
+  cudaMalloc(&g, (size_t)nlines * 128); cudaMemset(g, 0, (size_t)nlines * 128);
+  cudaMalloc(&sink, 4);
+  cudaMalloc(&lines, (size_t)warps * per * 4);
+  int* h = new int[(size_t)warps * per];
+  uint32_t s = 7;
+  for (int w = 0; w < warps; ++w)
+    for (int i = 0; i < per; ++i) {
+      s = s * 1664525u + 1013904223u;
+      h[(size_t)w * per + i] = window > 0 ? (int)(((size_t)w * window + (s >> 4) % window) % nlines) : (int)((s >> 4) % nlines);
+    }
+  cudaMemcpy(lines, h, (size_t)warps * per * 4, cudaMemcpyHostToDevice);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(a);
+    gatherK<<<blocks, threads>>>(g, lines, per, sink);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    const double nl = (double)warps * per;
+    printf("gather window %6d lines: %.3f ms  %.2f G lines/s  %.2f TB/s  (%s)\n", window, ms, nl / ms / 1e6,
+           nl * 128 / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}
+
+static int seq_mode() {
+  const int blocks = 148 * 4, threads = 256, warps = blocks * threads / 32, per = 64;
+  float* g;
+  cudaMalloc(&g, (size_t)warps * per * 128); cudaMemset(g, 0, (size_t)warps * per * 128);   // 24 MB
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(a);
+    for (int k = 0; k < 64; ++k) redSeq<<<blocks, threads>>>(g, per);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    const double nl = (double)warps * per * 64;
+    printf("seq lines (24 MB, 64 launches): %.3f ms  %.2f G lines/s  %.2f TB/s payload  (%s)\n", ms, nl / ms / 1e6,
+           nl * 128 / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}
+
 static int gran_mode(int gbytes, long long mb) {
   const long long nfl = mb * 1024 * 1024 / 4, ngran = nfl / (gbytes / 4);
   const int blocks = 148 * 4, threads = 256, warps = blocks * threads / 32, per = 4096;
@@ -80,7 +159,9 @@ static int gran_mode(int gbytes, long long mb) {
 }
 
 int main(int argc, char** argv) {
-  if (argc > 3 && argv[1][0] == 'g') return gran_mode(atoi(argv[2]), atoll(argv[3]));
+  if (argc > 3 && argv[1][0] == 'g' && argv[1][1] == 'r') return gran_mode(atoi(argv[2]), atoll(argv[3]));
+  if (argc > 2 && argv[1][0] == 'g' && argv[1][1] == 'a') return gather_mode(atoi(argv[2]));
+  if (argc > 1 && argv[1][0] == 's' && argv[1][1] == 'e') return seq_mode();
   // usage: red_bench [n_sm]  -- with n_sm < 148: one 1024-thread block per SM on n_sm SMs
   // (per-SM scaling of the reduction rate); default: 4 x 256-thread blocks per SM on all 148
   const int nlines = 24 * 1024 * 1024 / 128;  // 24 MB buffer
