@@ -58,7 +58,17 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU work for the oracle baseline")
     ap.add_argument("--l2-persist", type=float, default=0.0,
                     help="hit ratio of an L2 persisting access-policy window on theta (lp_set_l2_persist; 0 = off)")
+    ap.add_argument("--ray-order", default="tiled", choices=["tiled", "raster", "shuffled"],
+                    help="order of the rays in the batch (workload Config.ray_order): 16x8-pixel tiles "
+                         "(default), per-view raster, or a seeded shuffle of all rays of all views")
     return ap.parse_args()
+
+
+def bench_config(args):
+    cfg = wl.get_config(args.config)
+    if args.ray_order != "tiled":
+        cfg = wl.get_config(args.config, ray_order=args.ray_order)
+    return cfg
 
 
 # ------------------------------------------------------------------ algorithmic work
@@ -170,6 +180,15 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
+# What the path computes in ("Tensor-core precision"): fp32 ray I/O, fp32
+# epilogues and EA state, fp32 TMEM accumulation; the tcgen05 contractions take bf16-split operands
+# x = x0 + x1 (+ x2): forward-type ones (Z, Z2, g_s layers) 3 x 3 pieces / 6 products (24 significand
+# bits, fp32-class), gradient-type ones (dH, dW) 2 pieces / 3 products (16 bits, ~1.5e-5 relative
+# per product); sample positions and cell indices in fp64.
+DTYPE_RENDER = "f32 io/accum; split-bf16 tcgen05 MMA (3-piece fwd-type, 2-piece grad-type); fp64 positions"
+DTYPE_SPLAT = "f32 io/accum; split-bf16 tcgen05 MMA (g_s: 3-piece fwd-type, 2-piece grad-type)"
+
+
 # ------------------------------------------------------------------ CPU oracle baseline
 ORACLE_BUF_BYTES = 16e9   # host memory for the oracle's per-thread fp64 gradient copies
 
@@ -247,7 +266,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = wl.get_config(args.config)
+    cfg = bench_config(args)
     cores = host_cores()
     per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
     rates = []
@@ -283,7 +302,7 @@ def config_dict(cfg, n):
     return {"workload": f"{cfg.name}: {cfg.note}", "rays": cfg.n_rays, "rays_per_gpu": cfg.n_rays // n,
             "samples_per_ray": cfg.S, "grid": ("triplane" if cfg.kind == wl.TRIPLANE else "voxel"),
             "grid_res": cfg.res, "K": cfg.K, "mlp": "->".join(map(str, cfg.widths)),
-            "parallelism": f"dp{n} (rays sharded, grad all-reduce)",
+            "parallelism": f"dp{n} (rays sharded, grad all-reduce)", "ray_order": cfg.ray_order,
             "l2": "inputs larger than L2 (rays + upstream grads per step > 126 MB); theta stays L2-resident "
                   "by design (steady-state training)"}
 
@@ -316,7 +335,7 @@ def run_ours(args):
     import paper_2404_19760_b200 as lpb
     from paper_2404_19760_b200.dist import FlatGrads, allreduce_grads, shard_range
 
-    cfg = wl.get_config(args.config)
+    cfg = bench_config(args)
     if args.l2_persist > 0:
         lpb.set_l2_persist(args.l2_persist)
     M_all = cfg.n_rays
@@ -458,7 +477,7 @@ def run_ours(args):
     line = {
         "metric": "rays/s fwd+bwd", "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(cfg, world),
+        "vs_baseline": None, "dtype": DTYPE_RENDER, "data": "synthetic", "config": config_dict(cfg, world),
         "breakdown_ms": {"fwd": t_fwd, "bwd": t_bwd, "allreduce": t_ar},
         "peak_bytes_per_ray": bytes_per_ray,
         "roofline": {"bound": "l2_atomic", "kernel": kname[1],
@@ -547,7 +566,7 @@ def run_splat(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev = init_device_and_group(torch, dist, local, world)
-    cfg = wl.get_config(args.config)
+    cfg = bench_config(args)
     lo, hi = shard_range(cfg.n_rays, rank, world)
     M, S = hi - lo, cfg.S
     grid = lpb.SplatGrid(cfg.kind, (cfg.res,) * 3, cfg.K, cfg.contraction, cfg.contract_a)
@@ -639,7 +658,7 @@ def run_splat(args):
     line = {
         "metric": "rays/s splat fwd+bwd" + (" (g_s)" if gs is not None else ""), "value": cfg.n_rays / (ms / 1000.0), "unit": "rays/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE_SPLAT if cfg.splat_mlp else "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.note}", "rays": cfg.n_rays, "samples_per_ray": S,
                    "grid": "triplane" if cfg.kind == wl.TRIPLANE else "voxel", "grid_res": cfg.res, "K": cfg.K,
                    "parallelism": f"dp{world} (rays sharded, grid all-reduce)",

@@ -57,3 +57,23 @@ def test_tiled_pixel_order_is_a_permutation():
         assert r.min() == 0 and r.max() == img - 1 and c.max() == img - 1
     r, c = wl.pixel_of(np.arange(32), 256)     # first warp = 8x4 block
     assert set(r.tolist()) == {0, 1, 2, 3} and set(c.tolist()) == set(range(8))
+
+
+def test_ray_orders_are_permutations_of_the_same_rays():
+    """raster / shuffled orders (bench --ray-order) reorder the tiled batch's rays:
+    same multiset of (origin, direction, near, far); the shuffle is a bijection."""
+    n = 4096
+    for m in (100, n, 8388608):
+        x = wl._feistel_permute(np.arange(min(m, 1 << 16)), m)
+        assert len(np.unique(x)) == len(x) and x.min() >= 0 and x.max() < m
+    x = wl._feistel_permute(np.arange(n), n)
+    assert sorted(x.tolist()) == list(range(n)) and not np.array_equal(x, np.arange(n))
+    key = lambda r: sorted(map(tuple, np.concatenate([r[0], r[1], r[2][:, None], r[3][:, None]], 1).tolist()))
+    ref = key(wl.make_rays(wl.get_config("c1")))
+    for order in ("raster", "shuffled"):
+        c = wl.get_config("c1", ray_order=order)
+        rays = wl.make_rays(c)
+        assert key(rays) == ref, order
+        if order == "shuffled":   # any subset maps independently (no table)
+            sub = wl.make_rays(c, idx=np.array([5, 77, 4000]))
+            assert np.array_equal(sub[1], rays[1][[5, 77, 4000]])

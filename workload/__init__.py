@@ -95,6 +95,9 @@ class Config:
     op: str = "render"        # "render" (the renderer) or "splat" (the Splatter: widths unused)
     dir_freqs: int = 0        # F > 0: view-dependent colour, g_sigma(h) and g_v(h, direnc(d))
     splat_mlp: bool = False   # Splatter with g_s (Eq. 2): prior grid + MLP (dir_freqs = F of its direnc)
+    ray_order: str = "tiled"  # order of the global ray index: "tiled" (pixel_of), "raster" (per view),
+                              # "shuffled" (a seeded permutation of every ray of every view: NeRF-style
+                              # random ray batches)
 
     @property
     def n_rays(self) -> int:
@@ -285,6 +288,33 @@ def pixel_of(pix: np.ndarray, img: int):
     return row, col
 
 
+def _feistel_permute(idx: np.ndarray, n: int, seed: int = 6, rounds: int = 4) -> np.ndarray:
+    """A seeded bijection of [0, n): a balanced Feistel network on the smallest even
+    power-of-two domain >= n with splitmix64 round functions, cycle-walked back
+    into [0, n). Any subset of indices maps independently (no table)."""
+    bits = max(2, int(n - 1).bit_length())
+    bits += bits & 1
+    half = bits // 2
+    mask = np.uint64((1 << half) - 1)
+    with np.errstate(over="ignore"):
+        keys = [_mix64(np.uint64(seed) * _GOLDEN + np.uint64(r + 1) * _C1) for r in range(rounds)]
+
+    def perm(x):
+        lo, hi = x & mask, x >> np.uint64(half)
+        for k in keys:
+            with np.errstate(over="ignore"):
+                f = _mix64(lo ^ k) & mask
+            lo, hi = hi ^ f, lo
+        return (hi << np.uint64(half)) | lo
+
+    x = np.asarray(idx, dtype=np.uint64).copy()
+    todo = np.ones(x.shape, dtype=bool)
+    while todo.any():
+        x[todo] = perm(x[todo])
+        todo = x >= np.uint64(n)
+    return x.astype(np.int64)
+
+
 def make_rays(cfg: Config, idx: Optional[np.ndarray] = None, start: int = 0,
               count: Optional[int] = None, fov_deg: float = 30.0, margin: float = 1e-4):
     """Rays for global ray indices `idx` (or the contiguous range [start, start+count)).
@@ -296,10 +326,15 @@ def make_rays(cfg: Config, idx: Optional[np.ndarray] = None, start: int = 0,
             count = cfg.n_rays - start
         idx = np.arange(start, start + count, dtype=np.int64)
     idx = np.asarray(idx, dtype=np.int64)
+    if cfg.ray_order == "shuffled":
+        idx = _feistel_permute(idx, cfg.n_rays)
     npix = cfg.img * cfg.img
     view = idx // npix
     pix = idx % npix
-    row, col = pixel_of(pix, cfg.img)
+    if cfg.ray_order == "tiled":
+        row, col = pixel_of(pix, cfg.img)
+    else:
+        row, col = pix // cfg.img, pix % cfg.img
     row = row.astype(np.float64)
     col = col.astype(np.float64)
     f = cfg.img / (2.0 * math.tan(math.radians(fov_deg) / 2.0))
