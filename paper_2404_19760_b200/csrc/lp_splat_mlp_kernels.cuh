@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256 + 32 * kSplatScatterWarps, 1) lp_splat_mlp
   if (threadIdx.x == 0) {
     tc::mbar_init(bar, 1);
     tc::mbar_init(bar_st, 256);
-    tc::mbar_init(bar_dr, SW > 0 ? SW : 1);
+    tc::mbar_init(bar_dr, SW > 0 ? 32 * SW : 1);
   }
   if (threadIdx.x < 32) tc::tmem_alloc(tslot, 128);
   tc::fence_async_smem();
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256 + 32 * kSplatScatterWarps, 1) lp_splat_mlp
           ph ^= 1;
           for (int rb = sw; rb < 4; rb += SW) coop_scatter<KIND, kGsK>(sth, ptaps, s.dims, dhs, rb * 32, sl, 0, kGsK / 4, swt);
           __syncwarp();
-          if (sl == 0) tc::mbar_arrive(bar_dr);
+          tc::mbar_arrive(bar_dr);   // every lane: its own reads of the staging precede it
         }
     }
   }
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(256 + 32 * kSplatBwdScatterWarps, 1) lp_splat_
   if (threadIdx.x == 0) {
     tc::mbar_init(bar, 1);
     tc::mbar_init(bar_st, 256);
-    tc::mbar_init(bar_dr, SW > 0 ? SW : 1);
+    tc::mbar_init(bar_dr, SW > 0 ? 32 * SW : 1);
   }
   if (threadIdx.x < 32) tc::tmem_alloc(tslot, 256);
   if (threadIdx.x >= 256) {
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(256 + 32 * kSplatBwdScatterWarps, 1) lp_splat_
           ph ^= 1;
           for (int rb = sw; rb < 4; rb += SW) coop_scatter<KIND, kGsKp>(sgp, ptaps, s.dims, dhs, rb * 32, sl);
           __syncwarp();
-          if (sl == 0) tc::mbar_arrive(bar_dr);
+          tc::mbar_arrive(bar_dr);   // every lane: its own reads of the staging precede it
         }
     }
   }

@@ -64,6 +64,16 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// Same with the A operand in tensor memory (M = 128 lanes = rows, bf16 K pairs packed per
+// 32-bit column: K-step ks of 16 elements = 8 columns); probed: scripts/tc_probe3.cu.
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -131,6 +141,20 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[N]) {
 }
 #undef LP_TMEM_LD8
 
+// registers -> TMEM: lane = row of the warp's 32-lane quarter, N consecutive 32-bit columns.
+// The caller issues tmem_wait_st() (or to_tensor_core-style fences) before the MMA reads them.
+template <int N>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[N]) {
+  static_assert(N % 8 == 0, "TMEM store width");
+#pragma unroll
+  for (int i = 0; i < N; i += 8)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + (uint32_t)i),
+                 "r"(r[i + 0]), "r"(r[i + 1]), "r"(r[i + 2]), "r"(r[i + 3]), "r"(r[i + 4]), "r"(r[i + 5]),
+                 "r"(r[i + 6]), "r"(r[i + 7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // ---------------------------------------------------------------- bf16 pieces
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // .x = a (low half), .y = b
@@ -163,6 +187,20 @@ __device__ __forceinline__ void store8(uint8_t* base, uint32_t piece_stride, int
 #pragma unroll
   for (int i = 0; i < NP; ++i)
     *reinterpret_cast<uint4*>(base + i * piece_stride + off) = make_uint4(p0[i], p1[i], p2[i], p3[i]);
+}
+// 3-piece split of 8 consecutive values: pieces 0 and 1 stored like store8<2>, piece 2
+// returned as 4 packed bf16x2 words (for a TMEM-resident copy of the last piece).
+__device__ __forceinline__ void store8_split3(uint8_t* base, uint32_t piece_stride, int r, int c0, int C,
+                                              const float* v, uint32_t* p2) {
+  uint32_t q[4][3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) split_pair<3>(v[2 * i], v[2 * i + 1], q[i]);
+  const uint32_t off = cm_off(r, c0, C);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+    *reinterpret_cast<uint4*>(base + i * piece_stride + off) = make_uint4(q[0][i], q[1][i], q[2][i], q[3][i]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) p2[i] = q[i][2];
 }
 // Same for 4 consecutive values (c0 % 4 == 0): 8-byte stores.
 template <int NP>

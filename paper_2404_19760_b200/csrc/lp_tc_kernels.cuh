@@ -182,9 +182,6 @@ __device__ __forceinline__ int ray_slot(int rt) {
   }
 }
 
-#ifndef LP_SCATTER_UNIFORM  // coop_scatter: one reduction per line when all rays of an instruction share a cell
-#define LP_SCATTER_UNIFORM 0
-#endif
 
 // Warp-cooperative gather of the warp's 32 rays: lane = (ray RPI-subgroup, chunk).
 // Writes h into rows [row0, row0 + 32) of the H tile (NP bf16 pieces).
@@ -287,30 +284,6 @@ __device__ __forceinline__ void coop_scatter(float* const* gplanes, const float4
 #pragma unroll
     for (int p = 0; p < NPL; ++p) {
       const float4 rec = taps[row * NPL + p];
-#if LP_SCATTER_UNIFORM
-      if (!wplanes) {   // N1 experiment: all RPI rays of this instruction in one cell -> reduce once
-        const int base = __float_as_int(rec.x);
-        if (__all_sync(0xffffffffu, base >= 0 && base == __shfl_sync(0xffffffffu, base, 0))) {
-          Corners<KIND, K> c;
-          record_corners<KIND, K>(rec, p, g, c);
-          float* pl = gplanes[p] + 4 * ch;
-#pragma unroll
-          for (int cc = 0; cc < Corners<KIND, K>::N; ++cc) {
-            const float w = c.w[cc];
-            float4 v = make_float4(w * d.x, w * d.y, w * d.z, w * d.w);
-#pragma unroll
-            for (int off = KC; off < 32; off <<= 1) {   // sum over the rays (lanes of equal chunk)
-              v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
-              v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
-              v.z += __shfl_xor_sync(0xffffffffu, v.z, off);
-              v.w += __shfl_xor_sync(0xffffffffu, v.w, off);
-            }
-            if (sub == 0) atomicAdd(reinterpret_cast<float4*>(pl + c.off[cc]), v);
-          }
-          continue;
-        }
-      }
-#endif
       if (__float_as_int(rec.x) < 0) continue;
       Corners<KIND, K> c;
       record_corners<KIND, K>(rec, p, g, c);
@@ -580,7 +553,7 @@ __global__ void __launch_bounds__(128 * T * G + 32 * bwd_scatter_warps<T>(), 1) 
   stage_tc_weights<K, HID, S::KP>(w0p, fp, a.params);
   // per group: Z done, dH/dW done (tcgen05.commit), staged (128 compute threads),
   // drained (the group's scatter warps)
-  if (threadIdx.x < 4 * G) tc::mbar_init(&bars[threadIdx.x], threadIdx.x % 4 == 2 ? 128 : threadIdx.x % 4 == 3 ? (SWG > 0 ? SWG : 1) : 1);
+  if (threadIdx.x < 4 * G) tc::mbar_init(&bars[threadIdx.x], threadIdx.x % 4 == 2 ? 128 : threadIdx.x % 4 == 3 ? (SWG > 0 ? 32 * SWG : 1) : 1);
   if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
   tc::fence_async_smem();
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -603,7 +576,7 @@ __global__ void __launch_bounds__(128 * T * G + 32 * bwd_scatter_warps<T>(), 1) 
           ph ^= 1;
           for (int rb = part; rb < 4; rb += SWG) coop_scatter<KIND, K>(sgpl, sptaps, a.dims, sdhs, rb * 32, lane);
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&bars[4 * sg + 3]);
+          tc::mbar_arrive(&bars[4 * sg + 3]);   // every lane: its own reads of the staging precede it
         }
     }
   }

@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwdvScatterWarps, 1) lp_bwd_tcv_ke
   if (threadIdx.x == 0) {
     tc::mbar_init(bar, 1);
     tc::mbar_init(bar_st, 256);
-    tc::mbar_init(bar_dr, SW > 0 ? SW : 1);
+    tc::mbar_init(bar_dr, SW > 0 ? 32 * SW : 1);
   }
   if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
   if (hf == 0) *reinterpret_cast<__nv_bfloat16*>(Ht + tc::cm_off(rt, KV, HCB)) = __float2bfloat16_rn(1.0f);
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwdvScatterWarps, 1) lp_bwd_tcv_ke
           ph ^= 1;
           for (int rb = sw; rb < 4; rb += SW) coop_scatter<KIND, K>(sgpl, ptaps, a.dims, dhs, rb * 32, sl);
           __syncwarp();
-          if (sl == 0) tc::mbar_arrive(bar_dr);
+          tc::mbar_arrive(bar_dr);   // every lane: its own reads of the staging precede it
         }
     }
   }

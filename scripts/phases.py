@@ -28,8 +28,15 @@ v = np.array(list(buf), dtype=np.float64).reshape(2, 8)
 names = [["taps", "gather", "bar", "mma-issue", "mma-wait", "epilogue", "-", "-"],
          ["taps", "gather", "bar1", "mma1-wait", "epilogue", "bar2+mma2-wait", "scatter", "drained-wait"]]
 if len(cfg.widths) == 4 and not cfg.dir_freqs:   # K2tc2 (lp_tc2_kernels.cuh LP_PT slots)
-    names[1] = ["taps", "gather", "bar+Z1-wait", "epilogues", "bar+MMA2/3/4-wait", "-", "-", "drained-wait"]
+    # lp_bwd_tc2p_kernel: slots 0-1 producer warps, 2-7 compute warps
+    names[1] = ["prod:empty-wait", "prod:taps+gather", "full+Z1-wait", "epilogues", "bar+MMA2/3/4-wait", "-", "-",
+                "drained-wait"]
 for k, nm in enumerate(("fwd", "bwd")):
-    tot = v[k].sum()
-    print(nm, f"{(e0.elapsed_time(e1) if k == 0 else e1.elapsed_time(e2)):.2f} ms",
-          " ".join(f"{names[k][i]}={v[k][i] / tot * 100:.1f}%" for i in range(8) if v[k][i] > 0))
+    groups = [range(8)]
+    if names[k][0].startswith("prod"):   # producer and compute warps: shares of each role's own time
+        groups = [range(2), range(2, 8)]
+    parts = []
+    for g in groups:
+        tot = sum(v[k][i] for i in g)
+        parts += [f"{names[k][i]}={v[k][i] / tot * 100:.1f}%" for i in g if v[k][i] > 0]
+    print(nm, f"{(e0.elapsed_time(e1) if k == 0 else e1.elapsed_time(e2)):.2f} ms", " ".join(parts))
