@@ -42,6 +42,15 @@ L2_RED_GBS = 6070.0
 L2_RED_GBS_BY_GRAN = {128: 6070.0, 64: 4900.0, 32: 3560.0}
 
 
+# Measured line-gather ceilings of the forward's load side (scripts/red_bench.cu gather mode,
+# profiles/r2/measurements_n1_n2_rayorder_redbench.txt): 8 lanes x LDG.128 per 128-B line, 4 lines
+# per warp instruction, 4 in flight per lane, full occupancy. Lines drawn from a 16-line window per
+# warp (every load hits L1): 164 G lines/s = 21.05 TB/s, the ceiling used for K1tc's fraction;
+# random lines over a 24 MB L2-resident buffer (L1 misses served by L2): 17.67 TB/s.
+GATHER_L1_GBS = 21050.0
+GATHER_L2_GBS = 17670.0
+
+
 def red_peak_gbs(K: int) -> float:
     return L2_RED_GBS_BY_GRAN.get(4 * K, L2_RED_GBS)
 
@@ -500,9 +509,14 @@ def run_ours(args):
                              if traffic else None,
                              "peak_gbs": float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS)),
                              "peak_source": f"MEASURED_PEAKS.json ({peak_src}); traffic from profiles/ncu_traffic.json"},
-                     "fwd_kernel": {"kernel": kname[0],
-                                    "achieved_tflops": fwd_f * samples / (t_fwd / 1000.0) / 1e12,
-                                    "alu_frac": fwd_f * samples / (t_fwd / 1000.0) / 1e12 / alu_peak}},
+                     "fwd_kernel": {"kernel": kname[0], "bound": "gather (L1/L2 line loads)",
+                                    "achieved": red_b * samples / (t_fwd / 1000.0) / 1e9, "unit": "GB/s",
+                                    "peak": GATHER_L1_GBS, "frac": red_b * samples / (t_fwd / 1000.0) / 1e9 / GATHER_L1_GBS,
+                                    "frac_of_l2_random_line_gather": red_b * samples / (t_fwd / 1000.0) / 1e9 / GATHER_L2_GBS,
+                                    "algorithmic": f"{red_b} B of corner vectors gathered per sample (corners x K x 4)",
+                                    "peak_source": "measured: scripts/red_bench.cu gather mode, 128-B lines from a "
+                                                   "16-line window per warp (L1 hits) 21.05 TB/s; random lines of a "
+                                                   "24 MB buffer (L2) 17.67 TB/s"}},
         "clocks": clk_sum,
         "gpu_launches": 2 * args.steps,
     }

@@ -51,6 +51,14 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int C, int ks) {
   return sdesc(base + (uint32_t)ks * 2u * (uint32_t)(C >> 3) * 128u, (uint32_t)(C >> 3) * 128u, 128u);
 }
 
+// Precomputed descriptors: the K-major / MN-major view of a tile at `base`, moved by a byte
+// offset with one add (the start-address field holds addr >> 4 in its low 14 bits, and
+// shared-memory offsets stay below 256 KB, so the add never carries out of the field).
+// K-step ks: +ks * 256 B (K-major), +ks * 2 (C / 8) * 128 B (MN-major).
+__device__ __forceinline__ uint64_t kdesc0(uint32_t base, int C) { return sdesc(base, 128u, (uint32_t)(C >> 3) * 128u); }
+__device__ __forceinline__ uint64_t mdesc0(uint32_t base, int C) { return sdesc(base, (uint32_t)(C >> 3) * 128u, 128u); }
+__device__ __forceinline__ uint64_t dplus(uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); }
+
 // Instruction descriptor: kind::f16, A/B = BF16, D = F32.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |

@@ -667,6 +667,31 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
   }
 }
 
+#ifndef LP_PT_ROLES   // phase timers per role of lp_bwd_tc2p_kernel: 1 compute, 2 producers, 4 scatter
+#define LP_PT_ROLES 7
+#endif
+#define LP_PT_ROLE(bit, x) \
+  if constexpr ((LP_PT_ROLES & (bit)) != 0) { x; }
+#ifndef LP_PHASES
+// Without the debug timers the compute role still reads the clock at its phase boundaries and
+// accumulates the deltas (kept alive by a store that is never taken). Measured, not derived:
+// ptxas schedules the epilogues around these reads better -- c4p backward 509 -> 472 ms, cu
+// 196 -> 190 ms; bare clock reads without the arithmetic give 486 ms, compiler-only barriers
+// (asm volatile("" ::: "memory")) 508 ms.
+#define LP_PTC_DECL unsigned long long lpk_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long lpk_t = clock64();
+#define LP_PTC(i) { long long now_ = clock64(); lpk_acc[i] += (unsigned long long)(now_ - lpk_t); lpk_t = now_; }
+#define LP_PTC_KEEP_FLUSH if (a.M < 0) for (int i_ = 0; i_ < 8; ++i_) a.tau[i_] = (float)lpk_acc[i_];
+#else
+#define LP_PTC_DECL
+#define LP_PTC(i) LP_PT_ROLE(1, LP_PT(i))
+#define LP_PTC_KEEP_FLUSH
+#endif
+#define LP_PTP(i) LP_PT_ROLE(2, LP_PT(i))
+#define LP_PTS(i) LP_PT_ROLE(4, LP_PT(i))
+#define LP_PTC_FLUSH(k) LP_PT_ROLE(1, LP_PT_FLUSH(k))
+#define LP_PTP_FLUSH(k) LP_PT_ROLE(2, LP_PT_FLUSH(k))
+#define LP_PTS_FLUSH(k) LP_PT_ROLE(4, LP_PT_FLUSH(k))
+
 // ================================================================= K2tc2 backward, warp-specialised
 // Same arithmetic as lp_bwd_tc2_kernel, with the recompute's taps + cooperative gather (B2/F3)
 // taken out of the compute warps' chain: four producer warps march one step ahead into a
@@ -755,6 +780,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
   const int R = a.S - 1;
   const int64_t ntiles = (a.M + 127) / 128;
   LP_PT_DECL
+  LP_PTC_DECL
 
   if (threadIdx.x >= 384) {   // ---- scatter warps: B6 of every staged step
     const int sw = (threadIdx.x - 384) / 32, sl = threadIdx.x & 31;
@@ -764,6 +790,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
       for (int q = 0; q < a.S; ++q, ++n) {
         const int b = n & 1;
         tc::mbar_wait(&staged[b], (n >> 1) & 1);
+        LP_PTS(2)
         const float4* staps = reinterpret_cast<const float4*>(smem + L::TAPS + b * L::T::TAPS);
         const float* dhs = reinterpret_cast<const float*>(smem + L::H + b * 3 * L::HP_PIECE);
 #ifndef LP_ABL_NOSCATTER
@@ -771,7 +798,9 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
 #endif
         __syncwarp();
         tc::mbar_arrive(&empty[b]);   // every lane: its own reads of the staging / taps precede it
+        LP_PTS(3)
       }
+    LP_PTS_FLUSH(0)
   } else if (threadIdx.x >= 256) {   // ---- producers: taps + cooperative gather, one step ahead
     const int pw = (threadIdx.x - 256) >> 5, lane = threadIdx.x & 31, row = pw * 32 + lane;
     const float* planes[3] = {a.grid[0], a.grid[1], a.grid[2]};
@@ -784,7 +813,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
         float4* taps = reinterpret_cast<float4*>(smem + L::TAPS + b * L::T::TAPS);
         uint8_t* Hb = smem + L::H + b * 3 * L::HP_PIECE;
         tc::mbar_wait(&empty[b], ((n >> 1) & 1) ^ 1);
-        LP_PT(0)
+        LP_PTP(0)
         {   // the staging of step n - 2 overwrote pieces 0-1: restore this row's columns [KP, KP + 8)
           const uint32_t off = tc::cm_off(row, KP, HCP);
           *reinterpret_cast<uint4*>(Hb + off) = make_uint4(0x3F80u, 0u, 0u, 0u);   // bf16 1.0, then zeros
@@ -797,10 +826,10 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
         coop_gather<KIND, K, HCP, 3, false, true, LP_TC2P_UNROLL>(planes, taps, a.dims, Hb, L::HP_PIECE, pw * 32, lane);
         tc::fence_async_smem();
         tc::mbar_arrive(&full[b]);
-        LP_PT(1)
+        LP_PTP(1)
       }
     }
-    LP_PT_FLUSH(1)
+    LP_PTP_FLUSH(0)
   } else {   // ---- compute warps
     const int gt = threadIdx.x, hf = gt >> 7, rt = gt & 127, wq = (gt >> 5) & 3;
     const uint32_t tbase = *tslot;
@@ -817,6 +846,13 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
     const uint32_t h_addr = tc::smem_u32(smem + L::H), a1_addr = tc::smem_u32(A1t), d_addr = tc::smem_u32(Dt);
     const uint32_t w0_addr = tc::smem_u32(w0p), w1_addr = tc::smem_u32(w1p);
     constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
+    // base descriptors (the issuing thread adds compile-time piece / K-step offsets)
+    const uint64_t kH = tc::kdesc0(h_addr, HCP), kW0 = tc::kdesc0(w0_addr, KP), kA1 = tc::kdesc0(a1_addr, HC1);
+    const uint64_t kW1 = tc::kdesc0(w1_addr, HID), kD = tc::kdesc0(d_addr, 2 * HID);
+    const uint64_t mW1 = tc::mdesc0(w1_addr, HID), mD = tc::mdesc0(d_addr, 2 * HID), mA1 = tc::mdesc0(a1_addr, HC1);
+    const uint64_t mW0 = tc::mdesc0(w0_addr, KP), mH = tc::mdesc0(h_addr, HCP);
+    constexpr uint32_t MSD = 2 * (2 * HID / 8) * 128, MSA1 = 2 * (HC1 / 8) * 128, MSW1 = 2 * (HID / 8) * 128;
+    constexpr uint32_t MSW0 = 2 * (KP / 8) * 128, MSH = 2 * (HCP / 8) * 128;   // MN-major K-step bytes
     uint32_t phase = 0, wacc = 0, wacc0 = 0, n = 0;
     float dbo[kOut] = {0.0f, 0.0f, 0.0f, 0.0f};
     const float* b0 = fp + F::B0 + hf * HH;
@@ -853,16 +889,23 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
 
       for (int q = R; q >= 0; --q, ++n) {
         const int b = n & 1;
-        const uint32_t hb_addr = h_addr + (uint32_t)(b * 3) * L::HP_PIECE;
+        const uint64_t kHb = tc::dplus(kH, (uint32_t)(b * 3) * L::HP_PIECE);
+        const uint64_t mHb = tc::dplus(mH, (uint32_t)(b * 3) * L::HP_PIECE);
         // ---- B2: Z1 = H W0^T on the producers' H tile of this step
         if (gt == 0) {
           tc::mbar_wait(&full[b], (n >> 1) & 1);
           tc::fence_after_sync();
-          mma_split6(tS0, hb_addr, L::HP_PIECE, HCP, w0_addr, L::W0_PIECE, KP, KP / 16, id_z);
+          constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
+#pragma unroll
+          for (int ks = 0; ks < KP / 16; ++ks)
+#pragma unroll
+            for (int c = 0; c < 6; ++c)
+              tc::mma_bf16(tS0, tc::dplus(kHb, PA[c] * L::HP_PIECE + ks * 256), tc::dplus(kW0, PB[c] * L::W0_PIECE + ks * 256),
+                           id_z, (ks | c) != 0);
           tc::mma_commit(bar);
         }
         mma_done();
-        LP_PT(2)
+        LP_PTC(2)
         uint32_t mask1 = 0;   // ReLU'(z1) of this half's hidden units
         {
           float z[HH];
@@ -882,7 +925,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
           tc::tmem_st<HH / 2>(tA2 + tq + (uint32_t)(hf * HH / 2), p2);   // piece 2 of a1 -> TMEM
           tc::tmem_wait_st();
         }
-        LP_PT(3)
+        LP_PTC(3)
         to_tensor_core();
         if (gt == 0) {   // Z2 = A1 W1^T: pieces 0, 1 of A1 from shared memory, piece 2 from TMEM
           tc::fence_after_sync();
@@ -891,16 +934,16 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
           for (int ks = 0; ks < HID / 16; ++ks)
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
-              const uint64_t bd = tc::desc_kmajor(w1_addr + PB[c] * L::W1_PIECE, HID, ks);
+              const uint64_t bd = tc::dplus(kW1, PB[c] * L::W1_PIECE + ks * 256);
               if (PA[c] < 2)
-                tc::mma_bf16(tS1, tc::desc_kmajor(a1_addr + PA[c] * L::A1_PIECE, HC1, ks), bd, id_z, (ks | c) != 0);
+                tc::mma_bf16(tS1, tc::dplus(kA1, PA[c] * L::A1_PIECE + ks * 256), bd, id_z, (ks | c) != 0);
               else
                 tc::mma_bf16_ts(tS1, tA2 + (uint32_t)(ks * 8), bd, id_z, 1);
             }
           tc::mma_commit(bar);
         }
         mma_done();
-        LP_PT(4)
+        LP_PTC(4)
         float a2[HH];
         {
           tc::tmem_ld<HH>(tS1 + tq + hf * HH, a2);
@@ -971,7 +1014,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
           tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, 2 * HID, d2);
           tc::store8<2>(Dt, L::DP, rt, HID + hf * HH + 8 * c, 2 * HID, a2 + 8 * c);
         }
-        LP_PT(3)
+        LP_PTC(3)
         to_tensor_core();
         if (gt == 0) {
           tc::fence_after_sync();
@@ -980,21 +1023,21 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
           for (int ks = 0; ks < HID / 16; ++ks)
 #pragma unroll
             for (int c = 0; c < 3; ++c)
-              tc::mma_bf16(tS0, tc::desc_kmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
-                           tc::desc_mnmajor(w1_addr + QB[c] * L::W1_PIECE, HID, ks), id_da1, (ks | c) != 0);
+              tc::mma_bf16(tS0, tc::dplus(kD, QA[c] * L::DP + ks * 256), tc::dplus(mW1, QB[c] * L::W1_PIECE + ks * MSW1),
+                           id_da1, (ks | c) != 0);
           // [dW1 db1 . ; . . dWo^T] += [D2 | A2]^T [A1 | 1 | DOUT]   (K = the 128 samples of this step)
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-              tc::mma_bf16(tW1, tc::desc_mnmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
-                           tc::desc_mnmajor(a1_addr + QB[c] * L::A1_PIECE, HC1, ks), id_w1, wacc);
+              tc::mma_bf16(tW1, tc::dplus(mD, QA[c] * L::DP + ks * MSD), tc::dplus(mA1, QB[c] * L::A1_PIECE + ks * MSA1),
+                           id_w1, wacc);
               wacc = 1;
             }
           tc::mma_commit(bar);
         }
         mma_done();
-        LP_PT(4)
+        LP_PTC(4)
         {   // delta1 = ReLU'(z1) dA1 -> D1 (over D2, consumed)
           float da[HH];
           tc::tmem_ld<HH>(tS0 + tq + hf * HH, da);
@@ -1006,7 +1049,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
             tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, 2 * HID, d1);
           }
         }
-        LP_PT(3)
+        LP_PTC(3)
         to_tensor_core();
         if (gt == 0) {
           tc::fence_after_sync();
@@ -1015,20 +1058,20 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
           for (int ks = 0; ks < HID / 16; ++ks)
 #pragma unroll
             for (int c = 0; c < 3; ++c)
-              tc::mma_bf16(tS1, tc::desc_kmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
-                           tc::desc_mnmajor(w0_addr + QB[c] * L::W0_PIECE, KP, ks), id_dh, (ks | c) != 0);
+              tc::mma_bf16(tS1, tc::dplus(kD, QA[c] * L::DP + ks * 256), tc::dplus(mW0, QB[c] * L::W0_PIECE + ks * MSW0),
+                           id_dh, (ks | c) != 0);
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-              tc::mma_bf16(tW0, tc::desc_mnmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
-                           tc::desc_mnmajor(hb_addr + QB[c] * L::HP_PIECE, HCP, ks), id_w0, wacc0);
+              tc::mma_bf16(tW0, tc::dplus(mD, QA[c] * L::DP + ks * MSD), tc::dplus(mHb, QB[c] * L::HP_PIECE + ks * MSH),
+                           id_w0, wacc0);
               wacc0 = 1;
             }
           tc::mma_commit(bar);
         }
         mma_done();
-        LP_PT(4)
+        LP_PTC(4)
         // ---- B6: this half's dH channels -> fp32 staging over H[b] (Z1, dW0 are done with it)
         {
           float* dhs_b = reinterpret_cast<float*>(smem + L::H + b * 3 * L::HP_PIECE);
@@ -1044,10 +1087,11 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
         tc::mbar_arrive(&staged[b]);
         tc::fence_before_sync();
         tc::named_bar(1, 256);
-        LP_PT(3)
+        LP_PTC(3)
       }
     }
-    LP_PT_FLUSH(1)
+    LP_PTC_FLUSH(1)
+    LP_PTC_KEEP_FLUSH
 
     // ---- B7: flush the gradient partials (TMEM accumulators + register bias sums)
     tc::fence_after_sync();

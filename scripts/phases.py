@@ -28,13 +28,14 @@ v = np.array(list(buf), dtype=np.float64).reshape(2, 8)
 names = [["taps", "gather", "bar", "mma-issue", "mma-wait", "epilogue", "-", "-"],
          ["taps", "gather", "bar1", "mma1-wait", "epilogue", "bar2+mma2-wait", "scatter", "drained-wait"]]
 if len(cfg.widths) == 4 and not cfg.dir_freqs:   # K2tc2 (lp_tc2_kernels.cuh LP_PT slots)
-    # lp_bwd_tc2p_kernel: slots 0-1 producer warps, 2-7 compute warps
-    names[1] = ["prod:empty-wait", "prod:taps+gather", "full+Z1-wait", "epilogues", "bar+MMA2/3/4-wait", "-", "-",
-                "drained-wait"]
+    # lp_bwd_tc2p_kernel: kernel-0 slots = producer (0-1) and scatter (2-3) warps (K1tc2 has no
+    # timers), kernel-1 slots = compute warps
+    names[0] = ["prod:empty-wait", "prod:taps+gather", "scat:staged-wait", "scat:reduce", "-", "-", "-", "-"]
+    names[1] = ["-", "-", "full+Z1-wait", "epilogues", "bar+MMA2/3/4-wait", "-", "-", "-"]
 for k, nm in enumerate(("fwd", "bwd")):
     groups = [range(8)]
-    if names[k][0].startswith("prod"):   # producer and compute warps: shares of each role's own time
-        groups = [range(2), range(2, 8)]
+    if names[k][0].startswith("prod"):   # producer and scatter warps: shares of each role's own time
+        groups = [range(2), range(2, 4)]
     parts = []
     for g in groups:
         tot = sum(v[k][i] for i in g)
