@@ -59,9 +59,6 @@ inline bool force_fma() {
 #ifndef LP_FWD2_GROUPS
 #define LP_FWD2_GROUPS 2
 #endif
-#ifndef LP_TC2_PRODUCER   // K2tc2 with producer warps for the gather (lp_bwd_tc2p_kernel)
-#define LP_TC2_PRODUCER 1
-#endif
 #ifndef LP_BWD_GROUPS
 #define LP_BWD_GROUPS 2
 #endif
@@ -103,13 +100,8 @@ lp_status run_bwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
   if constexpr (NH == 2 && HID == 64 && K >= 8) {
     if (!force_fma()) {
       static LaunchShape shape;
-#if LP_TC2_PRODUCER
       return launch(lp::lp_bwd_tc2p_kernel<KIND, K, HID>, shape, lp::Bwd2pSmem<KIND, K, HID>::BYTES,
                     256 + 128 + 32 * lp::kBwd2ScatterWarps, 1, a.M, a, w, s);
-#else
-      return launch(lp::lp_bwd_tc2_kernel<KIND, K, HID>, shape, lp::Bwd2Smem<KIND, K, HID>::BYTES,
-                    256 + 32 * lp::kBwd2ScatterWarps, 1, a.M, a, w, s);
-#endif
     }
   }
   static LaunchShape shape;

@@ -11,10 +11,11 @@
 // halves exchange the 4 partial output-layer sums through shared memory and
 // then both hold the (identical) per-ray EA state. Per step:
 //   forward   gather H | Z1 = H W0^T | a1 -> A1 tile | Z2 = A1 W1^T | a2, o, heads, EA
-//   backward  gather H (+ scatter of step q+1) | Z1 | a1 -> A1 | Z2 | a2, o, heads, Eq. 3,
-//             [delta2 | a2] -> DA tile, dL/do -> A1 tile |
+//   backward  (producer warps: taps + gather H of the next step) | Z1 | a1 -> A1 | Z2 | a2, o,
+//             heads, Eq. 3, [delta2 | a2] -> D tile, dL/do -> A1 tile |
 //             dA1 = D2 W1, [dW1 db1 . ; . . dWo^T] += [D2 | A2]^T [A1 | 1 | DO] | delta1 -> D1 |
-//             dH = D1 W0, dW0|db0 += D1^T [H|1] | dH -> fp32 staging (scattered next step)
+//             dH = D1 W0, dW0|db0 += D1^T [H|1] | dH -> fp32 staging over the consumed H tile
+//             (reduced by the scatter warps during the next step)
 // Precision as in lp_tc.cuh: forward-type contractions (Z1, Z2) on 3 bf16 pieces
 // with 6 piece products (fp32-class), gradient contractions on 2 pieces with 3
 // products.
@@ -261,411 +262,11 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tc2_kernel(const KernelArgs
 }
 
 // ================================================================= K2tc2 backward
-template <int KIND, int K, int HID>
-struct Bwd2Smem : Tc2Shape<KIND, K, HID> {
-  using T = Tc2Shape<KIND, K, HID>;
-  static constexpr uint32_t A1_PIECE = 128 * T::HC1 * 2;
-  static constexpr uint32_t DP = 128 * 2 * HID * 2;
-  static constexpr uint32_t H = T::GRP;                          // [128][HC] x 3 (ones column at KP)
-  static constexpr uint32_t A1 = H + kTc2Pieces * T::HB_PIECE;   // [A1 | 1 | DO] [128][HC1] x 3; piece 2: ptaps
-  static constexpr uint32_t D = A1 + 3 * A1_PIECE;               // [D2 | A2] x 2, then D1, then fp32 dH
-  static constexpr uint32_t TAPS = D + 2 * DP;                   // [2 halves][128][NPL]
-  static constexpr uint32_t XO = TAPS + 2 * T::TAPS;             // [2 halves][128] float4
-  static constexpr uint32_t BAR = (XO + 2 * 128 * 16 + 127) & ~127u;   // MMA, tmem slot, staged, drained
-  static constexpr uint32_t BYTES = BAR + 32;
-  static constexpr uint32_t TMEM_COLS = 256;
-  static_assert(DP >= 128 * (K + 4) * 4, "dH staging fits the D region");
-  static_assert(A1_PIECE >= 128 * T::NPL * 16, "tap records fit A1 piece 2");
-};
-
-// TMEM columns: S0 [0,64) Z1 then dA1; S1 [64,128) Z2 then dH; W1 [128,208): M = 128
-// rows [D2 units | A2 units] x [A1 units | 1 | dout] (dW1, db1, dWo^T); [dW0|db0] [208,248)
-// kBwd2ScatterWarps dedicated warps issue each staged step's grid-gradient
-// reductions (as in K2tc); 0: fused into the next step's gather.
+// kBwd2ScatterWarps dedicated warps issue each staged step's grid-gradient reductions.
 #ifndef LP_BWD2_SW
 #define LP_BWD2_SW 4
 #endif
 constexpr int kBwd2ScatterWarps = LP_BWD2_SW;
-
-template <int KIND, int K, int HID>
-__global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_kernel(const KernelArgs a) {
-  using L = Bwd2Smem<KIND, K, HID>;
-  using F = Tc2Params<HID>;
-  using P = PackedParams<K, HID, 2>;
-  constexpr int HH = L::HH, KP = L::KP, HC = L::HC, HC1 = L::HC1, NPL = L::NPL, KC = K / 4;
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* w0p = smem + L::W0P;
-  uint8_t* w1p = smem + L::W1P;
-  float* fp = reinterpret_cast<float*>(smem + L::FP);
-  uint8_t* Ht = smem + L::H;
-  uint8_t* A1t = smem + L::A1;
-  uint8_t* Dt = smem + L::D;
-  float* dhs = reinterpret_cast<float*>(smem + L::D);
-  // previous step's tap records: A1 piece 2 (used only by the Z2 MMA; piece 0 holds the ones column)
-  float4* ptaps = reinterpret_cast<float4*>(smem + L::A1 + 2 * L::A1_PIECE);
-  float4* xo = reinterpret_cast<float4*>(smem + L::XO);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::BAR);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 8);
-  uint64_t* bar_st = reinterpret_cast<uint64_t*>(smem + L::BAR + 16);   // 256 compute threads
-  uint64_t* bar_dr = reinterpret_cast<uint64_t*>(smem + L::BAR + 24);   // the scatter warps
-  constexpr int SW = kBwd2ScatterWarps;
-  static_assert(SW == 0 || 4 % SW == 0, "scatter warps");
-
-  const int gt = threadIdx.x, hf = gt >> 7, rt = gt & 127, wq = (gt >> 5) & 3, lane = gt & 31;
-  float4* taps = reinterpret_cast<float4*>(smem + L::TAPS) + hf * 128 * NPL;
-
-  for (uint32_t i = threadIdx.x * 16; i < L::BAR; i += blockDim.x * 16)
-    *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
-  __syncthreads();
-  stage_tc2_weights<K, HID, KP>(w0p, w1p, fp, a.params);
-  if (threadIdx.x == 0) {
-    tc::mbar_init(bar, 1);
-    tc::mbar_init(bar_st, 256);
-    tc::mbar_init(bar_dr, SW > 0 ? 32 * SW : 1);
-  }
-  if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
-  // ones columns (piece 0 only; never overwritten): H[:, KP] -> db0, A1[:, HID] -> db1
-  if (threadIdx.x >= 256) {
-  } else if (hf == 0) *reinterpret_cast<__nv_bfloat16*>(Ht + tc::cm_off(rt, KP, HC)) = __float2bfloat16_rn(1.0f);
-  else *reinterpret_cast<__nv_bfloat16*>(A1t + tc::cm_off(rt, HID, HC1)) = __float2bfloat16_rn(1.0f);
-  tc::fence_async_smem();
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  if constexpr (SW > 0) {
-    if (threadIdx.x >= 256) {   // ---- scatter warps: B6 of every staged step
-      const int sw = (threadIdx.x - 256) / 32, sl = threadIdx.x & 31;
-      const float* sdhs = reinterpret_cast<const float*>(smem + L::D);
-      const float4* sptaps = reinterpret_cast<const float4*>(smem + L::A1 + 2 * L::A1_PIECE);
-      float* sgpl[3] = {a.ggrid[0], a.ggrid[1], a.ggrid[2]};
-      uint32_t ph = 0;
-      const int64_t nt = (a.M + 127) / 128;
-      for (int64_t tile = blockIdx.x; tile < nt; tile += gridDim.x)
-        for (int q = 0; q < a.S; ++q) {
-          tc::mbar_wait(bar_st, ph);
-          ph ^= 1;
-          for (int rb = sw; rb < 4; rb += SW) coop_scatter<KIND, K>(sgpl, sptaps, a.dims, sdhs, rb * 32, sl);
-          __syncwarp();
-          tc::mbar_arrive(bar_dr);   // every lane: its own reads of the staging precede it
-        }
-    }
-  }
-  if (SW == 0 || threadIdx.x < 256) {   // ---- compute warps
-    const uint32_t tbase = *tslot;
-    const uint32_t tS0 = tbase, tS1 = tbase + 64, tW1 = tbase + 128, tW0 = tbase + 208;
-    const uint32_t tq = (uint32_t)(wq * 32) << 16;
-    const int it0 = hf * (KC / 2), it1 = hf ? KC : KC / 2;
-
-    const int R = a.S - 1;
-    const float* planes[3] = {a.grid[0], a.grid[1], a.grid[2]};
-    float* gplanes[3] = {a.ggrid[0], a.ggrid[1], a.ggrid[2]};
-    float bg[kC];
-#pragma unroll
-    for (int c = 0; c < kC; ++c) bg[c] = a.bg ? __ldg(a.bg + c) : 0.0f;
-    const uint32_t id_z = tc::idesc_bf16(128, HID, 0, 0);
-    const uint32_t id_da1 = tc::idesc_bf16(128, HID, 0, 1);
-    const uint32_t id_dh = tc::idesc_bf16(128, KP, 0, 1);
-    const uint32_t id_w1 = tc::idesc_bf16(128, HC1, 1, 1);
-    const uint32_t id_w0 = tc::idesc_bf16(64, KP + 8, 1, 1);
-    const uint32_t h_addr = tc::smem_u32(Ht), a1_addr = tc::smem_u32(A1t), d_addr = tc::smem_u32(Dt);
-    const uint32_t w0_addr = tc::smem_u32(w0p), w1_addr = tc::smem_u32(w1p);
-    constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
-    uint32_t phase = 0, wacc = 0, wacc0 = 0;   // weight-gradient accumulators initialised (issuing thread)
-    bool pending = false;
-    uint32_t dphase = 0;
-    bool staged = false;   // a step is staged for the scatter warps
-    float dbo[kOut] = {0.0f, 0.0f, 0.0f, 0.0f};
-    const float* b0 = fp + F::B0 + hf * HH;
-    const float* b1 = fp + F::B1 + hf * HH;
-    const float4* wot = reinterpret_cast<const float4*>(fp + F::WOT) + hf * HH;
-    LP_PT_DECL
-
-    auto mma_done = [&]() {
-      tc::mbar_wait(bar, phase);
-      phase ^= 1;
-      tc::fence_after_sync();
-    };
-    auto to_tensor_core = [&]() {   // this thread's smem tiles / TMEM reads -> the MMA issuer
-      tc::fence_async_smem();
-      tc::fence_before_sync();
-      tc::named_bar(1, 256);
-    };
-
-    const int64_t ntiles = (a.M + 127) / 128;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int64_t r0 = tile * 128 + ray_slot<K>(rt);
-      const bool valid = r0 < a.M;
-      const int64_t r = valid ? r0 : a.M - 1;   // tail rows march a real ray with zero upstream
-      const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
-      float p[kC];
-#pragma unroll
-      for (int c = 0; c < kC; ++c) p[c] = valid ? __ldg(a.grad_out + 3 * r + c) : 0.0f;
-      const float gtau = (valid && a.grad_tau) ? __ldg(a.grad_tau + r) : 0.0f;
-      const float gdep = (valid && a.grad_depth) ? __ldg(a.grad_depth + r) : 0.0f;
-      const float tauR = __ldg(a.tau + r);
-      float pbg = 0.0f;
-#pragma unroll
-      for (int c = 0; c < kC; ++c) pbg = fmaf(p[c], bg[c], pbg);
-      float G_ = expf(-tauR) * pbg;      // B1
-      float U = 0.0f, Ue = 0.0f;
-
-      for (int q = R; q >= 0; --q) {
-        // ---- B2: recompute sample q (taps, gather fused with step q+1's scatter, Z1, Z2)
-        double x[3];
-        sample_point(ray, q, a.contract, x);
-        write_taps<KIND, K>(taps + rt * NPL, x, a.dims);
-        __syncwarp();
-        LP_PT(0)
-        if (SW == 0 && pending)   // warp-uniform
-          coop_gather<KIND, K, HC, kTc2Pieces, true>(planes, taps, a.dims, Ht, L::HB_PIECE, wq * 32, lane, gplanes, ptaps, dhs,
-                                            it0, it1);
-        else
-          coop_gather<KIND, K, HC, kTc2Pieces>(planes, taps, a.dims, Ht, L::HB_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
-                                      it0, it1);
-        pending = false;
-        LP_PT(1)
-        to_tensor_core();
-        if (gt == 0) {
-          tc::fence_after_sync();
-          mma_split6(tS0, h_addr, L::HB_PIECE, HC, w0_addr, L::W0_PIECE, KP, KP / 16, id_z);
-          tc::mma_commit(bar);
-        }
-        mma_done();
-        LP_PT(2)
-        if (SW > 0 && staged) {   // A1 piece 2 and the D region still hold the previous step's staging
-          tc::mbar_wait(bar_dr, dphase);
-          dphase ^= 1;
-        }
-        LP_PT(7)
-        uint32_t mask1 = 0;   // ReLU'(z1) of this half's hidden units
-        {
-          float z[HH];
-          tc::tmem_ld<HH>(tS0 + tq + hf * HH, z);
-#pragma unroll
-          for (int c = 0; c < HH / 8; ++c) {
-            float a1[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const float zz = z[8 * c + u] + b0[8 * c + u];
-              mask1 |= (zz > 0.0f ? 1u : 0u) << (8 * c + u);
-              a1[u] = fmaxf(zz, 0.0f);
-            }
-            tc::store8<kTc2Pieces>(A1t, L::A1_PIECE, rt, hf * HH + 8 * c, HC1, a1);
-          }
-        }
-        LP_PT(3)
-        to_tensor_core();
-        if (gt == 0) {
-          tc::fence_after_sync();
-          mma_split6(tS1, a1_addr, L::A1_PIECE, HC1, w1_addr, L::W1_PIECE, HID, HID / 16, id_z);
-          tc::mma_commit(bar);
-        }
-        mma_done();
-        LP_PT(4)
-        float a2[HH];
-        {
-          tc::tmem_ld<HH>(tS1 + tq + hf * HH, a2);
-          float4 part = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-#pragma unroll
-          for (int i = 0; i < HH; ++i) {
-            a2[i] = fmaxf(a2[i] + b1[i], 0.0f);
-            const float4 w = wot[i];
-            part.x = fmaf(w.x, a2[i], part.x);
-            part.y = fmaf(w.y, a2[i], part.y);
-            part.z = fmaf(w.z, a2[i], part.z);
-            part.w = fmaf(w.w, a2[i], part.w);
-          }
-          xo[hf * 128 + rt] = part;
-        }
-        tc::fence_before_sync();
-        tc::named_bar(1, 256);
-        float o[kOut];
-        {
-          const float4 p0 = xo[rt], p1 = xo[128 + rt];
-          o[0] = fp[F::BO + 0] + p0.x + p1.x;
-          o[1] = fp[F::BO + 1] + p0.y + p1.y;
-          o[2] = fp[F::BO + 2] + p0.z + p1.z;
-          o[3] = fp[F::BO + 3] + p0.w + p1.w;
-        }
-        const float s_sig = sigmoid_f(o[0]);
-        const float ds = (float)ray.delta * softplus_f(o[0]);
-        float col[kC];
-#pragma unroll
-        for (int c = 0; c < kC; ++c) col[c] = sigmoid_f(o[1 + c]);
-        // ---- B3: Eq. 3, log-domain reverse update (R12); both halves hold the same state
-        const float tau_q = (tauR - U) - Ue;
-        two_sum_add(U, Ue, ds);
-        const float tau_qm1 = (tauR - U) - Ue;
-        float aq = 0.0f;
-#pragma unroll
-        for (int c = 0; c < kC; ++c) aq = fmaf(p[c], col[c], aq);
-        aq = fmaf(gdep, (float)ray_t(ray, q), aq);   // depth channel: "colour" t_q, no MLP gradient
-        const float wq_ = q > 0 ? expf(-tau_qm1) * (-expm1f(-ds)) : 0.0f;
-        const float Tq_aq = q > 0 ? expf(-tau_q) * aq : 0.0f;
-        const float dsig = (float)ray.delta * (gtau - (G_ - Tq_aq));
-        G_ = fmaf(wq_, aq, G_);
-        // ---- B4: head VJP
-        float dout[8];
-        dout[0] = dsig * s_sig;
-#pragma unroll
-        for (int c = 0; c < kC; ++c) dout[1 + c] = wq_ * p[c] * col[c] * (1.0f - col[c]);
-#pragma unroll
-        for (int c = 4; c < 8; ++c) dout[c] = 0.0f;
-        // ---- B5: delta2 = ReLU'(z2) (Wo^T dout) -> D2, a2 -> A2, dout -> A1 tile columns [HID+8, HID+16)
-        if (hf == 0) {
-#pragma unroll
-          for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
-          tc::store8<2>(A1t, L::A1_PIECE, rt, HID + 8, HC1, dout);
-        }
-#pragma unroll
-        for (int c = 0; c < HH / 8; ++c) {
-          float d2[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const float4 w = wot[8 * c + u];
-            float s = w.x * dout[0];
-            s = fmaf(w.y, dout[1], s);
-            s = fmaf(w.z, dout[2], s);
-            s = fmaf(w.w, dout[3], s);
-            d2[u] = a2[8 * c + u] > 0.0f ? s : 0.0f;
-          }
-          tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, 2 * HID, d2);
-          tc::store8<2>(Dt, L::DP, rt, HID + hf * HH + 8 * c, 2 * HID, a2 + 8 * c);
-        }
-        LP_PT(3)
-        to_tensor_core();
-        if (gt == 0) {
-          tc::fence_after_sync();
-          // dA1 = D2 W1   (B = W1 [out][in] viewed MN-major: MN = in, K = out)
-#pragma unroll
-          for (int ks = 0; ks < HID / 16; ++ks)
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-              tc::mma_bf16(tS0, tc::desc_kmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
-                           tc::desc_mnmajor(w1_addr + QB[c] * L::W1_PIECE, HID, ks), id_da1, (ks | c) != 0);
-          // [dW1 db1 . ; . . dWo^T] += [D2 | A2]^T [A1 | 1 | DOUT]   (K = the 128 samples of this step)
-#pragma unroll
-          for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              tc::mma_bf16(tW1, tc::desc_mnmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
-                           tc::desc_mnmajor(a1_addr + QB[c] * L::A1_PIECE, HC1, ks), id_w1, wacc);
-              wacc = 1;
-            }
-          tc::mma_commit(bar);
-        }
-        mma_done();
-        LP_PT(4)
-        {   // delta1 = ReLU'(z1) dA1 -> D1 (over D2, consumed)
-          float da[HH];
-          tc::tmem_ld<HH>(tS0 + tq + hf * HH, da);
-#pragma unroll
-          for (int c = 0; c < HH / 8; ++c) {
-            float d1[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) d1[u] = (mask1 >> (8 * c + u)) & 1u ? da[8 * c + u] : 0.0f;
-            tc::store8<2>(Dt, L::DP, rt, hf * HH + 8 * c, 2 * HID, d1);
-          }
-        }
-        LP_PT(3)
-        to_tensor_core();
-        if (gt == 0) {
-          tc::fence_after_sync();
-          // dH = D1 W0 ; dW0|db0 += D1^T [H|1]
-#pragma unroll
-          for (int ks = 0; ks < HID / 16; ++ks)
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-              tc::mma_bf16(tS1, tc::desc_kmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
-                           tc::desc_mnmajor(w0_addr + QB[c] * L::W0_PIECE, KP, ks), id_dh, (ks | c) != 0);
-#pragma unroll
-          for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              tc::mma_bf16(tW0, tc::desc_mnmajor(d_addr + QA[c] * L::DP, 2 * HID, ks),
-                           tc::desc_mnmajor(h_addr + QB[c] * L::HB_PIECE, HC, ks), id_w0, wacc0);
-              wacc0 = 1;
-            }
-          tc::mma_commit(bar);
-        }
-        mma_done();
-        LP_PT(4)
-        // ---- B6: this half's dH channels -> fp32 staging; scattered by the next step's gather
-        {
-          constexpr int HK = KP / 2;
-          float dh[HK];
-          tc::tmem_ld<HK>(tS1 + tq + hf * HK, dh);
-#pragma unroll
-          for (int k4 = 0; k4 < HK / 4; ++k4)
-            if (hf * HK + 4 * k4 < K)
-              *reinterpret_cast<float4*>(dhs + rt * (K + 4) + hf * HK + 4 * k4) =
-                  make_float4(dh[4 * k4], dh[4 * k4 + 1], dh[4 * k4 + 2], dh[4 * k4 + 3]);
-        }
-        if (hf == 0) {
-#pragma unroll
-          for (int pp = 0; pp < NPL; ++pp) ptaps[rt * NPL + pp] = taps[rt * NPL + pp];
-        }
-        pending = true;
-        if constexpr (SW > 0) {
-          tc::mbar_arrive(bar_st);
-          staged = true;
-        }
-        tc::fence_before_sync();
-        tc::named_bar(1, 256);
-        LP_PT(3)
-      }
-    }
-    LP_PT_FLUSH(1)
-    if (SW == 0 && pending) coop_scatter<KIND, K>(gplanes, ptaps, a.dims, dhs, wq * 32, lane, it0, it1);
-
-    // ---- B7: flush the gradient partials (TMEM accumulators + register bias sums)
-    tc::fence_after_sync();
-    const bool had_tiles = (int64_t)blockIdx.x < ntiles;
-    if (hf == 0) {
-      // M = 64 accumulator: row i lives in TMEM lane (i/16)*32 + i%16
-      const int row = 16 * wq + lane;
-      float w0row[KP + 8];
-      tc::tmem_ld<KP + 8>(tW0 + tq, w0row);
-      if (had_tiles && lane < 16) {
-#pragma unroll
-        for (int c = 0; c < K; ++c) atomicAdd(a.gparams + P::W0 + row * K + c, w0row[c]);
-        atomicAdd(a.gparams + P::B0 + row, w0row[KP]);   // ones column: db0
-      }
-#pragma unroll
-      for (int i = 0; i < kOut; ++i) {
-        float s = dbo[i];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        dbo[i] = s;
-      }
-      if (lane == 0 && had_tiles) {
-#pragma unroll
-        for (int i = 0; i < kOut; ++i) atomicAdd(a.gparams + P::BO + i, dbo[i]);
-      }
-    } else {
-      // M = 128 accumulator: row i in TMEM lane i; rows < HID: D2 units (dW1, db1), rows >= HID: A2 units (dWo^T)
-      const int row = 32 * wq + lane;
-      float w1row[HC1];
-      tc::tmem_ld<HC1>(tW1 + tq, w1row);
-      if (had_tiles && row < HID) {
-#pragma unroll
-        for (int c = 0; c < HID; ++c) atomicAdd(a.gparams + P::W1 + row * HID + c, w1row[c]);
-        atomicAdd(a.gparams + P::B1 + row, w1row[HID]);   // ones column: db1
-      }
-      if (had_tiles && row >= HID) {
-#pragma unroll
-        for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + (row - HID), w1row[HID + 8 + rr]);
-      }
-    }
-  }   // compute warps
-  tc::fence_before_sync();
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    tc::fence_after_sync();
-    tc::tmem_dealloc(*tslot, L::TMEM_COLS);
-  }
-}
 
 #ifndef LP_PT_ROLES   // phase timers per role of lp_bwd_tc2p_kernel: 1 compute, 2 producers, 4 scatter
 #define LP_PT_ROLES 7
@@ -693,9 +294,8 @@ __global__ void __launch_bounds__(256 + 32 * kBwd2ScatterWarps, 1) lp_bwd_tc2_ke
 #define LP_PTS_FLUSH(k) LP_PT_ROLE(4, LP_PT_FLUSH(k))
 
 // ================================================================= K2tc2 backward, warp-specialised
-// Same arithmetic as lp_bwd_tc2_kernel, with the recompute's taps + cooperative gather (B2/F3)
-// taken out of the compute warps' chain: four producer warps march one step ahead into a
-// second H tile (double buffer, full/empty mbarriers), so the gather overlaps the compute
+// The recompute's taps + cooperative gather (B2/F3) run outside the compute warps' chain:
+// four producer warps march one step ahead into a second H tile (double buffer, full/empty mbarriers), so the gather overlaps the compute
 // warps' four serial MMA rounds and epilogues (the phase timers of the single-role kernel:
 // gather + taps 35% of the compute warps' time, MMA waits 38%, epilogues 26%). The shared
 // memory this needs comes from the A1 tile: its third bf16 piece feeds only Z2 = A1 W1^T
