@@ -59,6 +59,9 @@ inline bool force_fma() {
 #ifndef LP_FWD2_GROUPS
 #define LP_FWD2_GROUPS 2
 #endif
+#ifndef LP_TC_PRODUCER   // K2tc: warp-specialised producer kernel (lp_bwd_tcp_kernel)
+#define LP_TC_PRODUCER 1
+#endif
 #ifndef LP_BWD_GROUPS
 #define LP_BWD_GROUPS 2
 #endif
@@ -92,9 +95,17 @@ lp_status run_bwd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
   if constexpr (NH == 1) {
     if (!force_fma()) {
       static LaunchShape shape;
-      constexpr int G = kBwdGroups, T = LP_BWD_T;
-      return launch(lp::lp_bwd_tc_kernel<KIND, K, HID, G, T>, shape, lp::BwdTcSmem<KIND, K, HID, G, T>::BYTES,
-                    128 * T * G + 32 * lp::bwd_scatter_warps<T>(), G, a.M, a, w, s);
+      // K = 32 (c3, c4, c5): the warp-specialised producer kernel; K = 8 / 16 (c1, c2): two
+      // groups per CTA gathering for themselves (measured: c4 bwd 376.5 -> 358.2 ms, c3 123.7 ->
+      // 115.3 ms with producers; c2 12.8 -> 13.8 ms, so K = 16 keeps the two-group kernel)
+      if constexpr (K == 32 && LP_TC_PRODUCER) {
+        return launch(lp::lp_bwd_tcp_kernel<KIND, K, HID>, shape, lp::BwdTcpSmem<KIND, K, HID>::BYTES,
+                      256 + 128 + 32 * lp::kBwdpScatterWarps, 1, a.M, a, w, s);
+      } else {
+        constexpr int G = kBwdGroups, T = LP_BWD_T;
+        return launch(lp::lp_bwd_tc_kernel<KIND, K, HID, G, T>, shape, lp::BwdTcSmem<KIND, K, HID, G, T>::BYTES,
+                      128 * T * G + 32 * lp::bwd_scatter_warps<T>(), G, a.M, a, w, s);
+      }
     }
   }
   if constexpr (NH == 2 && HID == 64 && K >= 8) {

@@ -845,4 +845,353 @@ __global__ void __launch_bounds__(128 * T * G + 32 * bwd_scatter_warps<T>(), 1) 
   }
 }
 
+// ================================================================= K2tc backward, warp-specialised
+// The K2tc2 producer design (lp_tc2_kernels.cuh, lp_bwd_tc2p_kernel) for one hidden layer:
+// one 128-ray group per CTA with two threads per ray (thread (half, row) owns hidden units
+// [half*HID/2, (half+1)*HID/2) of its ray's sample), four producer warps that compute the
+// taps and gather the next step into the other buffer of a double-buffered [H | 1 | DO]
+// tile, and four scatter warps that reduce each step's dH, staged over the H buffer once
+// Z and the weight-gradient MMAs are done with it. The compute warps never load from the
+// grid and never wait for the scatter; per step they run Z = H W0^T, the epilogue (a1,
+// partial output layer, exchange, heads, Eq. 3, delta1) and one MMA round
+// dH = D1 W0, [dW0 db0 . ; . dWo^T] += [D1 | A1]^T [H | 1 | DO].
+#ifndef LP_BWDP_NB
+#define LP_BWDP_NB 3
+#endif
+// H / taps buffers in the producer -> compute -> scatter ring. Two are not enough here: the
+// cycle staging(n) -> scatter(n) -> gather(n + NB) -> Z(n + NB) spans the scatter, the gather and
+// the compute chain, ~2.5 steps of the short one-hidden-layer chain (c4 bwd 424 ms with NB = 2).
+constexpr int kBwdpBuffers = LP_BWDP_NB;
+
+template <int KIND, int K, int HID>
+struct BwdTcpSmem {
+  using S = TcShape<KIND, K, HID>;
+  static constexpr int NB = kBwdpBuffers;
+  static constexpr uint32_t W0P = 0;
+  static constexpr uint32_t FP = W0P + 3 * S::W0_PIECE;
+  static constexpr uint32_t H = (FP + TcParams<K, HID>::N * 4 + 127) & ~127u;   // 2 buffers x 3 pieces
+  static constexpr uint32_t DA = H + NB * 3 * S::HB_PIECE;                     // [D1 | A1], 2 pieces
+  static constexpr uint32_t TAPS = DA + 2 * S::DA_PIECE;                       // NB buffers [128][NPL]
+  static constexpr uint32_t XO = TAPS + NB * S::TAPS;                          // [2 halves][128] float4
+  static constexpr uint32_t BAR = (XO + 2 * 128 * 16 + 127) & ~127u;
+  // mbarriers: MMA, staged[NB], full[NB], empty[NB]; then the TMEM slot
+  static constexpr uint32_t SLOT = 8 * (1 + 3 * NB);
+  static constexpr uint32_t BYTES = BAR + SLOT + 16;
+  static constexpr uint32_t TMEM_COLS = 256;
+  static_assert(2 * S::HB_PIECE >= 128 * (K + 4) * 4, "dH staging fits pieces 0-1 of an H buffer");
+  static_assert(BYTES <= 227 * 1024, "shared memory");
+};
+
+#ifndef LP_BWDP_SW
+#define LP_BWDP_SW 4
+#endif
+constexpr int kBwdpScatterWarps = LP_BWDP_SW;
+
+template <int KIND, int K, int HID>
+__global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_tcp_kernel(const KernelArgs a) {
+  using L = BwdTcpSmem<KIND, K, HID>;
+  using S = TcShape<KIND, K, HID>;
+  using F = TcParams<K, HID>;
+  using P = PackedParams<K, HID, 1>;
+  constexpr int HH = HID / 2, KP = S::KP, HC = S::HC, HP = S::HP, NPL = S::NPL;
+  constexpr int SW = kBwdpScatterWarps, NB = L::NB;
+  static_assert(SW > 0 && 4 % SW == 0, "scatter warps");
+  static_assert(HH % 8 == 0, "per-half hidden units");
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* w0p = smem + L::W0P;
+  float* fp = reinterpret_cast<float*>(smem + L::FP);
+  uint8_t* DAt = smem + L::DA;
+  float4* xo = reinterpret_cast<float4*>(smem + L::XO);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* staged = bar + 1;        // [NB] 256 compute threads: dH of the step staged in H[b]
+  uint64_t* full = bar + 1 + NB;     // [NB] 128 producer threads: H / taps buffer written
+  uint64_t* empty = bar + 1 + 2 * NB;  // [NB] every lane of the scatter warps: staging + taps read
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + L::SLOT);
+
+  for (uint32_t i = threadIdx.x * 16; i < L::BAR; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  stage_tc_weights<K, HID, KP>(w0p, fp, a.params);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(bar, 1);
+    for (int b = 0; b < NB; ++b) {
+      tc::mbar_init(&staged[b], 256);
+      tc::mbar_init(&full[b], 128);
+      tc::mbar_init(&empty[b], 32 * SW);
+    }
+  }
+  if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
+  tc::fence_async_smem();
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const int R = a.S - 1;
+  const int64_t ntiles = (a.M + 127) / 128;
+
+  if (threadIdx.x >= 384) {   // ---- scatter warps: B6 of every staged step
+    const int sw = (threadIdx.x - 384) / 32, sl = threadIdx.x & 31;
+    float* sgpl[3] = {a.ggrid[0], a.ggrid[1], a.ggrid[2]};
+    uint32_t b = 0, ph = 0;   // ring position of the step and the parity of its use
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+      for (int q = 0; q < a.S; ++q) {
+        tc::mbar_wait(&staged[b], ph);
+        const float4* staps = reinterpret_cast<const float4*>(smem + L::TAPS + b * S::TAPS);
+        const float* dhs = reinterpret_cast<const float*>(smem + L::H + b * 3 * S::HB_PIECE);
+        for (int rb = sw; rb < 4; rb += SW) coop_scatter<KIND, K>(sgpl, staps, a.dims, dhs, rb * 32, sl);
+        __syncwarp();
+        tc::mbar_arrive(&empty[b]);   // every lane: its own reads of the staging / taps precede it
+        if (++b == NB) b = 0, ph ^= 1;
+      }
+  } else if (threadIdx.x >= 256) {   // ---- producers: taps + cooperative gather, one step ahead
+    const int pw = (threadIdx.x - 256) >> 5, lane = threadIdx.x & 31, row = pw * 32 + lane;
+    const float* planes[3] = {a.grid[0], a.grid[1], a.grid[2]};
+    uint32_t b = 0, ph = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t r0 = tile * 128 + ray_slot<K>(row);
+      const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r0 < a.M ? r0 : a.M - 1, R);
+      for (int q = R; q >= 0; --q) {
+        float4* taps = reinterpret_cast<float4*>(smem + L::TAPS + b * S::TAPS);
+        uint8_t* Hb = smem + L::H + b * 3 * S::HB_PIECE;
+        tc::mbar_wait(&empty[b], ph ^ 1);
+        {   // the staging of step n - NB overwrote pieces 0-1: restore this row's zero padding
+            // columns [K, KP) (K = 8) and its ones column block
+#pragma unroll
+          for (int c8 = K; c8 < KP; c8 += 8)
+#pragma unroll
+            for (int pc = 0; pc < 2; ++pc)
+              *reinterpret_cast<uint4*>(Hb + pc * S::HB_PIECE + tc::cm_off(row, c8, HC)) = make_uint4(0u, 0u, 0u, 0u);
+          const uint32_t off = tc::cm_off(row, KP, HC);
+          *reinterpret_cast<uint4*>(Hb + off) = make_uint4(0x3F80u, 0u, 0u, 0u);   // bf16 1.0, then zeros
+          *reinterpret_cast<uint4*>(Hb + S::HB_PIECE + off) = make_uint4(0u, 0u, 0u, 0u);
+        }
+        double x[3];
+        sample_point(ray, q, a.contract, x);
+        write_taps<KIND, K>(taps + row * NPL, x, a.dims);
+        __syncwarp();
+        coop_gather<KIND, K, HC, kBwdHPieces>(planes, taps, a.dims, Hb, S::HB_PIECE, pw * 32, lane);
+        tc::fence_async_smem();
+        tc::mbar_arrive(&full[b]);
+        if (++b == NB) b = 0, ph ^= 1;
+      }
+    }
+  } else {   // ---- compute warps
+    const int gt = threadIdx.x, hf = gt >> 7, rt = gt & 127, wq = (gt >> 5) & 3, lane = gt & 31;
+    const uint32_t tbase = *tslot;
+    const uint32_t tZ = tbase, tDH = tbase + 64, tW = tbase + 96;
+    const uint32_t tq = (uint32_t)(wq * 32) << 16;
+    float bg[kC];
+#pragma unroll
+    for (int c = 0; c < kC; ++c) bg[c] = a.bg ? __ldg(a.bg + c) : 0.0f;
+    const uint32_t id_z = tc::idesc_bf16(128, HID, 0, 0);
+    const uint32_t id_dh = tc::idesc_bf16(128, KP, 0, 1);
+    const uint32_t id_w = tc::idesc_bf16(128, HC, 1, 1);
+    const uint32_t h_addr = tc::smem_u32(smem + L::H), w_addr = tc::smem_u32(w0p), da_addr = tc::smem_u32(DAt);
+    // base descriptors (the issuing thread adds compile-time piece / K-step offsets)
+    const uint64_t kH = tc::kdesc0(h_addr, HC), kW0 = tc::kdesc0(w_addr, KP), kDA = tc::kdesc0(da_addr, 2 * HP);
+    const uint64_t mW0 = tc::mdesc0(w_addr, KP), mDA = tc::mdesc0(da_addr, 2 * HP), mH = tc::mdesc0(h_addr, HC);
+    constexpr uint32_t MSDA = 2 * (2 * HP / 8) * 128, MSW0 = 2 * (KP / 8) * 128, MSH = 2 * (HC / 8) * 128;
+    constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
+    uint32_t phase = 0, wacc = 0, b = 0, bph = 0;   // bph: parity of this use of ring buffer b
+    float dbo[kOut] = {0.0f, 0.0f, 0.0f, 0.0f};
+    const float* b0 = fp + F::B0 + hf * HH;
+    const float4* wot = reinterpret_cast<const float4*>(fp + F::WOT) + hf * HH;
+    LP_PT_DECL
+
+    auto mma_done = [&]() {
+      tc::mbar_wait(bar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+    };
+
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t r0 = tile * 128 + ray_slot<K>(rt);
+      const bool valid = r0 < a.M;
+      const int64_t r = valid ? r0 : a.M - 1;   // tail rows march a real ray with zero upstream
+      const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
+      float p[kC];
+#pragma unroll
+      for (int c = 0; c < kC; ++c) p[c] = valid ? __ldg(a.grad_out + 3 * r + c) : 0.0f;
+      const float gtau = (valid && a.grad_tau) ? __ldg(a.grad_tau + r) : 0.0f;
+      const float gdep = (valid && a.grad_depth) ? __ldg(a.grad_depth + r) : 0.0f;
+      const float tauR = __ldg(a.tau + r);
+      float pbg = 0.0f;
+#pragma unroll
+      for (int c = 0; c < kC; ++c) pbg = fmaf(p[c], bg[c], pbg);
+      float G_ = expf(-tauR) * pbg;      // B1
+      float U = 0.0f, Ue = 0.0f;
+
+      for (int q = R; q >= 0; --q) {
+        uint8_t* Hb = smem + L::H + b * 3 * S::HB_PIECE;
+        const uint64_t kHb = tc::dplus(kH, (uint32_t)(b * 3) * S::HB_PIECE);
+        const uint64_t mHb = tc::dplus(mH, (uint32_t)(b * 3) * S::HB_PIECE);
+        // ---- B2: Z = H W0^T on the producers' H tile of this step
+        if (gt == 0) {
+          tc::mbar_wait(&full[b], bph);
+          tc::fence_after_sync();
+          constexpr int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {0, 1, 0, 2, 1, 0};
+          constexpr int NPROD = kBwdHPieces == 3 ? 6 : 5;
+#pragma unroll
+          for (int ks = 0; ks < KP / 16; ++ks)
+#pragma unroll
+            for (int c = 0; c < NPROD; ++c)
+              tc::mma_bf16(tZ, tc::dplus(kHb, PA[c] * S::HB_PIECE + ks * 256),
+                           tc::dplus(kW0, PB[c] * S::W0_PIECE + ks * 256), id_z, (ks | c) != 0);
+          tc::mma_commit(bar);
+        }
+        mma_done();
+        LP_PT(2)
+        float a1[HH];
+        {   // this half's units: a1 = relu(z + b0), partial output layer, exchange
+          tc::tmem_ld<HH>(tZ + tq + (uint32_t)(hf * HH), a1);
+          float4 part = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+          for (int i = 0; i < HH; ++i) {
+            a1[i] = fmaxf(a1[i] + b0[i], 0.0f);
+            const float4 w = wot[i];
+            part.x = fmaf(w.x, a1[i], part.x);
+            part.y = fmaf(w.y, a1[i], part.y);
+            part.z = fmaf(w.z, a1[i], part.z);
+            part.w = fmaf(w.w, a1[i], part.w);
+          }
+          xo[hf * 128 + rt] = part;
+        }
+        tc::fence_before_sync();
+        tc::named_bar(1, 256);
+        float o[kOut];
+        {
+          const float4 p0 = xo[rt], p1 = xo[128 + rt];
+          o[0] = fp[F::BO + 0] + p0.x + p1.x;
+          o[1] = fp[F::BO + 1] + p0.y + p1.y;
+          o[2] = fp[F::BO + 2] + p0.z + p1.z;
+          o[3] = fp[F::BO + 3] + p0.w + p1.w;
+        }
+        const float s_sig = sigmoid_f(o[0]);
+        const float ds = (float)ray.delta * softplus_f(o[0]);
+        float col[kC];
+#pragma unroll
+        for (int c = 0; c < kC; ++c) col[c] = sigmoid_f(o[1 + c]);
+        // ---- B3: Eq. 3, log-domain reverse update (R12); both halves hold the same state
+        const float tau_q = (tauR - U) - Ue;
+        two_sum_add(U, Ue, ds);
+        const float tau_qm1 = (tauR - U) - Ue;
+        float aq = 0.0f;
+#pragma unroll
+        for (int c = 0; c < kC; ++c) aq = fmaf(p[c], col[c], aq);
+        aq = fmaf(gdep, (float)ray_t(ray, q), aq);   // depth channel: "colour" t_q, no MLP gradient
+        const float wq_ = q > 0 ? expf(-tau_qm1) * (-expm1f(-ds)) : 0.0f;
+        const float Tq_aq = q > 0 ? expf(-tau_q) * aq : 0.0f;
+        const float dsig = (float)ray.delta * (gtau - (G_ - Tq_aq));
+        G_ = fmaf(wq_, aq, G_);
+        // ---- B4: head VJP
+        float dout[8];
+        dout[0] = dsig * s_sig;
+#pragma unroll
+        for (int c = 0; c < kC; ++c) dout[1 + c] = wq_ * p[c] * col[c] * (1.0f - col[c]);
+#pragma unroll
+        for (int c = 4; c < 8; ++c) dout[c] = 0.0f;
+        // ---- B5: dL/do -> H[b] columns [KP + 8, KP + 16); a1 and delta1 = ReLU'(z) (Wo^T dout) -> [D1 | A1]
+        if (hf == 0) {
+#pragma unroll
+          for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
+          tc::store8<2>(Hb, S::HB_PIECE, rt, KP + 8, HC, dout);
+        }
+#pragma unroll
+        for (int c = 0; c < HH / 8; ++c) {
+          tc::store8<2>(DAt, S::DA_PIECE, rt, HP + hf * HH + 8 * c, 2 * HP, a1 + 8 * c);
+          float d1[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 w = wot[8 * c + u];
+            float sacc = w.x * dout[0];
+            sacc = fmaf(w.y, dout[1], sacc);
+            sacc = fmaf(w.z, dout[2], sacc);
+            sacc = fmaf(w.w, dout[3], sacc);
+            d1[u] = a1[8 * c + u] > 0.0f ? sacc : 0.0f;
+          }
+          tc::store8<2>(DAt, S::DA_PIECE, rt, hf * HH + 8 * c, 2 * HP, d1);
+        }
+        LP_PT(3)
+        tc::fence_async_smem();
+        tc::fence_before_sync();
+        tc::named_bar(1, 256);
+        if (gt == 0) {
+          tc::fence_after_sync();
+          // dH = D1 W0   (B = W0 viewed MN-major: MN = channel, K = hidden)
+#pragma unroll
+          for (int ks = 0; ks < HID / 16; ++ks)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              tc::mma_bf16(tDH, tc::dplus(kDA, QA[c] * S::DA_PIECE + ks * 256), tc::dplus(mW0, QB[c] * S::W0_PIECE + ks * MSW0),
+                           id_dh, (ks | c) != 0);
+          // [dW0 | db0 | . ; . | dWo^T] += [D1 | A1]^T [H | 1 | DOUT]   (K = the 128 samples of this step)
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              tc::mma_bf16(tW, tc::dplus(mDA, QA[c] * S::DA_PIECE + ks * MSDA), tc::dplus(mHb, QB[c] * S::HB_PIECE + ks * MSH),
+                           id_w, wacc);
+              wacc = 1;
+            }
+          tc::mma_commit(bar);
+        }
+        mma_done();
+        LP_PT(4)
+        // ---- B6: this half's dH channels -> fp32 staging over H[b] (Z and dW are done with it)
+        {
+          float* dhs_b = reinterpret_cast<float*>(Hb);
+          constexpr int HK = KP / 2;
+          float dh[HK];
+          tc::tmem_ld<HK>(tDH + tq + (uint32_t)(hf * HK), dh);
+#pragma unroll
+          for (int k4 = 0; k4 < HK / 4; ++k4)
+            if (hf * HK + 4 * k4 < K)
+              *reinterpret_cast<float4*>(dhs_b + rt * (K + 4) + hf * HK + 4 * k4) =
+                  make_float4(dh[4 * k4], dh[4 * k4 + 1], dh[4 * k4 + 2], dh[4 * k4 + 3]);
+        }
+        tc::mbar_arrive(&staged[b]);
+        if (++b == NB) b = 0, bph ^= 1;
+        LP_PT(3)
+      }
+    }
+    LP_PT_FLUSH(1)
+
+    // ---- B7: flush the weight-gradient accumulator (M = 128: row i in TMEM lane i; rows [0, HP)
+    // D1 units -> dW0, db0 (ones column); rows [HP, 2 HP) A1 units -> dWo^T) and the bias sums
+    tc::fence_after_sync();
+    const bool had_tiles = (int64_t)blockIdx.x < ntiles;
+    if (hf == 0) {
+      float wrow[HC];
+      tc::tmem_ld<HC>(tW + tq, wrow);
+      const int row = 32 * wq + lane;
+      if (had_tiles && row < HID) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) atomicAdd(a.gparams + P::W0 + row * K + c, wrow[c]);
+        atomicAdd(a.gparams + P::B0 + row, wrow[KP]);
+      }
+      if (had_tiles && row >= HP && row - HP < HID) {
+#pragma unroll
+        for (int rr = 0; rr < kOut; ++rr) atomicAdd(a.gparams + P::WO + rr * HID + (row - HP), wrow[KP + 8 + rr]);
+      }
+#pragma unroll
+      for (int i = 0; i < kOut; ++i) {
+        float s = dbo[i];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        dbo[i] = s;
+      }
+      if (lane == 0 && had_tiles) {
+#pragma unroll
+        for (int i = 0; i < kOut; ++i) atomicAdd(a.gparams + P::BO + i, dbo[i]);
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(*tslot, L::TMEM_COLS);
+  }
+}
+
 }  // namespace lp

@@ -32,6 +32,8 @@ if len(cfg.widths) == 4 and not cfg.dir_freqs:   # K2tc2 (lp_tc2_kernels.cuh LP_
     # timers), kernel-1 slots = compute warps
     names[0] = ["prod:empty-wait", "prod:taps+gather", "scat:staged-wait", "scat:reduce", "-", "-", "-", "-"]
     names[1] = ["-", "-", "full+Z1-wait", "epilogues", "bar+MMA2/3/4-wait", "-", "-", "-"]
+if len(cfg.widths) == 3 and not cfg.dir_freqs:   # lp_bwd_tcp_kernel (K2tc, producer warps): compute slots 2-4
+    names[1] = ["-", "-", "full+Z-wait", "epilogue", "MMA2-wait", "-", "-", "-"]
 for k, nm in enumerate(("fwd", "bwd")):
     groups = [range(8)]
     if names[k][0].startswith("prod"):   # producer and scatter warps: shares of each role's own time
