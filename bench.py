@@ -94,18 +94,31 @@ def algorithmic_flops_per_sample(cfg):
     corners = 12 if cfg.kind == wl.TRIPLANE else 8
     w = cfg.widths
     mlp = sum(w[i] * w[i + 1] for i in range(len(w) - 1))
+    if cfg.dir_freqs:   # g_sigma (K, hidden..., 1) and g_v (K + 6F, hidden..., C)
+        ws, wv = list(w[:-1]) + [1], [w[0] + 6 * cfg.dir_freqs] + list(w[1:-1]) + [w[-1] - 1]
+        mlp = sum(ws[i] * ws[i + 1] + wv[i] * wv[i + 1] for i in range(len(w) - 1))
     fwd = corners * cfg.K + mlp
     bwd = 2 * corners * cfg.K + 3 * mlp
     return 2 * fwd, 2 * bwd
 
 
 def tensor_flops_per_sample_bwd(cfg):
-    """Split-bf16 MMA FLOP the one-hidden-layer backward issues per sample (K2tc):
-    Z recompute 6 products x 2 K_p H, dH 3 x 2 H K_p, weight gradients 3 x 2 (2 H_p) (K_p + 16)."""
+    """Split-bf16 MMA FLOP the backward kernel issues per sample (6 piece products for the
+    forward-type contractions, 3 for the gradient-type ones; M x N x K per tile / tile rows).
+    K2tc: Z 6 x 2 K_p H, dH 3 x 2 H K_p, weight gradients 3 x 2 (2 H_p) (K_p + 16).
+    K2tc2: Z1, Z2, dA1, [dW1 db1 dWo] (M 128, N H + 16), dH, [dW0 db0] (M 64, N K_p + 8).
+    K2tcv2: both networks (2 x 64 units), Z1 over [h | direnc], dW1 (M 128, N 144),
+    dW0 (M 128, N 80), dWo (M 128, N 16)."""
     K = cfg.K
     KP = max(K, 16)
     H = cfg.widths[1]
     HP = max(H, 64)
+    if len(cfg.widths) == 4 and cfg.dir_freqs:
+        return (6 * 2 * (KP * H + (KP + 32) * H) + 6 * 2 * 2 * H * H + 3 * 2 * 2 * H * H + 3 * 2 * 128 * 144
+                + 3 * 2 * 2 * H * KP + 3 * 2 * 128 * 80 + 3 * 2 * 128 * 16)
+    if len(cfg.widths) == 4:
+        return (6 * 2 * KP * H + 6 * 2 * H * H + 3 * 2 * H * H + 3 * 2 * 128 * (H + 16) + 3 * 2 * H * KP
+                + 3 * 2 * 64 * (KP + 8))
     return 6 * 2 * KP * H + 3 * 2 * H * KP + 3 * 2 * (2 * HP) * (KP + 16)
 
 
@@ -480,8 +493,11 @@ def run_ours(args):
     alu_peak = fp32_peak_tflops(sm_max)
     traffic = ncu_traffic(cfg.name)
     tc_bwd_f = tensor_flops_per_sample_bwd(cfg)
-    kname = (("lp_fwd_tcv_kernel (K1tcv)", "lp_bwd_tcv_kernel (K2tcv, backward)") if cfg.dir_freqs > 0 else
-             ("lp_fwd_tc2_kernel (K1tc2)", "lp_bwd_tc2_kernel (K2tc2, backward)") if len(cfg.widths) == 4 else
+    kname = (("lp_fwd_tcv2_kernel (K1tcv2)", "lp_bwd_tcv2_kernel (K2tcv2, backward)")
+             if cfg.dir_freqs > 0 and len(cfg.widths) == 4 else
+             ("lp_fwd_tcv_kernel (K1tcv)", "lp_bwd_tcv_kernel (K2tcv, backward)") if cfg.dir_freqs > 0 else
+             ("lp_fwd_tc2_kernel (K1tc2)", "lp_bwd_tc2p_kernel (K2tc2, backward)") if len(cfg.widths) == 4 else
+             ("lp_fwd_tc_kernel (K1tc)", "lp_bwd_tcp_kernel (K2tc, backward)") if cfg.K == 32 else
              ("lp_fwd_tc_kernel (K1tc)", "lp_bwd_tc_kernel (K2tc, backward)"))
     line = {
         "metric": "rays/s fwd+bwd", "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,

@@ -96,8 +96,10 @@ typedef struct {
  * R29): two networks with the hidden widths of `widths`, g_sigma: K -> H -> 1
  * and g_v: K + 6F -> H -> C fed [h, direnc(d)], direnc(d) = per axis k, per
  * frequency 2^i (i < F): sin(pi 2^i d_k), cos(pi 2^i d_k). params packs g_sigma
- * then g_v, each as above. Compiled: one hidden layer, (K, H) = (8, 16) or
- * (32, 64), F <= 5. */
+ * then g_v, each as above. Compiled: one hidden layer with (K, H) = (8, 16) or
+ * (32, 64), and the paper's own networks ("3-layer MLPs with a width of
+ * 64": widths (32, 64, 64, 4), g_sigma 32 -> 64 -> 64 -> 1, g_v 32 + 6F -> 64
+ * -> 64 -> 3); F <= 5. */
 typedef struct {
   int32_t n_layers;
   int32_t widths[LP_MAX_LAYERS + 1];

@@ -93,8 +93,10 @@ lp_status validate(const lp_grid* g, const lp_mlp* m, const lp_rays* r, Inst* in
     return fail(LP_ERR_UNSUPPORTED, "no kernel instance for K=%d widths(n_layers=%d, hidden=%d, out=%d)", g->K,
                 m->n_layers, m->widths[1], m->widths[m->n_layers]);
   if (m->dir_freqs < 0 || m->dir_freqs > 5) return fail(LP_ERR_INVALID_ARG, "dir_freqs must be in [0, 5]");
-  if (m->dir_freqs > 0 && !(inst->nh == 1 && ((g->K == 8 && m->widths[1] == 16) || (g->K == 32 && m->widths[1] == 64))))
-    return fail(LP_ERR_UNSUPPORTED, "view-dependent fields: one hidden layer with (K, hidden) = (8, 16) or (32, 64)");
+  if (m->dir_freqs > 0 && !((inst->nh == 1 && ((g->K == 8 && m->widths[1] == 16) || (g->K == 32 && m->widths[1] == 64))) ||
+                            (inst->nh == 2 && g->K == 32 && m->widths[1] == 64)))
+    return fail(LP_ERR_UNSUPPORTED,
+                "view-dependent fields: (K, hidden) = (8, 16) or (32, 64) with one hidden layer, or (32, 64) with two");
   if (m->dir_freqs > 0 && getenv("LP_KERNELS") && getenv("LP_KERNELS")[0] == 'f')
     return fail(LP_ERR_UNSUPPORTED, "view-dependent fields have no FFMA kernel");
   return LP_OK;
@@ -126,6 +128,7 @@ L2Window theta_window(const lp_grid* g) {
 template <bool FWD, int KIND>
 lp_status dispatch_kind(const Inst& in, const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
   if (a.dir_freqs > 0) {
+    if (in.nh == 2) return FWD ? run_fwd_vd2<KIND, 32>(a, w, s) : run_bwd_vd2<KIND, 32>(a, w, s);
     if (in.K == 8) return FWD ? run_fwd_vd<KIND, 8, 16>(a, w, s) : run_bwd_vd<KIND, 8, 16>(a, w, s);
     return FWD ? run_fwd_vd<KIND, 32, 64>(a, w, s) : run_bwd_vd<KIND, 32, 64>(a, w, s);
   }

@@ -72,5 +72,9 @@ template <int KIND, int K, int HID>
 lp_status run_fwd_vd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s);
 template <int KIND, int K, int HID>
 lp_status run_bwd_vd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s);
+template <int KIND, int K>
+lp_status run_fwd_vd2(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s);
+template <int KIND, int K>
+lp_status run_bwd_vd2(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s);
 
 }  // namespace lpi

@@ -4,14 +4,15 @@
 #include "lp_internal.h"
 #include "lp_tc2_kernels.cuh"
 #include "lp_tcv_kernels.cuh"
+#include "lp_tcv2_kernels.cuh"
 
 namespace lpi {
 
-// Launch a persistent kernel whose CTAs each march `groups` tiles of 128 rays at a time.
+// Launch a persistent kernel whose CTAs each march `groups` tiles of `tile_rows` rays at a time.
 template <typename KernelT>
 lp_status launch(KernelT kernel, LaunchShape& shape, size_t smem, int threads, int groups, int64_t M,
-                 const lp::KernelArgs& args, const L2Window& win, cudaStream_t stream) {
-  const int64_t tiles = (M + 127) / 128;
+                 const lp::KernelArgs& args, const L2Window& win, cudaStream_t stream, int tile_rows = 128) {
+  const int64_t tiles = (M + tile_rows - 1) / tile_rows;
   int grid = 0;
   lp_status st = persistent_grid(kernel, shape, smem, threads, (tiles + groups - 1) / groups, grid);
   if (st != LP_OK || grid == 0) return st;
@@ -132,6 +133,24 @@ lp_status run_bwd_vd(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s)
   static LaunchShape shape;
   return launch(lp::lp_bwd_tcv_kernel<KIND, K, HID>, shape, lp::BwdTcvSmem<KIND, K, HID>::BYTES,
                 256 + 32 * lp::kBwdvScatterWarps, 1, a.M, a, w, s);
+}
+
+// View-dependent fields with the paper's 3-layer networks: K1tcv2 / K2tcv2, tiles of 64 rays.
+#ifndef LP_FWDV2_GROUPS
+#define LP_FWDV2_GROUPS 2
+#endif
+template <int KIND, int K>
+lp_status run_fwd_vd2(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
+  static LaunchShape shape;
+  constexpr int G = LP_FWDV2_GROUPS;
+  return launch(lp::lp_fwd_tcv2_kernel<KIND, K, G>, shape, lp::FwdTcv2Smem<KIND, K, G>::BYTES, 128 * G, G, a.M, a,
+                w, s, 64);
+}
+template <int KIND, int K>
+lp_status run_bwd_vd2(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
+  static LaunchShape shape;
+  return launch(lp::lp_bwd_tcv2_kernel<KIND, K>, shape, lp::BwdTcv2Smem<KIND, K>::BYTES,
+                128 + 32 * lp::kBwdv2ScatterWarps, 1, a.M, a, w, s, 64);
 }
 
 }  // namespace lpi

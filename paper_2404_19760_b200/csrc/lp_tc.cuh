@@ -149,6 +149,25 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[N]) {
 }
 #undef LP_TMEM_LD8
 
+// TMEM -> registers for an M = 64 accumulator (row i in lane (i/16)*32 + i%16), two threads
+// per row: thread t of the warp reads lane t%16 of the warp's quarter, columns
+// [taddr.col + (t/16)*SPLIT, + N). Shape 16x32bx2 (probed: scripts/tc_probe4.cu).
+template <int N, int SPLIT>
+__device__ __forceinline__ void tmem_ld16x2(uint32_t taddr, float (&v)[N]) {
+  static_assert(N % 8 == 0, "TMEM load width");
+  uint32_t r[N];
+#pragma unroll
+  for (int i = 0; i < N; i += 8) {
+    asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=r"(r[i + 0]), "=r"(r[i + 1]), "=r"(r[i + 2]), "=r"(r[i + 3]), "=r"(r[i + 4]), "=r"(r[i + 5]),
+                   "=r"(r[i + 6]), "=r"(r[i + 7])
+                 : "r"(taddr + (uint32_t)i), "n"(SPLIT));
+  }
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // registers -> TMEM: lane = row of the warp's 32-lane quarter, N consecutive 32-bit columns.
 // The caller issues tmem_wait_st() (or to_tensor_core-style fences) before the MMA reads them.
 template <int N>

@@ -227,8 +227,7 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tc2_kernel(const KernelArgs
         }
         xo[hf * 128 + rt] = part;
       }
-      tc::fence_before_sync();
-      tc::named_bar(1 + g, 256);
+      xo_exchange_barrier(1 + g, 256, 1 + G + 4 * g + wq);
       const float4 p0 = xo[rt], p1 = xo[128 + rt];
       float o[kOut];
       o[0] = fp[F::BO + 0] + p0.x + p1.x;
@@ -559,8 +558,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
           }
           xo[hf * 128 + rt] = part;
         }
-        tc::fence_before_sync();
-        tc::named_bar(1, 256);
+        xo_exchange_barrier(1, 256, 2 + wq);
         float o[kOut];
         {
           const float4 p0 = xo[rt], p1 = xo[128 + rt];

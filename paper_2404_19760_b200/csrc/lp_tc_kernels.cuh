@@ -53,7 +53,24 @@
 #define LP_PT_FLUSH(k)
 #endif
 
+#ifndef LP_PAIR_XO
+#define LP_PAIR_XO 1
+#endif
+
 namespace lp {
+
+// Exchange of the partial output-layer sums between the two threads of a ray (halves in
+// warps wq and wq + 4 of a 256-thread group): with LP_PAIR_XO a named barrier over that warp
+// pair only (64 threads, id `pair_id`), instead of the whole group; the next group-wide
+// barrier (with its tcgen05 fence) still precedes the next MMA that overwrites TMEM.
+__device__ __forceinline__ void xo_exchange_barrier(int group_id, int group_threads, int pair_id) {
+#if LP_PAIR_XO
+  tc::named_bar(pair_id, 64);
+#else
+  tc::fence_before_sync();
+  tc::named_bar(group_id, group_threads);
+#endif
+}
 
 // iterations of the cooperative gather whose loads are kept in flight together
 constexpr int kGatherUnroll = LP_GATHER_UNROLL;
@@ -197,12 +214,21 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
                                             const float* dhs = nullptr, int it0 = 0, int it1 = K / 4,
                                             float* const* wplanes = nullptr) {
   constexpr int KC = K / 4, RPI = 32 / KC, NPL = KIND == 0 ? 3 : 1;
-  const int ch = lane % KC, sub = lane / KC;
+  constexpr bool PAIRED = RPI == 4 && PAIR;
   // K = 32: an iteration's 4 rows fill half of each core matrix's 16-byte rows, so its
-  // 8-byte piece stores hit the same 16 banks from all 4 channel blocks (4 wavefronts per
-  // 256 B). Holding the even iteration and storing it with the odd one, lanes of channel
-  // blocks 0-1 write one iteration's rows and blocks 2-3 the other's: 2 wavefronts
-  // (PAIR; measured: c4 fwd -1.6%, c4p bwd -1.7%; off for K1tcv/K2tcv, +5% there).
+  // 8-byte piece stores hit the same 16 banks from all 4 channel blocks. Holding the even
+  // iteration and storing it with the odd one (PAIR; measured: c4 fwd -1.6%, c4p bwd -1.7%;
+  // off for K1tcv/K2tcv, +5% there), a store of 8-byte pieces is serviced per half-warp:
+  // the bank of (row r, chunk ch) is 4 (r % 8) + 2 (ch % 2), so each half-warp must cover 8
+  // distinct rows x both chunk parities. With PAIRED the half-warp holds chunks 4 (lane / 16)
+  // .. + 3 of the 4 rays (lane = (ch / 4) 16 + sub 4 + ch % 4), and lanes with (ch / 2) even
+  // write the even iteration's row first, the others the odd one: one wavefront per
+  // half-warp (the plain mapping lane = sub K/4 + ch gave two).
+#ifndef LP_GATHER_LANES
+#define LP_GATHER_LANES 0
+#endif
+  const int ch = (PAIRED && LP_GATHER_LANES) ? ((lane & 3) | ((lane >> 4) << 2)) : lane % KC;
+  const int sub = (PAIRED && LP_GATHER_LANES) ? ((lane >> 2) & 3) : lane / KC;
   float pacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
   int prow = 0;
 #pragma unroll UNROLL
@@ -250,7 +276,7 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
 #pragma unroll
         for (int i = 0; i < 4; ++i) pacc[i] = acc[i];
       } else {
-        const bool lo = ch < KC / 2;
+        const bool lo = LP_GATHER_LANES ? ((ch >> 1) & 1) == 0 : ch < KC / 2;
         float va[4], vb[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -1056,8 +1082,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
           }
           xo[hf * 128 + rt] = part;
         }
-        tc::fence_before_sync();
-        tc::named_bar(1, 256);
+        xo_exchange_barrier(1, 256, 2 + wq);
         float o[kOut];
         {
           const float4 p0 = xo[rt], p1 = xo[128 + rt];

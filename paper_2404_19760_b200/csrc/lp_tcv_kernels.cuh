@@ -115,6 +115,11 @@ __device__ __forceinline__ void stage_tcv_weights(uint8_t* wp, float* fp, const 
 // bf16 pieces of the [h | direnc(d)] operand of Z = [H | E] W'^T (the weights keep 3):
 // 3 = fp32-class (default); 2 = 16 significant bits, 5 products (experiment, c4v +9%)
 constexpr int kTcvPieces = LP_TCV_PIECES;
+#ifndef LP_TCV_PAIR
+#define LP_TCV_PAIR 0
+#endif
+// paired H-tile stores in the cooperative gather (coop_gather PAIR) for K1tcv / K2tcv
+constexpr bool kTcvPair = LP_TCV_PAIR != 0;
 
 __device__ __forceinline__ void write_direnc(uint8_t* tile, uint32_t piece, int row, int col0, int C, const float d[3],
                                              int F) {
@@ -204,7 +209,7 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tcv_kernel(const KernelArgs
       sample_point(ray, j, a.contract, x);                                 // F2
       write_taps<KIND, K>(taps + rt * NPL, x, a.dims);                     // F3 (cells)
       __syncwarp();
-      coop_gather<KIND, K, KV, kTcvPieces, false, false, 1>(planes, taps, a.dims, X, L::XF_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
+      coop_gather<KIND, K, KV, kTcvPieces, false, kTcvPair, 1>(planes, taps, a.dims, X, L::XF_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
                                   it0, it1);                               // F3 (gather)
       tc::fence_async_smem();
       tc::fence_before_sync();
@@ -246,8 +251,7 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tcv_kernel(const KernelArgs
         }
         xo[hf * 128 + rt] = part;
       }
-      tc::fence_before_sync();
-      tc::named_bar(1 + g, 256);
+      xo_exchange_barrier(1 + g, 256, 1 + G + 4 * g + wq);
       float o[kOut];
       {
         const float4 p0 = xo[rt], p1 = xo[128 + rt];
@@ -424,7 +428,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwdvScatterWarps, 1) lp_bwd_tcv_ke
           coop_gather<KIND, K, HCB, kTcvPieces, true, false, 1>(planes, taps, a.dims, Ht, L::XB_PIECE, wq * 32, lane, gplanes, ptaps, dhs,
                                              it0, it1);
         else
-          coop_gather<KIND, K, HCB, kTcvPieces, false, false, 1>(planes, taps, a.dims, Ht, L::XB_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
+          coop_gather<KIND, K, HCB, kTcvPieces, false, kTcvPair, 1>(planes, taps, a.dims, Ht, L::XB_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
                                        it0, it1);
         pending = false;
         to_tensor_core();
@@ -466,8 +470,7 @@ __global__ void __launch_bounds__(256 + 32 * kBwdvScatterWarps, 1) lp_bwd_tcv_ke
           }
           xo[hf * 128 + rt] = part;
         }
-        tc::fence_before_sync();
-        tc::named_bar(1, 256);
+        xo_exchange_barrier(1, 256, 2 + wq);
         float o[kOut];
         {
           const float4 p0 = xo[rt], p1 = xo[128 + rt];

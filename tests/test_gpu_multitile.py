@@ -86,9 +86,11 @@ print("ERRS" + json.dumps(run_case({cfg!r}, {n}, depth={depth!r}, over={over!r})
 """
 
 # (config, rays, depth): kernel families K2tc (K = 8 / 16 / 32, triplane and voxel),
-# K2tc2 (3-layer MLP, with contraction in cu) and K2tcv (view-dependent)
+# K2tc2 (3-layer MLP, with contraction in cu), K2tcv (view-dependent) and K2tcv2
+# (view-dependent 3-layer nets, 64-ray tiles: n / 128 tiles per CTA)
 CAPPED = [("c1", 4096, False), ("c2", 2048, False), ("c4", 4096, True), ("c5", 2048, False),
-          ("c4p", 2048, True), ("cu", 1024, True), ("c4v", 2048, True), ("c1v", 4096, False)]
+          ("c4p", 2048, True), ("cu", 1024, True), ("c4v", 2048, True), ("c1v", 4096, False),
+          ("cuv", 1024, True), ("c4pv", 2048, False)]
 
 
 @pytest.mark.parametrize("cfg,n,depth", CAPPED)
@@ -108,7 +110,7 @@ def test_multitile_capped_grid(cfg, n, depth):
 
 
 # default launch: K2tc has 148 x 2 groups, K2tc2 / K2tcv 148 x 1 -> >= 2 tiles per group
-LARGE = [("c4", 81920, False), ("c4p", 40960, False), ("c4v", 40960, False)]
+LARGE = [("c4", 81920, False), ("c4p", 40960, False), ("c4v", 40960, False), ("c4pv", 40960, False)]
 
 
 @pytest.mark.parametrize("cfg,n,depth", LARGE)

@@ -69,7 +69,7 @@ def test_parity_subset(torch_cuda, cfg, n):
     _assert(_compare(_gpu_fwd_bwd(torch_cuda, pb), _oracle_fwd_bwd(pb)))
 
 
-RAW_CASES = CASES + [("c4v", 1024), ("c1v", 2048), ("cu", 256)]
+RAW_CASES = CASES + [("c4v", 1024), ("c1v", 2048), ("cu", 256), ("cuv", 256), ("c4pv", 512)]
 
 
 @pytest.mark.parametrize("cfg,n", RAW_CASES)
@@ -83,17 +83,28 @@ def test_gradient_precision(torch_cuda, cfg, n):
         evaluations flip only decisions inside it (measured: every flip here lies
         below 1e-7), 16-bit operands flip decisions outside it;
       * the relative L2 error of the grid gradients < 1e-4 and of the MLP
-        gradients < 5e-4 (measured <= 6e-6 and <= 1.1e-4).
+        gradients < 5e-4 (measured <= 6e-6 and <= 1.1e-4), after the elementwise
+        slack of the decisions within 1e-7 of their scale (reading R15: any fp32
+        evaluation may take those either way). Without it the two-network 3-layer
+        field (c4pv: 256 hidden decisions per sample) measured grid L2 2e-4 from
+        decisions below 1e-7 alone -- its band-1e-7 inf-norm error is 5e-6.
     The 2-piece per-sample build (variants) fails one of these on
     every config here (band 1e-6: up to 4.3e-3; grid L2: 5e-5 .. 1.5e-3).
-    The slack-free error (raw_*) is reported."""
+    The slack-free errors (raw_*, raw_l2_*) are reported."""
     pb = problem_np(cfg, n=n)
     g = _gpu_fwd_bwd(torch_cuda, pb)
     r = oracle_reference(pb, extra_bands=(1e-7, 1e-6))
     errs = _compare(g, r)
-    for i, (a, b) in enumerate(zip(g["gplanes"], r["gplanes"])):
-        errs[f"l2_gplane{i}"] = float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
-    errs["l2_gparams"] = float(np.linalg.norm(g["gparams"] - r["gparams"]) / np.linalg.norm(r["gparams"]))
+    sg7, sp7 = r["extra"][1e-7]
+
+    def l2(a, b, sl):
+        d = np.maximum(np.abs(np.asarray(a, np.float64) - b) - sl, 0.0)
+        return float(np.linalg.norm(d) / max(np.linalg.norm(b), 1e-300))
+    for i, (a, b, sl) in enumerate(zip(g["gplanes"], r["gplanes"], sg7)):
+        errs[f"l2_gplane{i}"] = l2(a, b, sl)
+        errs[f"raw_l2_gplane{i}"] = l2(a, b, 0.0)
+    errs["l2_gparams"] = l2(g["gparams"], r["gparams"], sp7)
+    errs["raw_l2_gparams"] = l2(g["gparams"], r["gparams"], 0.0)
     print(errs)
     _assert(errs)
     assert errs["band1e-06"] < TOL_GRAD, errs
@@ -166,7 +177,7 @@ def test_zero_rays_is_noop(torch_cuda):
     assert out.shape == (0, 3) and float(gpar.abs().sum()) == 0.0
 
 
-@pytest.mark.parametrize("cfg,nsample", [("c2", 256), ("c4", 256), ("c4p", 256), ("c4v", 256)])
+@pytest.mark.parametrize("cfg,nsample", [("c2", 256), ("c4", 256), ("c4p", 256), ("c4v", 256), ("cuv", 128)])
 def test_full_size_sampled_forward(torch_cuda, cfg, nsample):
     """At BASELINE.json's full size, in bench.py's launch configuration: the
     forward over all M rays, checked on sampled rays the oracle computes one by one."""
@@ -286,7 +297,11 @@ def test_autograd_render_depth_contracted(torch_cuda):
 # view-dependent colour, sigma = g_sigma(h), c = g_v(h, direnc(d))
 # on the K1tcv / K2tcv kernels, with depth and contraction riding along.
 VD_CASES = [("c1v", 2048, {}), ("c4v", 1024, {}), ("c1v", 1024, dict(kind=wl.VOXEL)),
-            ("c4v", 512, dict(contraction=1, contract_a=1.0, near_far=(0.05, 9.0)))]
+            ("c4v", 512, dict(contraction=1, contract_a=1.0, near_far=(0.05, 9.0))),
+            # the paper's 3-layer g_sigma / g_v (K1tcv2 / K2tcv2): its renderer setting, c4's
+            # scene, a voxel grid, the radial contraction, F = 5 (E = 30 direnc columns)
+            ("cuv", 256, {}), ("c4pv", 512, {}), ("c4pv", 256, dict(kind=wl.VOXEL, res=40)),
+            ("cuv", 256, dict(contraction=2, contract_a=1.5)), ("c4pv", 256, dict(dir_freqs=5))]
 
 
 @pytest.mark.parametrize("cfg,n,over", VD_CASES)
@@ -297,6 +312,8 @@ def test_parity_view_dependent(torch_cuda, cfg, n, over):
         pb["cfg"] = dataclasses.replace(pb["cfg"], **over)
         if "kind" in over:
             pb["grid"] = wl.make_grid(pb["cfg"])
+        if "dir_freqs" in over:
+            pb["params"] = wl.make_params(pb["cfg"])
         if "near_far" in over:
             pb["near"] = np.full_like(pb["near"], over["near_far"][0])
             pb["far"] = np.full_like(pb["far"], over["near_far"][1])
@@ -320,10 +337,10 @@ def test_autograd_view_dependent(torch_cuda):
     _assert(_compare(g, r))
 
 
-@pytest.mark.parametrize("cfg", ["c4p", "c1v"])
+@pytest.mark.parametrize("cfg", ["c4p", "c1v", "c4pv"])
 def test_ragged_tail_other_kernel_families(torch_cuda, cfg):
-    """M not a multiple of 128 and minimal S on the 3-layer (K1tc2/K2tc2) and the
-    view-dependent (K1tcv/K2tcv) kernels."""
+    """M not a multiple of the tile and minimal S on the 3-layer (K1tc2/K2tc2) and the
+    view-dependent (K1tcv/K2tcv, K1tcv2/K2tcv2) kernels."""
     import dataclasses
     idx = np.arange(1000, dtype=np.int64) * 4 + 3      # within c1v's 4096 rays
     pb = problem_np(cfg, idx=idx, with_gdepth=True)

@@ -155,6 +155,15 @@ CONFIGS = {
                   "c1 with view-dependent colour g_v(h, direnc(d)), F = 4", dir_freqs=4),
     "c4v": Config("c4v", TRIPLANE, 256, 32, (32, 64, 4), 128, 256, 128,
                   "c4 with view-dependent colour g_v(h, direnc(d)), F = 4", dir_freqs=4),
+    # The paper's full renderer setting: view-dependent colour with
+    # g_sigma and g_v each a 3-layer width-64 MLP, 160x160 triplanes, 384 points per ray,
+    # 256x256 renders, per-axis contraction a = 1 (cu's scene); c4pv: c4's workload with these nets.
+    "cuv": Config("cuv", TRIPLANE, 160, 32, (32, 64, 64, 4), 16, 256, 384,
+                  "paper renderer setting: view-dependent g_sigma/g_v 3-layer width-64 MLPs (F = 4), "
+                  "triplane 3x160x160 C=32, 16 views at 256x256, 384 samples/ray, per-axis contraction a=1",
+                  contraction=1, contract_a=1.0, near_far=(0.05, 12.0), dir_freqs=4),
+    "c4pv": Config("c4pv", TRIPLANE, 256, 32, (32, 64, 64, 4), 128, 256, 128,
+                   "c4 with view-dependent g_sigma/g_v 3-layer width-64 MLPs (F = 4)", dir_freqs=4),
     # Splatter benchmark shape: N input feature maps lifted into a 160^3 voxel
     # grid, MLPs off; 32-channel features, 160 points per ray. N = 64 maps
     # of 128x128 pixels (the text gives neither N nor the map size: reading R28).
