@@ -150,7 +150,7 @@ template <int KIND, int K>
 lp_status run_bwd_vd2(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
   static LaunchShape shape;
   return launch(lp::lp_bwd_tcv2_kernel<KIND, K>, shape, lp::BwdTcv2Smem<KIND, K>::BYTES,
-                128 + 32 * lp::kBwdv2ScatterWarps, 1, a.M, a, w, s, 64);
+                128 * lp::kBwdv2CG + 32 * lp::kBwdv2ScatterWarps, 1, a.M, a, w, s, 64);
 }
 
 }  // namespace lpi

@@ -127,19 +127,20 @@ __host__ __device__ constexpr uint32_t v2pb(int c) { return c == 1 || c == 4 ? 1
 __host__ __device__ constexpr uint32_t v2qa(int c) { return c == 2 ? 1u : 0u; }                           // 0 0 1
 __host__ __device__ constexpr uint32_t v2qb(int c) { return c == 1 ? 1u : 0u; }                           // 0 1 0
 
-// The second-layer epilogue shared by both kernels: a2 = relu(z2 + b1) of this thread's
-// units of both networks, the partial output layer, and the exchange with the other half.
-// Returns the logits o and leaves a2 in zs (g_sigma units) / zv (g_v units).
-__device__ __forceinline__ void tcv2_out_layer(const float* fp, int hf, float (&zs)[32], float (&zv)[32],
-                                               float (&o)[kOut]) {
+// The second-layer epilogue shared by both kernels: a2 = relu(z2 + b1) of this thread's UPT
+// units of both networks (from unit u0), and the partial output layer summed over the two
+// halves of the warp (shuffle). Leaves a2 in zs (g_sigma units) / zv (g_v units); returns
+// the partial (sigma logit, 3 colour logits) without the output bias.
+template <int UPT>
+__device__ __forceinline__ float4 tcv2_out_partial(const float* fp, int u0, float (&zs)[UPT], float (&zv)[UPT]) {
   using F = Tcv2Params;
-  const float* bs1 = fp + F::BS1 + 32 * hf;
-  const float* bv1 = fp + F::BV1 + 32 * hf;
-  const float* ws2 = fp + F::WS2 + 32 * hf;
-  const float4* wv2 = reinterpret_cast<const float4*>(fp + F::WV2T) + 32 * hf;
+  const float* bs1 = fp + F::BS1 + u0;
+  const float* bv1 = fp + F::BV1 + u0;
+  const float* ws2 = fp + F::WS2 + u0;
+  const float4* wv2 = reinterpret_cast<const float4*>(fp + F::WV2T) + u0;
   float s = 0.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < UPT; ++i) {
     zs[i] = fmaxf(zs[i] + bs1[i], 0.0f);
     s = fmaf(ws2[i], zs[i], s);
     zv[i] = fmaxf(zv[i] + bv1[i], 0.0f);
@@ -152,10 +153,7 @@ __device__ __forceinline__ void tcv2_out_layer(const float* fp, int hf, float (&
   c0 += __shfl_xor_sync(0xffffffffu, c0, 16);
   c1 += __shfl_xor_sync(0xffffffffu, c1, 16);
   c2 += __shfl_xor_sync(0xffffffffu, c2, 16);
-  o[0] = fp[F::BO + 0] + s;
-  o[1] = fp[F::BO + 1] + c0;
-  o[2] = fp[F::BO + 2] + c1;
-  o[3] = fp[F::BO + 3] + c2;
+  return make_float4(s, c0, c1, c2);
 }
 
 // ================================================================= K1tcv2 forward
@@ -302,7 +300,11 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tcv2_kernel(const KernelArg
         float zs[32], zv[32];
         tc::tmem_ld16x2<32, 32>(tZ2 + tl, zs);
         tc::tmem_ld16x2<32, 32>(tZ2 + tl + 64, zv);
-        tcv2_out_layer(fp, hf, zs, zv, o);
+        const float4 part = tcv2_out_partial<32>(fp, 32 * hf, zs, zv);
+        o[0] = fp[F::BO + 0] + part.x;
+        o[1] = fp[F::BO + 1] + part.y;
+        o[2] = fp[F::BO + 2] + part.z;
+        o[3] = fp[F::BO + 3] + part.w;
       }
       const float ds = (float)ray.delta * softplus_f(o[0]);                // F5
       if (j > 0) {                                                         // F6
@@ -331,9 +333,19 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tcv2_kernel(const KernelArg
 }
 
 // ================================================================= K2tcv2 backward
+// CG column groups: 2 CG threads per ray. Warps w and w + 4 (CG = 2) read the same TMEM lanes
+// (rows) and split the hidden units: thread (cg, half) of a ray owns units
+// [32 cg + half UPT, + UPT), UPT = 32 / CG, of both networks; the four partial output-layer
+// sums meet by shuffle (halves) and through shared memory between the warp pair.
+#ifndef LP_BWDV2_CG
+#define LP_BWDV2_CG 2
+#endif
+constexpr int kBwdv2CG = LP_BWDV2_CG;
+
 template <int KIND, int K>
 struct BwdTcv2Smem : Tcv2Shape<KIND, K> {
   using T = Tcv2Shape<KIND, K>;
+  static constexpr int CG = kBwdv2CG;
   static constexpr int XC = T::KP + T::EP + 16;   // [H | E | 1 | 0]: ones column at KP + EP (db0)
   static constexpr int AC = 144;                  // [A1_s | A1_v | 1 | 0 | DOUT | 0]: ones at 128, dL/do at 136
   static constexpr uint32_t X_PIECE = T::ROWS * XC * 2;
@@ -343,11 +355,13 @@ struct BwdTcv2Smem : Tcv2Shape<KIND, K> {
   static constexpr uint32_t A = X + 3 * X_PIECE;
   static constexpr uint32_t D = A + 3 * A_PIECE;
   static constexpr uint32_t DHS = D + 2 * D_PIECE;          // fp32 dH rows [64][K + 4]
-  static constexpr uint32_t TAPS = DHS + T::ROWS * (K + 4) * 4;
-  static constexpr uint32_t PTAPS = TAPS + T::TAPS;
-  static constexpr uint32_t BAR = (PTAPS + T::TAPS + 127) & ~127u;   // MMA, staged, drained, tmem slot
+  static constexpr uint32_t TAPS = DHS + T::ROWS * (K + 4) * 4;   // [CG][64][NPL] (one copy per column group)
+  static constexpr uint32_t PTAPS = TAPS + CG * T::TAPS;
+  static constexpr uint32_t XO = PTAPS + T::TAPS;           // [CG][64] float4 partial outputs
+  static constexpr uint32_t BAR = (XO + CG * 64 * 16 + 127) & ~127u;   // MMA, staged, drained, tmem slot
   static constexpr uint32_t BYTES = BAR + 32;
   static constexpr uint32_t TMEM_COLS = 512;
+  static_assert(CG == 1 || CG == 2, "column groups");
   static_assert(BYTES <= 227 * 1024, "shared memory");
 };
 
@@ -358,12 +372,12 @@ constexpr int kBwdv2ScatterWarps = LP_BWDV2_SW;
 
 // TMEM: Z1 [0, 128) (then dA1), Z2 [128, 256) (then dH), dW1 [256, 400), dWo [400, 416), dW0 [416, 496)
 template <int KIND, int K>
-__global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(128 * kBwdv2CG + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_kernel(const KernelArgs a) {
   using L = BwdTcv2Smem<KIND, K>;
   using F = Tcv2Params;
   using P = Vd3Packed<K>;
   constexpr int KP = L::KP, EP = L::EP, XC = L::XC, AC = L::AC, NPL = L::NPL, KC = K / 4;
-  constexpr int SW = kBwdv2ScatterWarps;
+  constexpr int SW = kBwdv2ScatterWarps, CG = L::CG, UPT = 32 / CG, NC = 128 * CG;
   static_assert(SW == 1 || SW == 2, "scatter warps");
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* wp = smem;
@@ -372,10 +386,10 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
   uint8_t* At = smem + L::A;
   uint8_t* Dt = smem + L::D;
   float* dhs = reinterpret_cast<float*>(smem + L::DHS);
-  float4* taps = reinterpret_cast<float4*>(smem + L::TAPS);
   float4* ptaps = reinterpret_cast<float4*>(smem + L::PTAPS);
+  float4* xo = reinterpret_cast<float4*>(smem + L::XO);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::BAR);
-  uint64_t* bar_st = bar + 1;   // 128 compute threads: dH of the step staged
+  uint64_t* bar_st = bar + 1;   // NC compute threads: dH of the step staged
   uint64_t* bar_dr = bar + 2;   // every lane of the scatter warps: staging read
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 24);
   const int E = 6 * a.dir_freqs;
@@ -386,7 +400,7 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
   stage_tcv2_weights<K>(wp, fp, a.params, E);
   if (threadIdx.x == 0) {
     tc::mbar_init(bar, 1);
-    tc::mbar_init(bar_st, 128);
+    tc::mbar_init(bar_st, NC);
     tc::mbar_init(bar_dr, 32 * SW);
   }
   if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
@@ -402,8 +416,8 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
   const int R = a.S - 1;
   const int64_t ntiles = (a.M + 63) / 64;
 
-  if (threadIdx.x >= 128) {   // ---- scatter warps: B6 of every staged step
-    const int sw = (threadIdx.x - 128) >> 5, sl = threadIdx.x & 31;
+  if (threadIdx.x >= NC) {   // ---- scatter warps: B6 of every staged step
+    const int sw = (threadIdx.x - NC) >> 5, sl = threadIdx.x & 31;
     float* sgpl[3] = {a.ggrid[0], a.ggrid[1], a.ggrid[2]};
     uint32_t ph = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
@@ -414,11 +428,14 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
         __syncwarp();
         tc::mbar_arrive(bar_dr);   // every lane: its own reads of the staging precede it
       }
-  } else {   // ---- compute warps: 64 rays, two threads per ray
-    const int gt = threadIdx.x, wq = gt >> 5, lane = gt & 31, hf = lane >> 4, rt = 16 * wq + (lane & 15);
+  } else {   // ---- compute warps: 64 rays, 2 CG threads per ray
+    const int gt = threadIdx.x, w = gt >> 5, wq = w & 3, cg = w >> 2, lane = gt & 31, hf = lane >> 4;
+    const int rt = 16 * wq + (lane & 15), u0 = 32 * cg + UPT * hf;   // ray slot, first owned unit
+    const bool lead = cg == 0 && hf == 0;                            // one thread per ray
+    float4* taps = reinterpret_cast<float4*>(smem + L::TAPS) + cg * 64 * NPL;
     const uint32_t tbase = *tslot;
     const uint32_t tZ1 = tbase, tZ2 = tbase + 128, tW1 = tbase + 256, tWo = tbase + 400, tW0 = tbase + 416;
-    const uint32_t tl = (uint32_t)(wq * 32) << 16;
+    const uint32_t tl = (uint32_t)(wq * 32) << 16, tc0 = (uint32_t)(32 * cg);
     const float* planes[3] = {a.grid[0], a.grid[1], a.grid[2]};
     float bg[kC];
 #pragma unroll
@@ -441,12 +458,12 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
     // MN-major K-step (16 rows) bytes of each tile
     constexpr uint32_t MSX = 2 * (XC / 8) * 128, MSA = 2 * (AC / 8) * 128, MSD = 2 * (128 / 8) * 128;
     constexpr uint32_t MSW0S = 2 * (KP / 8) * 128, MSW0V = 2 * ((KP + EP) / 8) * 128, MSW1 = 2 * (64 / 8) * 128;
-    const float* bs0 = fp + F::BS0 + 32 * hf;
-    const float* bv0 = fp + F::BV0 + 32 * hf;
-    const float* bs1 = fp + F::BS1 + 32 * hf;
-    const float* bv1 = fp + F::BV1 + 32 * hf;
-    const float* ws2 = fp + F::WS2 + 32 * hf;
-    const float4* wv2 = reinterpret_cast<const float4*>(fp + F::WV2T) + 32 * hf;
+    const float* bs0 = fp + F::BS0 + u0;
+    const float* bv0 = fp + F::BV0 + u0;
+    const float* bs1 = fp + F::BS1 + u0;
+    const float* bv1 = fp + F::BV1 + u0;
+    const float* ws2 = fp + F::WS2 + u0;
+    const float4* wv2 = reinterpret_cast<const float4*>(fp + F::WV2T) + u0;
     uint32_t phase = 0, wacc1 = 0, wacc0 = 0, dphase = 0;
     bool staged = false;
     float dbo[kOut] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -459,7 +476,7 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
     auto to_tensor_core = [&]() {
       tc::fence_async_smem();
       tc::fence_before_sync();
-      tc::named_bar(1, 128);
+      tc::named_bar(1, NC);
     };
 
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -467,7 +484,7 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
       const bool valid = r0 < a.M;
       const int64_t r = valid ? r0 : a.M - 1;   // tail rows march a real ray with zero upstream
       const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
-      if (hf == 1) write_direnc(Xt, L::X_PIECE, rt, KP, XC, ray.d, a.dir_freqs);   // once per ray
+      if (cg == CG - 1 && hf == 1) write_direnc(Xt, L::X_PIECE, rt, KP, XC, ray.d, a.dir_freqs);   // once per ray
       float p[kC];
 #pragma unroll
       for (int c = 0; c < kC; ++c) p[c] = valid ? __ldg(a.grad_out + 3 * r + c) : 0.0f;
@@ -481,15 +498,16 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
       float U = 0.0f, Ue = 0.0f;
 
       for (int q = R; q >= 0; --q) {
-        // ---- B2: recompute the sample (taps + cooperative gather of the warp's 16 rays)
+        // ---- B2: recompute the sample (taps + cooperative gather; the CG warps of a row
+        // block split its iterations, each with its own copy of the taps)
         if (hf == 0) {
           double x[3];
           sample_point(ray, q, a.contract, x);
           write_taps<KIND, K>(taps + rt * NPL, x, a.dims);
         }
         __syncwarp();
-        coop_gather<KIND, K, XC, 3>(planes, taps, a.dims, Xt, L::X_PIECE, 16 * wq, lane, nullptr, nullptr, nullptr, 0,
-                                    KC / 2);
+        coop_gather<KIND, K, XC, 3>(planes, taps, a.dims, Xt, L::X_PIECE, 16 * wq, lane, nullptr, nullptr, nullptr,
+                                    cg * (KC / 2 / CG), (cg + 1) * (KC / 2 / CG));
         to_tensor_core();
         if (gt == 0) {   // Z1 = [H | E] W0'^T
           tc::fence_after_sync();
@@ -509,11 +527,11 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
         mma_done();
         uint32_t ms1 = 0, mv1 = 0;   // ReLU'(z1) of this thread's units
         {
-          float zs[32], zv[32];
-          tc::tmem_ld16x2<32, 32>(tZ1 + tl, zs);
-          tc::tmem_ld16x2<32, 32>(tZ1 + tl + 64, zv);
+          float zs[UPT], zv[UPT];
+          tc::tmem_ld16x2<UPT, UPT>(tZ1 + tl + tc0, zs);
+          tc::tmem_ld16x2<UPT, UPT>(tZ1 + tl + tc0 + 64, zv);
 #pragma unroll
-          for (int c8 = 0; c8 < 4; ++c8) {
+          for (int c8 = 0; c8 < UPT / 8; ++c8) {
             float as[8], av[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -523,8 +541,8 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
               as[u] = fmaxf(a_s, 0.0f);
               av[u] = fmaxf(a_v, 0.0f);
             }
-            tc::store8<3>(At, L::A_PIECE, rt, 32 * hf + 8 * c8, AC, as);
-            tc::store8<3>(At, L::A_PIECE, rt, 64 + 32 * hf + 8 * c8, AC, av);
+            tc::store8<3>(At, L::A_PIECE, rt, u0 + 8 * c8, AC, as);
+            tc::store8<3>(At, L::A_PIECE, rt, 64 + u0 + 8 * c8, AC, av);
           }
         }
         to_tensor_core();
@@ -546,22 +564,32 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
         float o[kOut];
         uint32_t ms2 = 0, mv2 = 0;   // ReLU'(z2)
         {
-          float zs[32], zv[32];
-          tc::tmem_ld16x2<32, 32>(tZ2 + tl, zs);
-          tc::tmem_ld16x2<32, 32>(tZ2 + tl + 64, zv);
+          float zs[UPT], zv[UPT];
+          tc::tmem_ld16x2<UPT, UPT>(tZ2 + tl + tc0, zs);
+          tc::tmem_ld16x2<UPT, UPT>(tZ2 + tl + tc0 + 64, zv);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < UPT; ++i) {
             ms2 |= (zs[i] + bs1[i] > 0.0f ? 1u : 0u) << i;
             mv2 |= (zv[i] + bv1[i] > 0.0f ? 1u : 0u) << i;
           }
-          tcv2_out_layer(fp, hf, zs, zv, o);
+          float4 part = tcv2_out_partial<UPT>(fp, u0, zs, zv);
+          if constexpr (CG == 2) {   // the other warp of the pair holds the other half of the units
+            xo[cg * 64 + rt] = part;
+            tc::named_bar(2 + wq, 64);
+            const float4 p0 = xo[rt], p1 = xo[64 + rt];
+            part = make_float4(p0.x + p1.x, p0.y + p1.y, p0.z + p1.z, p0.w + p1.w);
+          }
+          o[0] = fp[F::BO + 0] + part.x;
+          o[1] = fp[F::BO + 1] + part.y;
+          o[2] = fp[F::BO + 2] + part.z;
+          o[3] = fp[F::BO + 3] + part.w;
         }
         const float s_sig = sigmoid_f(o[0]);
         const float ds = (float)ray.delta * softplus_f(o[0]);
         float col[kC];
 #pragma unroll
         for (int c = 0; c < kC; ++c) col[c] = sigmoid_f(o[1 + c]);
-        // ---- B3: Eq. 3, log-domain reverse update (R12); both halves hold the same state
+        // ---- B3: Eq. 3, log-domain reverse update (R12); every thread of the ray holds the same state
         const float tau_q = (tauR - U) - Ue;
         two_sum_add(U, Ue, ds);
         const float tau_qm1 = (tauR - U) - Ue;
@@ -581,26 +609,26 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
 #pragma unroll
         for (int c = 4; c < 8; ++c) dout[c] = 0.0f;
         // ---- B5: delta2 -> D tile, dL/do -> A1 tile columns [136, 144)
-        if (hf == 0) {
+        if (lead) {
 #pragma unroll
           for (int i = 0; i < kOut; ++i) dbo[i] += dout[i];
           tc::store8<2>(At, L::A_PIECE, rt, 136, AC, dout);
         }
 #pragma unroll
-        for (int c8 = 0; c8 < 4; ++c8) {
+        for (int c8 = 0; c8 < UPT / 8; ++c8) {
           float ds8[8], dv8[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int i = 8 * c8 + u;
-            const float4 w = wv2[i];
-            float sv = w.x * dout[1];
-            sv = fmaf(w.y, dout[2], sv);
-            sv = fmaf(w.z, dout[3], sv);
+            const float4 w4 = wv2[i];
+            float sv = w4.x * dout[1];
+            sv = fmaf(w4.y, dout[2], sv);
+            sv = fmaf(w4.z, dout[3], sv);
             ds8[u] = (ms2 >> i) & 1u ? ws2[i] * dout[0] : 0.0f;
             dv8[u] = (mv2 >> i) & 1u ? sv : 0.0f;
           }
-          tc::store8<2>(Dt, L::D_PIECE, rt, 32 * hf + 8 * c8, 128, ds8);
-          tc::store8<2>(Dt, L::D_PIECE, rt, 64 + 32 * hf + 8 * c8, 128, dv8);
+          tc::store8<2>(Dt, L::D_PIECE, rt, u0 + 8 * c8, 128, ds8);
+          tc::store8<2>(Dt, L::D_PIECE, rt, 64 + u0 + 8 * c8, 128, dv8);
         }
         to_tensor_core();
         if (gt == 0) {
@@ -629,11 +657,11 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
         }
         mma_done();
         {   // delta1 = ReLU'(z1) dA1 -> D (over delta2, consumed); a2 -> A1 columns [0, 128) (consumed)
-          float da_s[32], da_v[32];
-          tc::tmem_ld16x2<32, 32>(tZ1 + tl, da_s);
-          tc::tmem_ld16x2<32, 32>(tZ1 + tl + 64, da_v);
+          float da_s[UPT], da_v[UPT];
+          tc::tmem_ld16x2<UPT, UPT>(tZ1 + tl + tc0, da_s);
+          tc::tmem_ld16x2<UPT, UPT>(tZ1 + tl + tc0 + 64, da_v);
 #pragma unroll
-          for (int c8 = 0; c8 < 4; ++c8) {
+          for (int c8 = 0; c8 < UPT / 8; ++c8) {
             float ds8[8], dv8[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -641,22 +669,22 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
               ds8[u] = (ms1 >> i) & 1u ? da_s[i] : 0.0f;
               dv8[u] = (mv1 >> i) & 1u ? da_v[i] : 0.0f;
             }
-            tc::store8<2>(Dt, L::D_PIECE, rt, 32 * hf + 8 * c8, 128, ds8);
-            tc::store8<2>(Dt, L::D_PIECE, rt, 64 + 32 * hf + 8 * c8, 128, dv8);
+            tc::store8<2>(Dt, L::D_PIECE, rt, u0 + 8 * c8, 128, ds8);
+            tc::store8<2>(Dt, L::D_PIECE, rt, 64 + u0 + 8 * c8, 128, dv8);
           }
-          float zs[32], zv[32];
-          tc::tmem_ld16x2<32, 32>(tZ2 + tl, zs);
-          tc::tmem_ld16x2<32, 32>(tZ2 + tl + 64, zv);
+          float zs[UPT], zv[UPT];
+          tc::tmem_ld16x2<UPT, UPT>(tZ2 + tl + tc0, zs);
+          tc::tmem_ld16x2<UPT, UPT>(tZ2 + tl + tc0 + 64, zv);
 #pragma unroll
-          for (int c8 = 0; c8 < 4; ++c8) {
+          for (int c8 = 0; c8 < UPT / 8; ++c8) {
             float as[8], av[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               as[u] = fmaxf(zs[8 * c8 + u] + bs1[8 * c8 + u], 0.0f);
               av[u] = fmaxf(zv[8 * c8 + u] + bv1[8 * c8 + u], 0.0f);
             }
-            tc::store8<2>(At, L::A_PIECE, rt, 32 * hf + 8 * c8, AC, as);
-            tc::store8<2>(At, L::A_PIECE, rt, 64 + 32 * hf + 8 * c8, AC, av);
+            tc::store8<2>(At, L::A_PIECE, rt, u0 + 8 * c8, AC, as);
+            tc::store8<2>(At, L::A_PIECE, rt, 64 + u0 + 8 * c8, AC, av);
           }
         }
         to_tensor_core();   // (its tcgen05 fence orders the Z2 reads above before the dH MMA into those columns)
@@ -694,14 +722,15 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
           dphase ^= 1;
         }
         {
-          float dh[16];
-          tc::tmem_ld16x2<16, 16>(tZ2 + tl, dh);
+          constexpr int DHC = 32 / (2 * CG);   // channels of dH per thread
+          float dh[DHC];
+          tc::tmem_ld16x2<DHC, DHC>(tZ2 + tl + (uint32_t)(2 * DHC * cg), dh);
 #pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4)
-            *reinterpret_cast<float4*>(dhs + rt * (K + 4) + 16 * hf + 4 * k4) =
+          for (int k4 = 0; k4 < DHC / 4; ++k4)
+            *reinterpret_cast<float4*>(dhs + rt * (K + 4) + 2 * DHC * cg + DHC * hf + 4 * k4) =
                 make_float4(dh[4 * k4], dh[4 * k4 + 1], dh[4 * k4 + 2], dh[4 * k4 + 3]);
         }
-        if (hf == 0) {
+        if (lead) {
 #pragma unroll
           for (int pp = 0; pp < NPL; ++pp) ptaps[rt * NPL + pp] = taps[rt * NPL + pp];
         }
@@ -710,7 +739,8 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
       }
     }
 
-    // ---- B7: flush the weight-gradient accumulators (M = 128: row u = TMEM lane u) and bias sums
+    // ---- B7: flush the weight-gradient accumulators (M = 128: row u = TMEM lane u; the CG warps of
+    // a lane quarter split the columns) and the bias sums
     tc::fence_after_sync();
     const bool had_tiles = (int64_t)blockIdx.x < ntiles;
     const int u = 32 * wq + lane;          // hidden unit: g_sigma u < 64, g_v u - 64
@@ -718,58 +748,58 @@ __global__ void __launch_bounds__(128 + 32 * kBwdv2ScatterWarps, 1) lp_bwd_tcv2_
     const int uu = sig ? u : u - 64;
     const int KE = K + E;
 #pragma unroll 1
-    for (int c0 = 0; c0 < AC; c0 += 16) {   // dW1, db1 (row u against A1 columns)
-      float w[16];
-      tc::tmem_ld<16>(tW1 + tl + (uint32_t)c0, w);
+    for (int c0 = 16 * cg; c0 < AC; c0 += 16 * CG) {   // dW1, db1 (row u against A1 columns)
+      float wv[16];
+      tc::tmem_ld<16>(tW1 + tl + (uint32_t)c0, wv);
       if (!had_tiles) continue;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int c = c0 + i;
         if (c < 128) {
-          if (sig && c < 64) atomicAdd(a.gparams + P::WS1() + uu * 64 + c, w[i]);
-          if (!sig && c >= 64) atomicAdd(a.gparams + P::WV1(E) + uu * 64 + (c - 64), w[i]);
+          if (sig && c < 64) atomicAdd(a.gparams + P::WS1() + uu * 64 + c, wv[i]);
+          if (!sig && c >= 64) atomicAdd(a.gparams + P::WV1(E) + uu * 64 + (c - 64), wv[i]);
         } else if (c == 128) {
-          atomicAdd(a.gparams + (sig ? P::BS1() : P::BV1(E)) + uu, w[i]);
+          atomicAdd(a.gparams + (sig ? P::BS1() : P::BV1(E)) + uu, wv[i]);
         }
       }
     }
 #pragma unroll 1
-    for (int c0 = 0; c0 < XC; c0 += 16) {   // dW0, db0 (row u against [H | E | 1])
-      float w[16];
-      tc::tmem_ld<16>(tW0 + tl + (uint32_t)c0, w);
+    for (int c0 = 16 * cg; c0 < XC; c0 += 16 * CG) {   // dW0, db0 (row u against [H | E | 1])
+      float wv[16];
+      tc::tmem_ld<16>(tW0 + tl + (uint32_t)c0, wv);
       if (!had_tiles) continue;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int c = c0 + i;
         if (c < K) {
-          atomicAdd(a.gparams + (sig ? P::WS0() + uu * K : P::WV0() + uu * KE) + c, w[i]);
+          atomicAdd(a.gparams + (sig ? P::WS0() + uu * K : P::WV0() + uu * KE) + c, wv[i]);
         } else if (c >= KP && c < KP + E) {
-          if (!sig) atomicAdd(a.gparams + P::WV0() + uu * KE + K + (c - KP), w[i]);
+          if (!sig) atomicAdd(a.gparams + P::WV0() + uu * KE + K + (c - KP), wv[i]);
         } else if (c == KP + EP) {
-          atomicAdd(a.gparams + (sig ? P::BS0() : P::BV0(E)) + uu, w[i]);
+          atomicAdd(a.gparams + (sig ? P::BS0() : P::BV0(E)) + uu, wv[i]);
         }
       }
     }
-    {   // dWo (row u against the DOUT columns 8..11 of [1 | 0 | DOUT | 0])
-      float w[16];
-      tc::tmem_ld<16>(tWo + tl, w);
+    if (cg == 0) {   // dWo (row u against the DOUT columns 8..11 of [1 | 0 | DOUT | 0])
+      float wv[16];
+      tc::tmem_ld<16>(tWo + tl, wv);
       if (had_tiles) {
         if (sig) {
-          atomicAdd(a.gparams + P::WS2() + uu, w[8]);
+          atomicAdd(a.gparams + P::WS2() + uu, wv[8]);
         } else {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) atomicAdd(a.gparams + P::WV2(E) + c * 64 + uu, w[9 + c]);
+          for (int c = 0; c < 3; ++c) atomicAdd(a.gparams + P::WV2(E) + c * 64 + uu, wv[9 + c]);
         }
       }
     }
 #pragma unroll
     for (int i = 0; i < kOut; ++i) {
-      float s = dbo[i];
+      float sum = dbo[i];
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      dbo[i] = s;
+      for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      dbo[i] = sum;
     }
-    if (lane == 0 && had_tiles) {
+    if (lane == 0 && cg == 0 && had_tiles) {
       atomicAdd(a.gparams + P::BS2(), dbo[0]);
 #pragma unroll
       for (int c = 0; c < 3; ++c) atomicAdd(a.gparams + P::BV2(E) + c, dbo[1 + c]);
