@@ -143,8 +143,8 @@ template <int KIND, int K>
 lp_status run_fwd_vd2(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {
   static LaunchShape shape;
   constexpr int G = LP_FWDV2_GROUPS;
-  return launch(lp::lp_fwd_tcv2_kernel<KIND, K, G>, shape, lp::FwdTcv2Smem<KIND, K, G>::BYTES, 128 * G, G, a.M, a,
-                w, s, 64);
+  return launch(lp::lp_fwd_tcv2_kernel<KIND, K, G>, shape, lp::FwdTcv2Smem<KIND, K, G>::BYTES, 128 * lp::kFwdv2CG * G,
+                G, a.M, a, w, s, 64);
 }
 template <int KIND, int K>
 lp_status run_bwd_vd2(const lp::KernelArgs& a, const L2Window& w, cudaStream_t s) {

@@ -157,38 +157,51 @@ __device__ __forceinline__ float4 tcv2_out_partial(const float* fp, int u0, floa
 }
 
 // ================================================================= K1tcv2 forward
+// G groups of 64 rays per CTA; each group has CG column groups of 4 warps (2 CG threads per
+// ray, UPT = 32 / CG units of each network per thread), as in the backward.
+#ifndef LP_FWDV2_CG
+#define LP_FWDV2_CG 1
+#endif
+constexpr int kFwdv2CG = LP_FWDV2_CG;
+
 template <int KIND, int K, int G>
 struct FwdTcv2Smem : Tcv2Shape<KIND, K> {
   using T = Tcv2Shape<KIND, K>;
+  static constexpr int CG = kFwdv2CG;
   static constexpr uint32_t H_PIECE = T::ROWS * T::KP * 2;   // H tile [64][KP]
   static constexpr uint32_t A_PIECE = T::ROWS * 128 * 2;     // A1 tile [64][128] (over H)
   static constexpr uint32_t E_PIECE = T::ROWS * T::EP * 2;   // direnc tile [64][EP]
   static constexpr uint32_t X = 0;
   static constexpr uint32_t E = X + 3 * A_PIECE;
-  static constexpr uint32_t TAPS = E + 3 * E_PIECE;
-  static constexpr uint32_t GSIZE = (TAPS + T::TAPS + 127) & ~127u;
+  static constexpr uint32_t TAPS = E + 3 * E_PIECE;          // [CG][64][NPL]
+  static constexpr uint32_t XO = TAPS + CG * T::TAPS;        // [CG][64] float4
+  static constexpr uint32_t GSIZE = (XO + CG * 64 * 16 + 127) & ~127u;
   static constexpr uint32_t BAR = T::GRP + G * GSIZE;
   static constexpr uint32_t BYTES = BAR + 8 * G + 16;
   static constexpr uint32_t TMEM_COLS = G * 256 <= 256 ? 256 : 512;
+  static_assert(CG == 1 || CG == 2, "column groups");
+  static_assert(1 + G + 4 * G <= 16, "named barriers");
   static_assert(BYTES <= 227 * 1024, "shared memory");
 };
 
 template <int KIND, int K, int G>
-__global__ void __launch_bounds__(128 * G, 1) lp_fwd_tcv2_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(128 * kFwdv2CG * G, 1) lp_fwd_tcv2_kernel(const KernelArgs a) {
   using L = FwdTcv2Smem<KIND, K, G>;
   using F = Tcv2Params;
-  constexpr int KP = L::KP, EP = L::EP, NPL = L::NPL, KC = K / 4;
+  constexpr int KP = L::KP, EP = L::EP, NPL = L::NPL, KC = K / 4, CG = L::CG, UPT = 32 / CG, NG = 128 * CG;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* wp = smem;
   float* fp = reinterpret_cast<float*>(smem + L::FP);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 8 * G);
-  const int g = threadIdx.x >> 7, gt = threadIdx.x & 127, wq = gt >> 5, lane = gt & 31;
-  const int hf = lane >> 4, rt = 16 * wq + (lane & 15);
+  const int g = threadIdx.x / NG, gt = threadIdx.x % NG, w = gt >> 5, wq = w & 3, cg = w >> 2, lane = gt & 31;
+  const int hf = lane >> 4, rt = 16 * wq + (lane & 15), u0 = 32 * cg + UPT * hf;
+  const bool lead = cg == 0 && hf == 0;
   uint8_t* gsm = smem + L::GRP + g * L::GSIZE;
   uint8_t* X = gsm + L::X;
   uint8_t* Et = gsm + L::E;
-  float4* taps = reinterpret_cast<float4*>(gsm + L::TAPS);
+  float4* taps = reinterpret_cast<float4*>(gsm + L::TAPS) + cg * 64 * NPL;
+  float4* xo = reinterpret_cast<float4*>(gsm + L::XO);
 
   for (uint32_t i = threadIdx.x * 16; i < L::BAR; i += blockDim.x * 16)
     *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
@@ -202,7 +215,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tcv2_kernel(const KernelArg
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tZ1 = *tslot + (uint32_t)(g * 256), tZ2 = tZ1 + 128;
-  const uint32_t tl = (uint32_t)(wq * 32) << 16;
+  const uint32_t tl = ((uint32_t)(wq * 32) << 16) + (uint32_t)(32 * cg);
 
   const int R = a.S - 1;
   const float* planes[3] = {a.grid[0], a.grid[1], a.grid[2]};
@@ -214,8 +227,8 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tcv2_kernel(const KernelArg
   const uint64_t kH = tc::kdesc0(x_addr, KP), kE = tc::kdesc0(e_addr, EP), kA = tc::kdesc0(x_addr, 128);
   const uint64_t kW0S = tc::kdesc0(w_addr + L::W0S, KP), kW0V = tc::kdesc0(w_addr + L::W0V, KP + EP);
   const uint64_t kW1S = tc::kdesc0(w_addr + L::W1S, 64), kW1V = tc::kdesc0(w_addr + L::W1V, 64);
-  const float* bs0 = fp + F::BS0 + 32 * hf;
-  const float* bv0 = fp + F::BV0 + 32 * hf;
+  const float* bs0 = fp + F::BS0 + u0;
+  const float* bv0 = fp + F::BV0 + u0;
   uint32_t phase = 0;
 
   const int64_t ntiles = (a.M + 63) / 64;
@@ -224,7 +237,7 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tcv2_kernel(const KernelArg
     const bool valid = r0 < a.M;
     const int64_t r = valid ? r0 : a.M - 1;
     const RayIn ray = load_ray(a.orig, a.dir, a.tnear, a.tfar, r, R);
-    if (hf == 1) write_direnc(Et, L::E_PIECE, rt, 0, EP, ray.d, a.dir_freqs);   // once per ray
+    if (cg == CG - 1 && hf == 1) write_direnc(Et, L::E_PIECE, rt, 0, EP, ray.d, a.dir_freqs);   // once per ray
     float tau = 0.0f, tau_e = 0.0f, dep = 0.0f;
     float v[kC] = {0.0f, 0.0f, 0.0f};
     for (int j = 0; j <= R; ++j) {
@@ -234,11 +247,11 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tcv2_kernel(const KernelArg
         write_taps<KIND, K>(taps + rt * NPL, x, a.dims);                     // F3 (cells)
       }
       __syncwarp();
-      coop_gather<KIND, K, KP, 3>(planes, taps, a.dims, X, L::H_PIECE, 16 * wq, lane, nullptr, nullptr, nullptr, 0,
-                                  KC / 2);                                   // F3 (gather)
+      coop_gather<KIND, K, KP, 3>(planes, taps, a.dims, X, L::H_PIECE, 16 * wq, lane, nullptr, nullptr, nullptr,
+                                  cg * (KC / 2 / CG), (cg + 1) * (KC / 2 / CG));   // F3 (gather)
       tc::fence_async_smem();
       tc::fence_before_sync();
-      tc::named_bar(1 + g, 128);
+      tc::named_bar(1 + g, NG);
       if (gt == 0) {   // F4: Z1 = [H | E] W0'^T (g_sigma: the h columns only)
         tc::fence_after_sync();
 #pragma unroll
@@ -260,24 +273,24 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tcv2_kernel(const KernelArg
       phase ^= 1;
       tc::fence_after_sync();
       {   // a1 = relu(z1 + b0) of this thread's units -> A1 tile (over the consumed H tile)
-        float zs[32], zv[32];
-        tc::tmem_ld16x2<32, 32>(tZ1 + tl, zs);
-        tc::tmem_ld16x2<32, 32>(tZ1 + tl + 64, zv);
+        float zs[UPT], zv[UPT];
+        tc::tmem_ld16x2<UPT, UPT>(tZ1 + tl, zs);
+        tc::tmem_ld16x2<UPT, UPT>(tZ1 + tl + 64, zv);
 #pragma unroll
-        for (int c8 = 0; c8 < 4; ++c8) {
+        for (int c8 = 0; c8 < UPT / 8; ++c8) {
           float as[8], av[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             as[u] = fmaxf(zs[8 * c8 + u] + bs0[8 * c8 + u], 0.0f);
             av[u] = fmaxf(zv[8 * c8 + u] + bv0[8 * c8 + u], 0.0f);
           }
-          tc::store8<3>(X, L::A_PIECE, rt, 32 * hf + 8 * c8, 128, as);
-          tc::store8<3>(X, L::A_PIECE, rt, 64 + 32 * hf + 8 * c8, 128, av);
+          tc::store8<3>(X, L::A_PIECE, rt, u0 + 8 * c8, 128, as);
+          tc::store8<3>(X, L::A_PIECE, rt, 64 + u0 + 8 * c8, 128, av);
         }
       }
       tc::fence_async_smem();
       tc::fence_before_sync();
-      tc::named_bar(1 + g, 128);
+      tc::named_bar(1 + g, NG);
       if (gt == 0) {   // Z2 = A1 W1'^T: A1_s W_s1^T | A1_v W_v1^T
         tc::fence_after_sync();
 #pragma unroll
@@ -297,10 +310,16 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tcv2_kernel(const KernelArg
       tc::fence_after_sync();
       float o[kOut];
       {
-        float zs[32], zv[32];
-        tc::tmem_ld16x2<32, 32>(tZ2 + tl, zs);
-        tc::tmem_ld16x2<32, 32>(tZ2 + tl + 64, zv);
-        const float4 part = tcv2_out_partial<32>(fp, 32 * hf, zs, zv);
+        float zs[UPT], zv[UPT];
+        tc::tmem_ld16x2<UPT, UPT>(tZ2 + tl, zs);
+        tc::tmem_ld16x2<UPT, UPT>(tZ2 + tl + 64, zv);
+        float4 part = tcv2_out_partial<UPT>(fp, u0, zs, zv);
+        if constexpr (CG == 2) {   // the other warp of the pair holds the other half of the units
+          xo[cg * 64 + rt] = part;
+          tc::named_bar(1 + G + 4 * g + wq, 64);
+          const float4 p0 = xo[rt], p1 = xo[64 + rt];
+          part = make_float4(p0.x + p1.x, p0.y + p1.y, p0.z + p1.z, p0.w + p1.w);
+        }
         o[0] = fp[F::BO + 0] + part.x;
         o[1] = fp[F::BO + 1] + part.y;
         o[2] = fp[F::BO + 2] + part.z;
@@ -308,14 +327,14 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tcv2_kernel(const KernelArg
       }
       const float ds = (float)ray.delta * softplus_f(o[0]);                // F5
       if (j > 0) {                                                         // F6
-        const float w = expf(-(tau + tau_e)) * (-expm1f(-ds));
+        const float w_ = expf(-(tau + tau_e)) * (-expm1f(-ds));
 #pragma unroll
-        for (int c = 0; c < kC; ++c) v[c] = fmaf(w, sigmoid_f(o[1 + c]), v[c]);
-        dep = fmaf(w, (float)ray_t(ray, j), dep);
+        for (int c = 0; c < kC; ++c) v[c] = fmaf(w_, sigmoid_f(o[1 + c]), v[c]);
+        dep = fmaf(w_, (float)ray_t(ray, j), dep);
       }
       two_sum_add(tau, tau_e, ds);
     }
-    if (valid && hf == 0) {                                                // F7
+    if (valid && lead) {                                                   // F7
       const float tauR = tau + tau_e;
       const float TR = expf(-tauR);
 #pragma unroll

@@ -249,13 +249,16 @@ def test_depth_backward_eq3_equals_literal_derivative():
 
 
 # ---------------------------------------------------------------- view-dependent colour (row 1)
-def _vd_field(kind=wl.TRIPLANE, dims=(4, 5, 6), K=3, hid=5, F=2, seed=61, sigma_bias=0.5, contraction=0):
-    cfg = wl.Config("t", kind, 4, K, (K, hid, 4), 1, 1, 2, dir_freqs=F)
-    grid, _ = tiny_field_arrays(kind, dims, K, (K, hid, 4), seed=seed)
+def _vd_field(kind=wl.TRIPLANE, dims=(4, 5, 6), K=3, hid=5, F=2, seed=61, sigma_bias=0.5, contraction=0, nh=1):
+    """View-dependent field with nh hidden layers per network (nh = 2: the paper's
+    3-layer g_sigma / g_v)."""
+    widths = (K,) + (hid,) * nh + (4,)
+    cfg = wl.Config("t", kind, 4, K, widths, 1, 1, 2, dir_freqs=F)
+    grid, _ = tiny_field_arrays(kind, dims, K, widths, seed=seed)
     params = wl.make_params(cfg, seed=seed + 1, sigma_bias=sigma_bias).astype(np.float64)
     # nonzero hidden biases so that ReLU decisions vary
     params = params + 0.1 * wl.counter_uniform(seed + 2, np.arange(params.size, dtype=np.uint64), -1, 1)
-    return oracle.Field(kind, grid, (K, hid, 4), params, contraction, 0.7, F), cfg
+    return oracle.Field(kind, grid, widths, params, contraction, 0.7, F), cfg
 
 
 def test_direnc_through_a_probe_network():
@@ -287,10 +290,11 @@ def test_direnc_through_a_probe_network():
         assert np.max(np.abs(col[:, c] - 1.0 / (1.0 + np.exp(-v)))) < 1e-13
 
 
-def test_density_is_view_independent():
+@pytest.mark.parametrize("nh", [1, 2])
+def test_density_is_view_independent(nh):
     """sigma = g_sigma(h) only: the same points traversed in opposite directions get
     the same densities (in reverse order); the colours differ."""
-    Fd, _ = _vd_field(kind=wl.VOXEL, dims=(3, 4, 5))
+    Fd, _ = _vd_field(kind=wl.VOXEL, dims=(3, 4, 5), nh=nh)
     a, b = np.array([-0.7, -0.2, 0.5]), np.array([0.6, 0.4, -0.5])
     L = np.linalg.norm(b - a)
     d = (b - a) / L
@@ -300,10 +304,10 @@ def test_density_is_view_independent():
     assert np.max(np.abs(c1 - c2[::-1])) > 1e-3
 
 
-@pytest.mark.parametrize("kind,contraction", [(wl.TRIPLANE, 0), (wl.VOXEL, 1)])
-def test_view_dependent_backward_matches_finite_differences(kind, contraction):
+@pytest.mark.parametrize("kind,contraction,nh", [(wl.TRIPLANE, 0, 1), (wl.VOXEL, 1, 1), (wl.TRIPLANE, 1, 2)])
+def test_view_dependent_backward_matches_finite_differences(kind, contraction, nh):
     dims = (4, 5, 6) if kind == wl.TRIPLANE else (3, 4, 5)
-    F, _ = _vd_field(kind, dims, contraction=contraction)
+    F, _ = _vd_field(kind, dims, contraction=contraction, nh=nh)
     o, d, near, far = tiny_rays(6)
     rays = oracle.Rays(o, d, near, far * (2.0 if contraction else 1.0), 9)
     p = wl.counter_uniform(71, np.arange(18, dtype=np.uint64), -1, 1).reshape(6, 3).astype(np.float64)
@@ -418,15 +422,16 @@ def _direnc(d, F):
     return np.array(e)
 
 
-@pytest.mark.parametrize("net", ["sigma", "color"])
-def test_view_dependent_relu_slack_bounds_a_flipped_decision(net):
+@pytest.mark.parametrize("net,nh", [("sigma", 1), ("color", 1), ("sigma", 2), ("color", 2)])
+def test_view_dependent_relu_slack_bounds_a_flipped_decision(net, nh):
     """The two-network slack (R29) bounds the gradient jump of a flipped decision in
     either network: put hidden unit 1 of g_sigma (or g_v, whose input is
     [h ; direnc(d)]) exactly at z = 0 on one sample, evaluate the oracle gradients
     with its bias nudged to either side (the forward does not move, ReLU'
-    flips), and check |g+ - g-| <= slack elementwise."""
+    flips), and check |g+ - g-| <= slack elementwise. nh = 2: the paper's 3-layer
+    networks, the flipped first-layer decision propagating through the second."""
     K, hid, Fq = 3, 5, 2
-    Fd, _ = _vd_field(wl.TRIPLANE, (4, 5, 6), K=K, hid=hid, F=Fq)
+    Fd, _ = _vd_field(wl.TRIPLANE, (4, 5, 6), K=K, hid=hid, F=Fq, nh=nh)
     o, d, near, far = tiny_rays(2, inside_start=True)
     S = 7
     rays = oracle.Rays(o[:1], d[:1], near[:1], far[:1], S)
@@ -436,7 +441,7 @@ def test_view_dependent_relu_slack_bounds_a_flipped_decision(net):
     Dl = (float(far[0]) - float(near[0])) / (S - 1)
     x = o[0].astype(np.float64) + (float(near[0]) + 3 * Dl) * d[0].astype(np.float64)
     h = oracle.sample(Fd, x[None])[0]
-    nsig = hid * K + hid + hid + 1
+    nsig = hid * K + hid + (hid * hid + hid) * (nh - 1) + hid + 1
     if net == "sigma":
         W0, b_at, u = Fd.params[:hid * K].reshape(hid, K), hid * K, h
     else:
