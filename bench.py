@@ -609,7 +609,7 @@ def run_splat(args):
         prior = [T(wl.counter_uniform(9 + i, np.arange(int(np.prod(sh)), dtype=np.uint64), -1, 1).reshape(sh))
                  for i, sh in enumerate(grid.shapes())]
         gs = lpb.SplatMlp(T(wl.make_mlp(cfg.widths, seed=10, hidden_bias_scale=0.2)), prior, cfg.K, cfg.dir_freqs,
-                          cfg.widths[1])
+                          cfg.widths[1], n_hidden=len(cfg.widths) - 2)
         gprior = [torch.zeros_like(p) for p in prior]
         gparams = torch.zeros_like(gs.params)
     theta, weight = grid.zeros(dev), grid.zeros(dev, 1)
@@ -694,7 +694,8 @@ def run_splat(args):
                    "parallelism": f"dp{world} (rays sharded, grid all-reduce)",
                    "l2": "theta + theta_weight (grid-sized, L2-resident for s2, not for s1) re-zeroed every step"},
         "breakdown_ms": {"splat_fwd": t_f, "normalize": t_n, "splat_bwd": t_b},
-        "roofline": {"bound": "l2_atomic", "kernel": "lp_splat_mlp_fwd_kernel" if gs is not None else "lp_splat_fwd_kernel",
+        "roofline": {"bound": "l2_atomic", "kernel": ("lp_splat_mlp2_fwd_kernel" if len(cfg.widths) == 4 else "lp_splat_mlp_fwd_kernel")
+                     if gs is not None else "lp_splat_fwd_kernel",
                      "achieved": ach, "peak": red_peak_gbs(cfg.K),
                      "unit": "GB/s", "frac": ach / red_peak_gbs(cfg.K), "traffic": None,
                      "algorithmic": f"{red_b} B of fp32 reductions per sample (corners x (K + 1) x 4)",

@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 2
+#define LP_ABI_VERSION 3
 #define LP_MAX_LAYERS 8
 
 typedef enum {
@@ -195,11 +195,16 @@ lp_status lp_splat_backward(const lp_grid* grid, const lp_rays* rays, const floa
 /* Splatter with its MLP g_s (Eq. 2; reading R30):
  *   v~_ij = g_s(v_i, h_prior(x_ij), direnc(d_i)),  theta += sum_ij w(x_ij) v~_ij,
  * theta_weight as in lp_splat_forward (the weight pass runs with the MLP off,
- * P:748). g_s = Linear(C_in + K_prior + 6F -> hidden) -> ReLU -> Linear(-> K),
- * params packed W0 [hidden][C_in + K_prior + 6F] (input order: v, h_prior,
- * direnc as in lp_mlp), b0, W1 [K][hidden], b1. The prior grid has the kind,
- * dims and contraction of `grid`, K_prior channels, channel-last, 16-byte
- * aligned. Compiled: C_in = K_prior = K = 32, hidden = 64, dir_freqs <= 5. */
+ * P:748). g_s = Linear(C_in + K_prior + 6F -> hidden) -> ReLU -> Linear(-> K)
+ * (n_hidden = 1; 0 means 1), or with a second hidden layer Linear(hidden ->
+ * hidden) -> ReLU before the output layer (n_hidden = 2: the paper's "3-layer
+ * MLPs with a width of 64"). params packed layer by layer, W_l
+ * [out][in] then b_l: W0 [hidden][C_in + K_prior + 6F] (input order: v,
+ * h_prior, direnc as in lp_mlp), b0, (W1 [hidden][hidden], b1,) W_out
+ * [K][hidden], b_out. The prior grid has the kind, dims and contraction of
+ * `grid`, K_prior channels, channel-last, 16-byte aligned. Compiled: C_in =
+ * K_prior = K = 32, hidden = 64, n_hidden 1 or 2, dir_freqs <= 5.
+ * (ABI version 3 added n_hidden.) */
 typedef struct {
   const float* params;
   int32_t hidden;
@@ -207,6 +212,7 @@ typedef struct {
   int32_t dir_freqs;
   int32_t K_prior;
   const float* prior[3];
+  int32_t n_hidden;
 } lp_splat_mlp;
 
 /* theta, theta_weight ACCUMULATED (+=). features [M][C_in]. */

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("LP_LIB_PATH") or os.path.join(_HERE, "liblp_b200.so")
 LP_OK, LP_ERR_INVALID_ARG, LP_ERR_UNSUPPORTED, LP_ERR_MISALIGNED, LP_ERR_CUDA = range(5)
 LP_GRID_TRIPLANE, LP_GRID_VOXEL = 0, 1
 LP_CONTRACT_NONE, LP_CONTRACT_PER_AXIS, LP_CONTRACT_RADIAL = 0, 1, 2
-LP_ABI_VERSION = 2
+LP_ABI_VERSION = 3
 LP_MAX_LAYERS = 8
 _STATUS = {0: "LP_OK", 1: "LP_ERR_INVALID_ARG", 2: "LP_ERR_UNSUPPORTED", 3: "LP_ERR_MISALIGNED", 4: "LP_ERR_CUDA"}
 
@@ -44,7 +44,8 @@ class LpRays(ctypes.Structure):
 
 class LpSplatMlp(ctypes.Structure):
     _fields_ = [("params", ctypes.c_void_p), ("hidden", ctypes.c_int32), ("C_in", ctypes.c_int32),
-                ("dir_freqs", ctypes.c_int32), ("K_prior", ctypes.c_int32), ("prior", ctypes.c_void_p * 3)]
+                ("dir_freqs", ctypes.c_int32), ("K_prior", ctypes.c_int32), ("prior", ctypes.c_void_p * 3),
+                ("n_hidden", ctypes.c_int32)]
 
 
 class LpError(RuntimeError):

@@ -5,6 +5,7 @@
 #include "../../include/lp.h"
 #include "lp_internal.h"
 #include "lp_splat_mlp_kernels.cuh"
+#include "lp_splat_mlp2_kernels.cuh"
 
 namespace {
 using namespace lpi;
@@ -169,6 +170,7 @@ namespace {
 
 lp_status validate_gs(const lp_grid* grid, const lp_splat_mlp* gs) {
   if (!gs || !gs->params) return fail(LP_ERR_INVALID_ARG, "null g_s descriptor / params");
+  if (gs->n_hidden < 0 || gs->n_hidden > 2) return fail(LP_ERR_UNSUPPORTED, "g_s n_hidden must be 1 or 2 (got %d)", gs->n_hidden);
   if (gs->hidden != lp::kGsH || gs->C_in != lp::kGsC || gs->K_prior != lp::kGsKp || grid->K != lp::kGsK)
     return fail(LP_ERR_UNSUPPORTED, "g_s instance: C_in = K_prior = K = 32, hidden = 64 (got %d, %d, %d, %d)",
                 gs->C_in, gs->K_prior, grid->K, gs->hidden);
@@ -176,8 +178,23 @@ lp_status validate_gs(const lp_grid* grid, const lp_splat_mlp* gs) {
   return check_planes(grid, gs->prior, "prior");
 }
 
+// the paper's 3-layer g_s (two hidden layers): 64-ray tiles (lp_splat_mlp2_kernels.cuh)
+template <bool FWD, int KIND>
+lp_status run_gs2(const lp::SplatMlpArgs& a, cudaStream_t s) {
+  static LaunchShape sh;
+  auto kernel = FWD ? lp::lp_splat_mlp2_fwd_kernel<KIND> : lp::lp_splat_mlp2_bwd_kernel<KIND>;
+  const size_t smem = FWD ? lp::Gs2FwdSmem<KIND>::BYTES : lp::Gs2BwdSmem<KIND>::BYTES;
+  const int threads = 128 * lp::kGs2CG + 32 * lp::kGs2ScatterWarps;
+  int grid = 0;
+  lp_status st = persistent_grid(kernel, sh, smem, threads, (a.s.M + 63) / 64, grid);
+  if (st != LP_OK || grid == 0) return st;
+  kernel<<<grid, threads, smem, s>>>(a);
+  return cuda_check(cudaGetLastError(), "g_s splat kernel launch");
+}
+
 template <bool FWD, int KIND>
 lp_status run_gs(const lp::SplatMlpArgs& a, cudaStream_t s) {
+  if (a.n_hidden == 2) return run_gs2<FWD, KIND>(a, s);
   static LaunchShape sh;
   auto kernel = FWD ? lp::lp_splat_mlp_fwd_kernel<KIND> : lp::lp_splat_mlp_bwd_kernel<KIND>;
   const size_t smem = FWD ? lp::GsFwdSmem<KIND>::BYTES : lp::GsBwdSmem<KIND>::BYTES;
@@ -212,6 +229,7 @@ extern "C" lp_status lp_splat_forward_mlp(const lp_grid* grid, const lp_rays* ra
   a.s.feat = features;
   a.params = gs->params;
   a.dir_freqs = gs->dir_freqs;
+  a.n_hidden = gs->n_hidden == 2 ? 2 : 1;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return grid->kind == LP_GRID_TRIPLANE ? run_gs<true, 0>(a, s) : run_gs<true, 1>(a, s);
 }
@@ -244,6 +262,7 @@ extern "C" lp_status lp_splat_backward_mlp(const lp_grid* grid, const lp_rays* r
   a.params = gs->params;
   a.gparams = grad_params;
   a.dir_freqs = gs->dir_freqs;
+  a.n_hidden = gs->n_hidden == 2 ? 2 : 1;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return grid->kind == LP_GRID_TRIPLANE ? run_gs<false, 0>(a, s) : run_gs<false, 1>(a, s);
 }

@@ -32,6 +32,7 @@ struct SplatMlpArgs {
   const float* params;     // W0 [H][C + Kp + E], b0 [H], W1 [K][H], b1 [K]
   float* gparams;          // bwd: accumulated
   int dir_freqs;
+  int n_hidden;            // 1, or 2 (the paper's 3-layer g_s: lp_splat_mlp2_kernels.cuh)
 };
 
 struct GsLayout {          // shared by both kernels

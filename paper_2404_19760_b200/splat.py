@@ -123,13 +123,15 @@ def splat(grid: SplatGrid, origins, dirs, near, far, n_samples: int, features) -
 # ---------------------------------------------------------------- Splatter with g_s (Eq. 2)
 @dataclass
 class SplatMlp:
-    """g_s of Eq. 2: params (W0 [hidden][C_in + K_prior + 6F], b0, W1 [K][hidden], b1),
-    the prior grid theta^ (same kind / dims as the target, K_prior channels), C_in, dir_freqs."""
+    """g_s of Eq. 2: params packed layer by layer (W0 [hidden][C_in + K_prior + 6F], b0,
+    (W1 [hidden][hidden], b1 when n_hidden = 2: the paper's 3-layer g_s), W_out [K][hidden],
+    b_out), the prior grid theta^ (same kind / dims as the target, K_prior channels), C_in, dir_freqs."""
     params: torch.Tensor
     prior: List[torch.Tensor]
     C_in: int = 32
     dir_freqs: int = 4
     hidden: int = 64
+    n_hidden: int = 1
 
     def c_struct(self, grid: "SplatGrid", params=None, prior=None) -> _lib.LpSplatMlp:
         params = self.params if params is None else params
@@ -140,6 +142,7 @@ class SplatMlp:
         m = _lib.LpSplatMlp()
         m.params, m.hidden, m.C_in, m.dir_freqs, m.K_prior = params.data_ptr(), self.hidden, self.C_in, \
             self.dir_freqs, Kp
+        m.n_hidden = self.n_hidden
         for i in range(3):
             m.prior[i] = prior[i].data_ptr() if i < len(prior) else None
         return m

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol(L):
     for name in declared:
         assert hasattr(L.lib, name), name
     assert set(declared) == set(L.EXPORTED)
-    assert L.lib.lp_abi_version() == L.LP_ABI_VERSION == 2
+    assert L.lib.lp_abi_version() == L.LP_ABI_VERSION == 3
 
 
 def _args(L, K=8, widths=(8, 16, 4), kind=0, ptr=0x1000, S=8, n=4):

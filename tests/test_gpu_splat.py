@@ -143,14 +143,18 @@ def test_splat_edge_cases(torch_cuda):
 # ---------------------------------------------------------------- g_s (Eq. 2)
 # every ray compared at the benchmark's 160 points per ray; grid resolution
 # 24-40 for the quick cases, the benchmark's 160 (triplane) / 128 (voxel) for one each
-GS_CASES = [(wl.VOXEL, 24, 768, {}), (wl.TRIPLANE, 40, 768, {}),
-            (wl.TRIPLANE, 32, 768, dict(contraction=1, contract_a=0.9)),
-            (wl.TRIPLANE, 160, 512, {}), (wl.VOXEL, 128, 256, {})]
+# nh = 2: the paper's 3-layer g_s (lp_splat_mlp2_kernels.cuh, 64-ray tiles)
+GS_CASES = [(wl.VOXEL, 24, 768, {}, 1), (wl.TRIPLANE, 40, 768, {}, 1),
+            (wl.TRIPLANE, 32, 768, dict(contraction=1, contract_a=0.9), 1),
+            (wl.TRIPLANE, 160, 512, {}, 1), (wl.VOXEL, 128, 256, {}, 1),
+            (wl.VOXEL, 24, 768, {}, 2), (wl.TRIPLANE, 40, 700, {}, 2),
+            (wl.TRIPLANE, 32, 512, dict(contraction=2, contract_a=1.2), 2), (wl.TRIPLANE, 160, 512, {}, 2),
+            (wl.VOXEL, 128, 256, {}, 2)]
 RELU_BAND = (88 + 2) * 2.0 ** -24   # fp32 rounding bound of a fan-in-88 pre-activation (tests/gpu_problem.py)
 
 
-@pytest.mark.parametrize("kind,res,n,over", GS_CASES)
-def test_splat_mlp_parity(torch_cuda, kind, res, n, over):
+@pytest.mark.parametrize("kind,res,n,over,nh", GS_CASES)
+def test_splat_mlp_parity(torch_cuda, kind, res, n, over, nh):
     """Forward (theta, theta_weight, normalised) and all gradients (features, prior, g_s
     params) of the g_s Splatter vs the oracle, on every ray. Gradients: the metric
     subtracts the oracle's bound for g_s ReLU decisions within RELU_BAND of 0
@@ -162,7 +166,7 @@ def test_splat_mlp_parity(torch_cuda, kind, res, n, over):
     cfg = wl.get_config("s1" if kind == wl.VOXEL else "s2", res=res, S=160, **over)
     spec = _spec(cfg)
     F = 4
-    widths = (32 + 32 + 6 * F, 64, 32)
+    widths = (32 + 32 + 6 * F,) + (64,) * nh + (32,)
     params = wl.make_mlp(widths, seed=120, hidden_bias_scale=0.2)
     prior = [wl.counter_uniform(121 + i, np.arange(int(np.prod(s)), dtype=np.uint64), -1, 1).reshape(s)
              for i, s in enumerate(spec.shapes(32))]
@@ -178,7 +182,7 @@ def test_splat_mlp_parity(torch_cuda, kind, res, n, over):
 
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     grid = lpb.SplatGrid(cfg.kind, (cfg.res,) * 3, 32, cfg.contraction, cfg.contract_a)
-    gs = lpb.SplatMlp(T(params), [T(p) for p in prior], 32, F, 64)
+    gs = lpb.SplatMlp(T(params), [T(p) for p in prior], 32, F, 64, n_hidden=nh)
     o, d, nr, fr = (T(a) for a in rays)
     th, wt = lpb.splat_forward_mlp(grid, o, d, nr, fr, cfg.S, T(v), gs)
     out = lpb.splat_normalize(grid, th, wt)

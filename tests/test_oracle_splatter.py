@@ -208,13 +208,14 @@ def test_gs_reading_direnc():
         assert np.max(np.abs(u - w)) < 1e-12
 
 
-@pytest.mark.parametrize("kind", [wl.TRIPLANE, wl.VOXEL])
-def test_gs_backward_matches_finite_differences(kind):
+@pytest.mark.parametrize("kind,nh", [(wl.TRIPLANE, 1), (wl.VOXEL, 1), (wl.TRIPLANE, 2), (wl.VOXEL, 2)])
+def test_gs_backward_matches_finite_differences(kind, nh):
+    """nh = 2: the paper's 3-layer g_s."""
     spec = _spec(kind, K=3)
     o, d, near, far = tiny_rays(4)
     rays = oracle.Rays(o, d, near, far, 6)
     C_in, Kp, F, hid = 2, 2, 1, 5
-    widths = (C_in + Kp + 6 * F, hid, spec.K)
+    widths = (C_in + Kp + 6 * F,) + (hid,) * nh + (spec.K,)
     params = wl.make_mlp(widths, seed=97, hidden_bias_scale=0.3).astype(np.float64)
     prior = _prior(spec, Kp)
     g = oracle.SplatMlp(prior, widths, params, C_in, F)
@@ -259,19 +260,21 @@ def test_gs_backward_matches_finite_differences(kind):
     assert np.max(np.abs(gv)) > 1e-3 and max(np.max(np.abs(a)) for a in gpr) > 1e-3
 
 
-@pytest.mark.parametrize("kind", [wl.TRIPLANE, wl.VOXEL])
-def test_gs_relu_slack_bounds_a_flipped_decision(kind):
+@pytest.mark.parametrize("kind,nh", [(wl.TRIPLANE, 1), (wl.VOXEL, 1), (wl.TRIPLANE, 2)])
+def test_gs_relu_slack_bounds_a_flipped_decision(kind, nh):
     """The g_s slack (parity metric allowance) bounds the jump of the features,
     prior and parameter gradients when one g_s ReLU decision flips: hidden
     unit 2 is put exactly at z = 0 on one sample (u = [v ; h_prior(x) ;
     direnc(d)]), the gradients are evaluated with its bias nudged to either
-    side, and |g+ - g-| <= slack elementwise; band 0 gives zero slack."""
+    side, and |g+ - g-| <= slack elementwise; band 0 gives zero slack. nh = 2:
+    the paper's 3-layer g_s, the flipped first-layer decision propagating
+    through the second hidden layer."""
     spec = _spec(kind, K=3)
     o, d, near, far = tiny_rays(2, inside_start=True)
     S = 6
     rays = oracle.Rays(o[:1], d[:1], near[:1], far[:1], S)
     C_in, Kp, F, hid = 2, 2, 1, 5
-    widths = (C_in + Kp + 6 * F, hid, spec.K)
+    widths = (C_in + Kp + 6 * F,) + (hid,) * nh + (spec.K,)
     params = wl.make_mlp(widths, seed=97, hidden_bias_scale=0.3).astype(np.float64)
     prior = _prior(spec, Kp)
     v = np.array([[0.6, -0.8]])

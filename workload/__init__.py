@@ -179,6 +179,13 @@ CONFIGS = {
     "s2g": Config("s2g", TRIPLANE, 160, 32, (88, 64, 32), 64, 128, 160,
                   "splatter with g_s: 64 maps of 128x128x32 into 3x160x160 triplanes, prior of the same shape, "
                   "160 points/ray", op="splat", dir_freqs=4, splat_mlp=True),
+    # ... with the paper's 3-layer g_s ("3-layer MLPs with a width of 64")
+    "s1gp": Config("s1gp", VOXEL, 160, 32, (88, 64, 64, 32), 64, 128, 160,
+                   "splatter with the 3-layer g_s: 64 maps of 128x128x32 into a 160^3 voxel grid, prior 160^3x32, "
+                   "160 points/ray", op="splat", dir_freqs=4, splat_mlp=True),
+    "s2gp": Config("s2gp", TRIPLANE, 160, 32, (88, 64, 64, 32), 64, 128, 160,
+                   "splatter with the 3-layer g_s: 64 maps of 128x128x32 into 3x160x160 triplanes, prior of the "
+                   "same shape, 160 points/ray", op="splat", dir_freqs=4, splat_mlp=True),
 }
 
 
