@@ -392,9 +392,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
         LP_PTS(2)
         const float4* staps = reinterpret_cast<const float4*>(smem + L::TAPS + b * L::T::TAPS);
         const float* dhs = reinterpret_cast<const float*>(smem + L::H + b * 3 * L::HP_PIECE);
-#ifndef LP_ABL_NOSCATTER
         for (int rb = sw; rb < 4; rb += SW) coop_scatter<KIND, K>(sgpl, staps, a.dims, dhs, rb * 32, sl);
-#endif
         __syncwarp();
         tc::mbar_arrive(&empty[b]);   // every lane: its own reads of the staging / taps precede it
         LP_PTS(3)

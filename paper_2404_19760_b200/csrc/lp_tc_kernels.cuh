@@ -57,6 +57,26 @@
 #define LP_PAIR_XO 1
 #endif
 
+// K2tcp compute-role phase clocks: with LP_TCP_ANCHOR the clock reads and their accumulation
+// stay in the product build (kept alive by a store that is never taken), as in K2tc2
+// (lp_tc2_kernels.cuh LP_PTC_DECL: there they made ptxas schedule the epilogues better).
+#ifndef LP_TCP_ANCHOR
+#define LP_TCP_ANCHOR 0
+#endif
+#if defined(LP_PHASES)
+#define LP_TCPA_DECL LP_PT_DECL
+#define LP_TCPA(i) LP_PT(i)
+#define LP_TCPA_FLUSH(k) LP_PT_FLUSH(k)
+#elif LP_TCP_ANCHOR
+#define LP_TCPA_DECL unsigned long long lpa_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long lpa_t = clock64();
+#define LP_TCPA(i) { long long now_ = clock64(); lpa_acc[i] += (unsigned long long)(now_ - lpa_t); lpa_t = now_; }
+#define LP_TCPA_FLUSH(k) if (a.M < 0) for (int i_ = 0; i_ < 8; ++i_) a.tau[i_] = (float)lpa_acc[i_];
+#else
+#define LP_TCPA_DECL
+#define LP_TCPA(i)
+#define LP_TCPA_FLUSH(k)
+#endif
+
 namespace lp {
 
 // Exchange of the partial output-layer sums between the two threads of a ray (halves in
@@ -214,21 +234,13 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
                                             const float* dhs = nullptr, int it0 = 0, int it1 = K / 4,
                                             float* const* wplanes = nullptr) {
   constexpr int KC = K / 4, RPI = 32 / KC, NPL = KIND == 0 ? 3 : 1;
-  constexpr bool PAIRED = RPI == 4 && PAIR;
+  const int ch = lane % KC, sub = lane / KC;
   // K = 32: an iteration's 4 rows fill half of each core matrix's 16-byte rows, so its
   // 8-byte piece stores hit the same 16 banks from all 4 channel blocks. Holding the even
-  // iteration and storing it with the odd one (PAIR; measured: c4 fwd -1.6%, c4p bwd -1.7%;
-  // off for K1tcv/K2tcv, +5% there), a store of 8-byte pieces is serviced per half-warp:
-  // the bank of (row r, chunk ch) is 4 (r % 8) + 2 (ch % 2), so each half-warp must cover 8
-  // distinct rows x both chunk parities. With PAIRED the half-warp holds chunks 4 (lane / 16)
-  // .. + 3 of the 4 rays (lane = (ch / 4) 16 + sub 4 + ch % 4), and lanes with (ch / 2) even
-  // write the even iteration's row first, the others the odd one: one wavefront per
-  // half-warp (the plain mapping lane = sub K/4 + ch gave two).
-#ifndef LP_GATHER_LANES
-#define LP_GATHER_LANES 0
-#endif
-  const int ch = (PAIRED && LP_GATHER_LANES) ? ((lane & 3) | ((lane >> 4) << 2)) : lane % KC;
-  const int sub = (PAIRED && LP_GATHER_LANES) ? ((lane >> 2) & 3) : lane / KC;
+  // iteration and storing it with the odd one, lanes of channel blocks 0-1 write one
+  // iteration's rows and blocks 2-3 the other's (PAIR; measured: c4 fwd -1.6%, c4p bwd -1.7%;
+  // off for K1tcv/K2tcv, +5% there). A half-warp still covers only 4 rows (2-way conflicts,
+  // ncu); the conflict-free lane mapping was measured slower (DESIGN.md round-2 measurements).
   float pacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
   int prow = 0;
 #pragma unroll UNROLL
@@ -276,7 +288,7 @@ __device__ __forceinline__ void coop_gather(const float* const* planes, const fl
 #pragma unroll
         for (int i = 0; i < 4; ++i) pacc[i] = acc[i];
       } else {
-        const bool lo = LP_GATHER_LANES ? ((ch >> 1) & 1) == 0 : ch < KC / 2;
+        const bool lo = ch < KC / 2;
         float va[4], vb[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -1022,7 +1034,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
     float dbo[kOut] = {0.0f, 0.0f, 0.0f, 0.0f};
     const float* b0 = fp + F::B0 + hf * HH;
     const float4* wot = reinterpret_cast<const float4*>(fp + F::WOT) + hf * HH;
-    LP_PT_DECL
+    LP_TCPA_DECL
 
     auto mma_done = [&]() {
       tc::mbar_wait(bar, phase);
@@ -1066,7 +1078,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
           tc::mma_commit(bar);
         }
         mma_done();
-        LP_PT(2)
+        LP_TCPA(2)
         float a1[HH];
         {   // this half's units: a1 = relu(z + b0), partial output layer, exchange
           tc::tmem_ld<HH>(tZ + tq + (uint32_t)(hf * HH), a1);
@@ -1136,7 +1148,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
           }
           tc::store8<2>(DAt, S::DA_PIECE, rt, hf * HH + 8 * c, 2 * HP, d1);
         }
-        LP_PT(3)
+        LP_TCPA(3)
         tc::fence_async_smem();
         tc::fence_before_sync();
         tc::named_bar(1, 256);
@@ -1161,7 +1173,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
           tc::mma_commit(bar);
         }
         mma_done();
-        LP_PT(4)
+        LP_TCPA(4)
         // ---- B6: this half's dH channels -> fp32 staging over H[b] (Z and dW are done with it)
         {
           float* dhs_b = reinterpret_cast<float*>(Hb);
@@ -1176,10 +1188,10 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
         }
         tc::mbar_arrive(&staged[b]);
         if (++b == NB) b = 0, bph ^= 1;
-        LP_PT(3)
+        LP_TCPA(3)
       }
     }
-    LP_PT_FLUSH(1)
+    LP_TCPA_FLUSH(1)
 
     // ---- B7: flush the weight-gradient accumulator (M = 128: row i in TMEM lane i; rows [0, HP)
     // D1 units -> dW0, db0 (ones column); rows [HP, 2 HP) A1 units -> dWo^T) and the bias sums

@@ -115,11 +115,8 @@ __device__ __forceinline__ void stage_tcv_weights(uint8_t* wp, float* fp, const 
 // bf16 pieces of the [h | direnc(d)] operand of Z = [H | E] W'^T (the weights keep 3):
 // 3 = fp32-class (default); 2 = 16 significant bits, 5 products (experiment, c4v +9%)
 constexpr int kTcvPieces = LP_TCV_PIECES;
-#ifndef LP_TCV_PAIR
-#define LP_TCV_PAIR 0
-#endif
-// paired H-tile stores in the cooperative gather (coop_gather PAIR) for K1tcv / K2tcv
-constexpr bool kTcvPair = LP_TCV_PAIR != 0;
+// unpaired H-tile stores in the cooperative gather for K1tcv / K2tcv (paired: c4v 10.70 -> 9.59 M rays/s)
+constexpr bool kTcvPair = false;
 
 __device__ __forceinline__ void write_direnc(uint8_t* tile, uint32_t piece, int row, int col0, int C, const float d[3],
                                              int F) {

@@ -89,3 +89,28 @@ def test_fwd_bwd_host_validates_before_enqueue(L):
     assert call(gptr, p, ws, need, None) == L.LP_ERR_INVALID_ARG
     g.contraction, g.contract_scale = L.LP_CONTRACT_PER_AXIS, 2.0   # a = 2 collapses the background: rejected
     assert call(gptr, p, ws, need, p) == L.LP_ERR_INVALID_ARG
+
+
+def test_splat_mlp_descriptor_validation(L):
+    """lp_splat_forward_mlp rejects g_s descriptors no kernel is compiled for
+    (hidden width, channel counts, n_hidden outside {1, 2}) before any CUDA call;
+    n_hidden = 0 reads as 1 (ABI 2 callers zero-initialise it)."""
+    g = L.make_grid(1, 4, 4, 4, 32, [0x1000, 0x1000, 0x1000])
+    r = L.make_rays(4, 0x1000, 0x1000, 0x1000, 0x1000, 8)
+    P3 = L.ptr_array3([0x1000, 0x1000, 0x1000])
+
+    def gs(**kw):
+        m = L.LpSplatMlp()
+        m.params, m.hidden, m.C_in, m.dir_freqs, m.K_prior, m.n_hidden = 0x1000, 64, 32, 4, 32, 1
+        for k, v in kw.items():
+            setattr(m, k, v)
+        for i in range(3):
+            m.prior[i] = 0x1000
+        return m
+    call = lambda m: L.lib.lp_splat_forward_mlp(ctypes.byref(g), ctypes.byref(r), ctypes.c_void_p(0x1000),
+                                                ctypes.byref(m), P3, P3, None)
+    assert call(gs(n_hidden=3)) == L.LP_ERR_UNSUPPORTED and "n_hidden" in L.lib.lp_last_error().decode()
+    assert call(gs(n_hidden=-1)) == L.LP_ERR_UNSUPPORTED
+    assert call(gs(hidden=32)) == L.LP_ERR_UNSUPPORTED
+    assert call(gs(C_in=16, n_hidden=2)) == L.LP_ERR_UNSUPPORTED
+    assert call(gs(dir_freqs=6)) == L.LP_ERR_INVALID_ARG
