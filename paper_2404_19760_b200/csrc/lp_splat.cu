@@ -198,7 +198,7 @@ lp_status run_gs(const lp::SplatMlpArgs& a, cudaStream_t s) {
   static LaunchShape sh;
   auto kernel = FWD ? lp::lp_splat_mlp_fwd_kernel<KIND> : lp::lp_splat_mlp_bwd_kernel<KIND>;
   const size_t smem = FWD ? lp::GsFwdSmem<KIND>::BYTES : lp::GsBwdSmem<KIND>::BYTES;
-  const int threads = 256 + 32 * (FWD ? lp::kSplatScatterWarps : lp::kSplatBwdScatterWarps);
+  const int threads = 256 + 32 * (FWD ? lp::splat_scatter_warps<KIND>() : lp::splat_bwd_scatter_warps<KIND>());
   int grid = 0;
   lp_status st = persistent_grid(kernel, sh, smem, threads, (a.s.M + 127) / 128, grid);
   if (st != LP_OK || grid == 0) return st;

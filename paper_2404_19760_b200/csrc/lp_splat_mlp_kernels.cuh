@@ -107,10 +107,14 @@ struct GsFwdSmem : GsLayout {
 #ifndef LP_SPLAT_SW
 #define LP_SPLAT_SW 4
 #endif
-constexpr int kSplatScatterWarps = LP_SPLAT_SW;
+#ifndef LP_SPLAT_SW_VOXEL   // voxel grids (8 corner lines per sample): 2 measured better (s1g 5.62 -> 5.92 M rays/s)
+#define LP_SPLAT_SW_VOXEL 2
+#endif
+template <int KIND>
+constexpr int splat_scatter_warps() { return KIND == 1 ? LP_SPLAT_SW_VOXEL : LP_SPLAT_SW; }
 
 template <int KIND>
-__global__ void __launch_bounds__(256 + 32 * kSplatScatterWarps, 1) lp_splat_mlp_fwd_kernel(const SplatMlpArgs a) {
+__global__ void __launch_bounds__(256 + 32 * splat_scatter_warps<KIND>(), 1) lp_splat_mlp_fwd_kernel(const SplatMlpArgs a) {
   using L = GsFwdSmem<KIND>;
   constexpr int NPL = L::NPL, KC = kGsKp / 4;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -123,7 +127,7 @@ __global__ void __launch_bounds__(256 + 32 * kSplatScatterWarps, 1) lp_splat_mlp
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 8);
   uint64_t* bar_st = reinterpret_cast<uint64_t*>(smem + L::BAR + 16);   // 256 compute threads
   uint64_t* bar_dr = reinterpret_cast<uint64_t*>(smem + L::BAR + 24);   // the scatter warps
-  constexpr int SW = kSplatScatterWarps;
+  constexpr int SW = splat_scatter_warps<KIND>();
   static_assert(SW == 0 || 4 % SW == 0, "scatter warps");
   const int gt = threadIdx.x, hf = gt >> 7, rt = gt & 127, wq = (gt >> 5) & 3, lane = gt & 31;
   float4* taps = reinterpret_cast<float4*>(smem + L::TAPS) + hf * 128 * NPL;
@@ -337,11 +341,15 @@ struct GsBwdSmem : GsLayout {
 #ifndef LP_SPLAT_BWD_SW
 #define LP_SPLAT_BWD_SW 4
 #endif
-constexpr int kSplatBwdScatterWarps = LP_SPLAT_BWD_SW;
+#ifndef LP_SPLAT_BWD_SW_VOXEL   // voxel grids: 2 (s1g bwd 123.7 -> 118.0 ms)
+#define LP_SPLAT_BWD_SW_VOXEL 2
+#endif
+template <int KIND>
+constexpr int splat_bwd_scatter_warps() { return KIND == 1 ? LP_SPLAT_BWD_SW_VOXEL : LP_SPLAT_BWD_SW; }
 
 // TMEM: S0 [0,64) Z -> dA1 -> dA; dW1|db1 [64,136) (M = 64, rows < 32 real); dW0|db0 [136,240)
 template <int KIND>
-__global__ void __launch_bounds__(256 + 32 * kSplatBwdScatterWarps, 1) lp_splat_mlp_bwd_kernel(const SplatMlpArgs a) {
+__global__ void __launch_bounds__(256 + 32 * splat_bwd_scatter_warps<KIND>(), 1) lp_splat_mlp_bwd_kernel(const SplatMlpArgs a) {
   using L = GsBwdSmem<KIND>;
   constexpr int NPL = L::NPL, KC = kGsKp / 4;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -355,7 +363,7 @@ __global__ void __launch_bounds__(256 + 32 * kSplatBwdScatterWarps, 1) lp_splat_
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + 8);
   uint64_t* bar_st = reinterpret_cast<uint64_t*>(smem + L::BAR + 16);   // 256 compute threads
   uint64_t* bar_dr = reinterpret_cast<uint64_t*>(smem + L::BAR + 24);   // the scatter warps
-  constexpr int SW = kSplatBwdScatterWarps;
+  constexpr int SW = splat_bwd_scatter_warps<KIND>();
   static_assert(SW == 0 || 4 % SW == 0, "scatter warps");
   const int gt = threadIdx.x, hf = gt >> 7, rt = gt & 127, wq = (gt >> 5) & 3, lane = gt & 31;
   float4* taps = reinterpret_cast<float4*>(smem + L::TAPS) + hf * 128 * NPL;

@@ -920,8 +920,8 @@ struct BwdTcpSmem {
   static_assert(BYTES <= 227 * 1024, "shared memory");
 };
 
-#ifndef LP_BWDP_SW
-#define LP_BWDP_SW 4
+#ifndef LP_BWDP_SW   // scatter warps of K2tcp: 2 measured better than 4 (c4 bwd 354 -> 340 ms; c3, c5 neutral), 1 worse (514 ms)
+#define LP_BWDP_SW 2
 #endif
 constexpr int kBwdpScatterWarps = LP_BWDP_SW;
 
