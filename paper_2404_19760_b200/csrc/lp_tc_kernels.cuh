@@ -57,26 +57,6 @@
 #define LP_PAIR_XO 1
 #endif
 
-// K2tcp compute-role phase clocks: with LP_TCP_ANCHOR the clock reads and their accumulation
-// stay in the product build (kept alive by a store that is never taken), as in K2tc2
-// (lp_tc2_kernels.cuh LP_PTC_DECL: there they made ptxas schedule the epilogues better).
-#ifndef LP_TCP_ANCHOR
-#define LP_TCP_ANCHOR 0
-#endif
-#if defined(LP_PHASES)
-#define LP_TCPA_DECL LP_PT_DECL
-#define LP_TCPA(i) LP_PT(i)
-#define LP_TCPA_FLUSH(k) LP_PT_FLUSH(k)
-#elif LP_TCP_ANCHOR
-#define LP_TCPA_DECL unsigned long long lpa_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long lpa_t = clock64();
-#define LP_TCPA(i) { long long now_ = clock64(); lpa_acc[i] += (unsigned long long)(now_ - lpa_t); lpa_t = now_; }
-#define LP_TCPA_FLUSH(k) if (a.M < 0) for (int i_ = 0; i_ < 8; ++i_) a.tau[i_] = (float)lpa_acc[i_];
-#else
-#define LP_TCPA_DECL
-#define LP_TCPA(i)
-#define LP_TCPA_FLUSH(k)
-#endif
-
 namespace lp {
 
 // Exchange of the partial output-layer sums between the two threads of a ray (halves in
@@ -94,6 +74,14 @@ __device__ __forceinline__ void xo_exchange_barrier(int group_id, int group_thre
 
 // iterations of the cooperative gather whose loads are kept in flight together
 constexpr int kGatherUnroll = LP_GATHER_UNROLL;
+// ... in K1tc (all K/4 iterations: c4 fwd 129.3 -> 125.2 ms, c3 36.7 -> 36.0, c5 1606 -> 1584) and in
+// K2tcp's producers (c4 bwd 342.8 -> 338.4 ms; 8 there: 379.5 ms)
+#ifndef LP_FWD_GATHER_UNROLL
+#define LP_FWD_GATHER_UNROLL 8
+#endif
+#ifndef LP_BWDP_UNROLL
+#define LP_BWDP_UNROLL 4
+#endif
 
 #ifndef LP_BWD_HPIECES
 #define LP_BWD_HPIECES 3
@@ -457,7 +445,8 @@ __global__ void __launch_bounds__(128 * G, 1) lp_fwd_tc_kernel(const KernelArgs 
       write_taps<KIND, K>(taps + gt * S::NPL, x, a.dims);          // F3 (cells)
       __syncwarp();
       LP_PT(0)
-      coop_gather<KIND, K, S::KP, kFwdHPieces>(planes, taps, a.dims, Ht, S::H_PIECE, wg * 32, lane);  // F3 (gather)
+      coop_gather<KIND, K, S::KP, kFwdHPieces, false, true, LP_FWD_GATHER_UNROLL>(planes, taps, a.dims, Ht, S::H_PIECE,
+                                                                               wg * 32, lane);  // F3 (gather)
       LP_PT(1)
       tc::fence_async_smem();
       tc::fence_before_sync();
@@ -1007,7 +996,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
         sample_point(ray, q, a.contract, x);
         write_taps<KIND, K>(taps + row * NPL, x, a.dims);
         __syncwarp();
-        coop_gather<KIND, K, HC, kBwdHPieces>(planes, taps, a.dims, Hb, S::HB_PIECE, pw * 32, lane);
+        coop_gather<KIND, K, HC, kBwdHPieces, false, true, LP_BWDP_UNROLL>(planes, taps, a.dims, Hb, S::HB_PIECE, pw * 32, lane);
         tc::fence_async_smem();
         tc::mbar_arrive(&full[b]);
         if (++b == NB) b = 0, ph ^= 1;
@@ -1034,7 +1023,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
     float dbo[kOut] = {0.0f, 0.0f, 0.0f, 0.0f};
     const float* b0 = fp + F::B0 + hf * HH;
     const float4* wot = reinterpret_cast<const float4*>(fp + F::WOT) + hf * HH;
-    LP_TCPA_DECL
+    LP_PT_DECL
 
     auto mma_done = [&]() {
       tc::mbar_wait(bar, phase);
@@ -1078,7 +1067,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
           tc::mma_commit(bar);
         }
         mma_done();
-        LP_TCPA(2)
+        LP_PT(2)
         float a1[HH];
         {   // this half's units: a1 = relu(z + b0), partial output layer, exchange
           tc::tmem_ld<HH>(tZ + tq + (uint32_t)(hf * HH), a1);
@@ -1148,7 +1137,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
           }
           tc::store8<2>(DAt, S::DA_PIECE, rt, hf * HH + 8 * c, 2 * HP, d1);
         }
-        LP_TCPA(3)
+        LP_PT(3)
         tc::fence_async_smem();
         tc::fence_before_sync();
         tc::named_bar(1, 256);
@@ -1173,7 +1162,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
           tc::mma_commit(bar);
         }
         mma_done();
-        LP_TCPA(4)
+        LP_PT(4)
         // ---- B6: this half's dH channels -> fp32 staging over H[b] (Z and dW are done with it)
         {
           float* dhs_b = reinterpret_cast<float*>(Hb);
@@ -1188,10 +1177,10 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
         }
         tc::mbar_arrive(&staged[b]);
         if (++b == NB) b = 0, bph ^= 1;
-        LP_TCPA(3)
+        LP_PT(3)
       }
     }
-    LP_TCPA_FLUSH(1)
+    LP_PT_FLUSH(1)
 
     // ---- B7: flush the weight-gradient accumulator (M = 128: row i in TMEM lane i; rows [0, HP)
     // D1 units -> dW0, db0 (ones column); rows [HP, 2 HP) A1 units -> dWo^T) and the bias sums
