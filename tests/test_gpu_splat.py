@@ -160,9 +160,50 @@ def test_splat_mlp_parity(torch_cuda, kind, res, n, over, nh):
     subtracts the oracle's bound for g_s ReLU decisions within RELU_BAND of 0
     (oracle.splat_mlp_relu_slack); the slack-free (raw)
     and relative L2 errors are reported."""
+    _assert_gs(gs_case(kind, res, n, over, nh))
+
+
+def _assert_gs(errs):
+    print(errs)
+    assert errs["out"] < 1e-4 and errs["theta"] < 1e-4 and errs["weight"] < 1e-4, errs
+    for k in ("gfeat", "gprior", "gparams"):
+        assert errs[k] < 1e-3, (k, errs)
+
+
+_GS_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, {root!r})
+from tests.test_gpu_splat import gs_case
+print("ERRS" + json.dumps(gs_case({kind!r}, {res!r}, {n!r}, {over!r}, {nh!r})))
+"""
+
+
+@pytest.mark.parametrize("kind,nh", [(wl.VOXEL, 1), (wl.TRIPLANE, 1), (wl.VOXEL, 2), (wl.TRIPLANE, 2)])
+def test_splat_mlp_multitile_capped_grid(torch_cuda, kind, nh):
+    """The g_s Splatter kernels with LP_MAX_CTAS=2 (read once per process, in a
+    subprocess): every persistent CTA marches many tiles (128-ray tiles for one hidden
+    layer, 64-ray tiles for the 3-layer g_s: 1536 rays -> 6 / 12 tiles per CTA), so
+    the TMEM weight-gradient accumulators, the per-ray dL/dv and the scatter warps'
+    barrier phases carry across tiles, as in the benchmark launch."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LP_MAX_CTAS="2")
+    r = subprocess.run([sys.executable, "-c", _GS_SCRIPT.format(root=root, kind=kind, res=24, n=1536, over={}, nh=nh)],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("ERRS")][-1]
+    _assert_gs(json.loads(line[4:]))
+
+
+def gs_case(kind, res, n, over, nh):
+    """GPU g_s Splatter forward + backward on n rays vs the oracle: the error dict."""
+    import torch
+
     import paper_2404_19760_b200 as lpb
     from tests.helpers import rel_inf_slack
-    torch = torch_cuda
     cfg = wl.get_config("s1" if kind == wl.VOXEL else "s2", res=res, S=160, **over)
     spec = _spec(cfg)
     F = 4
@@ -201,7 +242,4 @@ def test_splat_mlp_parity(torch_cuda, kind, res, n, over, nh):
                 l2_gparams=float(np.linalg.norm(gpa - ref_gpa) / np.linalg.norm(ref_gpa)),
                 l2_gprior=max(float(np.linalg.norm(a - b) / np.linalg.norm(b)) for a, b in zip(gpr, ref_gpr)),
                 ambiguous_rays=int(np.count_nonzero(sv.max(axis=1) > 0)), rays=len(idx))
-    print(errs)
-    assert errs["out"] < 1e-4 and errs["theta"] < 1e-4 and errs["weight"] < 1e-4, errs
-    for k in ("gfeat", "gprior", "gparams"):
-        assert errs[k] < 1e-3, (k, errs)
+    return errs
