@@ -305,6 +305,9 @@ constexpr int kBwd2ScatterWarps = LP_BWD2_SW;
 #ifndef LP_TC2P_UNROLL
 #define LP_TC2P_UNROLL 2
 #endif
+#ifndef LP_TC2P_SPLIT   // commit the gradient-input MMAs (dA1, dH) ahead of the weight-gradient ones
+#define LP_TC2P_SPLIT 1
+#endif
 template <int KIND, int K, int HID>
 struct Bwd2pSmem : Tc2Shape<KIND, K, HID> {
   using T = Tc2Shape<KIND, K, HID>;
@@ -355,8 +358,10 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
     *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
   __syncthreads();
   stage_tc2_weights<K, HID, KP>(w0p, w1p, fp, a.params);
+  uint64_t* bar2 = bar + 7;      // the gradient-input half of a split MMA round (LP_TC2P_SPLIT)
   if (threadIdx.x == 0) {
     tc::mbar_init(bar, 1);
+    tc::mbar_init(bar2, 1);
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&staged[b], 256);
       tc::mbar_init(&full[b], 128);
@@ -450,7 +455,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
     const uint64_t mW0 = tc::mdesc0(w0_addr, KP), mH = tc::mdesc0(h_addr, HCP);
     constexpr uint32_t MSD = 2 * (2 * HID / 8) * 128, MSA1 = 2 * (HC1 / 8) * 128, MSW1 = 2 * (HID / 8) * 128;
     constexpr uint32_t MSW0 = 2 * (KP / 8) * 128, MSH = 2 * (HCP / 8) * 128;   // MN-major K-step bytes
-    uint32_t phase = 0, wacc = 0, wacc0 = 0, n = 0;
+    uint32_t phase = 0, phase2 = 0, wacc = 0, wacc0 = 0, n = 0;
     float dbo[kOut] = {0.0f, 0.0f, 0.0f, 0.0f};
     const float* b0 = fp + F::B0 + hf * HH;
     const float* b1 = fp + F::B1 + hf * HH;
@@ -621,6 +626,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
             for (int c = 0; c < 3; ++c)
               tc::mma_bf16(tS0, tc::dplus(kD, QA[c] * L::DP + ks * 256), tc::dplus(mW1, QB[c] * L::W1_PIECE + ks * MSW1),
                            id_da1, (ks | c) != 0);
+          if constexpr (LP_TC2P_SPLIT) tc::mma_commit(bar2);   // dA1 complete
           // [dW1 db1 . ; . . dWo^T] += [D2 | A2]^T [A1 | 1 | DOUT]   (K = the 128 samples of this step)
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
@@ -632,11 +638,18 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
             }
           tc::mma_commit(bar);
         }
-        mma_done();
+        if constexpr (LP_TC2P_SPLIT) {   // dA1 first: its TMEM loads overlap the dW1 MMAs
+          tc::mbar_wait(bar2, phase2);
+          phase2 ^= 1;
+          tc::fence_after_sync();
+        } else {
+          mma_done();
+        }
         LP_PTC(4)
         {   // delta1 = ReLU'(z1) dA1 -> D1 (over D2, consumed)
           float da[HH];
           tc::tmem_ld<HH>(tS0 + tq + hf * HH, da);
+          if constexpr (LP_TC2P_SPLIT) mma_done();   // dW1 has read D2
 #pragma unroll
           for (int c = 0; c < HH / 8; ++c) {
             float d1[8];
@@ -656,6 +669,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
             for (int c = 0; c < 3; ++c)
               tc::mma_bf16(tS1, tc::dplus(kD, QA[c] * L::DP + ks * 256), tc::dplus(mW0, QB[c] * L::W0_PIECE + ks * MSW0),
                            id_dh, (ks | c) != 0);
+          if constexpr (LP_TC2P_SPLIT) tc::mma_commit(bar2);   // dH complete
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
@@ -666,7 +680,13 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
             }
           tc::mma_commit(bar);
         }
-        mma_done();
+        if constexpr (LP_TC2P_SPLIT) {   // dH first: its TMEM loads overlap the dW0 MMAs
+          tc::mbar_wait(bar2, phase2);
+          phase2 ^= 1;
+          tc::fence_after_sync();
+        } else {
+          mma_done();
+        }
         LP_PTC(4)
         // ---- B6: this half's dH channels -> fp32 staging over H[b] (Z1, dW0 are done with it)
         {
@@ -674,6 +694,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
           constexpr int HK = KP / 2;
           float dh[HK];
           tc::tmem_ld<HK>(tS1 + tq + hf * HK, dh);
+          if constexpr (LP_TC2P_SPLIT) mma_done();   // dW0 has read H[b]
 #pragma unroll
           for (int k4 = 0; k4 < HK / 4; ++k4)
             if (hf * HK + 4 * k4 < K)

@@ -901,14 +901,17 @@ struct BwdTcpSmem {
   static constexpr uint32_t TAPS = DA + 2 * S::DA_PIECE;                       // NB buffers [128][NPL]
   static constexpr uint32_t XO = TAPS + NB * S::TAPS;                          // [2 halves][128] float4
   static constexpr uint32_t BAR = (XO + 2 * 128 * 16 + 127) & ~127u;
-  // mbarriers: MMA, staged[NB], full[NB], empty[NB]; then the TMEM slot
-  static constexpr uint32_t SLOT = 8 * (1 + 3 * NB);
+  // mbarriers: MMA, staged[NB], full[NB], empty[NB], MMA (dH half, LP_TCP_SPLIT); then the TMEM slot
+  static constexpr uint32_t SLOT = 8 * (2 + 3 * NB);
   static constexpr uint32_t BYTES = BAR + SLOT + 16;
   static constexpr uint32_t TMEM_COLS = 256;
   static_assert(2 * S::HB_PIECE >= 128 * (K + 4) * 4, "dH staging fits pieces 0-1 of an H buffer");
   static_assert(BYTES <= 227 * 1024, "shared memory");
 };
 
+#ifndef LP_TCP_SPLIT   // commit dH ahead of the weight-gradient MMAs
+#define LP_TCP_SPLIT 0
+#endif
 #ifndef LP_BWDP_SW   // scatter warps of K2tcp: 2 measured better than 4 (c4 bwd 354 -> 340 ms; c3, c5 neutral), 1 worse (514 ms)
 #define LP_BWDP_SW 2
 #endif
@@ -933,6 +936,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
   uint64_t* staged = bar + 1;        // [NB] 256 compute threads: dH of the step staged in H[b]
   uint64_t* full = bar + 1 + NB;     // [NB] 128 producer threads: H / taps buffer written
   uint64_t* empty = bar + 1 + 2 * NB;  // [NB] every lane of the scatter warps: staging + taps read
+  uint64_t* bar2 = bar + 1 + 3 * NB;   // dH complete (LP_TCP_SPLIT)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L::BAR + L::SLOT);
 
   for (uint32_t i = threadIdx.x * 16; i < L::BAR; i += blockDim.x * 16)
@@ -941,6 +945,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
   stage_tc_weights<K, HID, KP>(w0p, fp, a.params);
   if (threadIdx.x == 0) {
     tc::mbar_init(bar, 1);
+    tc::mbar_init(bar2, 1);
     for (int b = 0; b < NB; ++b) {
       tc::mbar_init(&staged[b], 256);
       tc::mbar_init(&full[b], 128);
@@ -1019,7 +1024,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
     const uint64_t mW0 = tc::mdesc0(w_addr, KP), mDA = tc::mdesc0(da_addr, 2 * HP), mH = tc::mdesc0(h_addr, HC);
     constexpr uint32_t MSDA = 2 * (2 * HP / 8) * 128, MSW0 = 2 * (KP / 8) * 128, MSH = 2 * (HC / 8) * 128;
     constexpr int QA[3] = {0, 0, 1}, QB[3] = {0, 1, 0};
-    uint32_t phase = 0, wacc = 0, b = 0, bph = 0;   // bph: parity of this use of ring buffer b
+    uint32_t phase = 0, phase2 = 0, wacc = 0, b = 0, bph = 0;   // bph: parity of this use of ring buffer b
     float dbo[kOut] = {0.0f, 0.0f, 0.0f, 0.0f};
     const float* b0 = fp + F::B0 + hf * HH;
     const float4* wot = reinterpret_cast<const float4*>(fp + F::WOT) + hf * HH;
@@ -1150,6 +1155,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
             for (int c = 0; c < 3; ++c)
               tc::mma_bf16(tDH, tc::dplus(kDA, QA[c] * S::DA_PIECE + ks * 256), tc::dplus(mW0, QB[c] * S::W0_PIECE + ks * MSW0),
                            id_dh, (ks | c) != 0);
+          if constexpr (LP_TCP_SPLIT) tc::mma_commit(bar2);   // dH complete
           // [dW0 | db0 | . ; . | dWo^T] += [D1 | A1]^T [H | 1 | DOUT]   (K = the 128 samples of this step)
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
@@ -1161,7 +1167,13 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
             }
           tc::mma_commit(bar);
         }
-        mma_done();
+        if constexpr (LP_TCP_SPLIT) {   // dH first: its TMEM loads overlap the dW MMAs
+          tc::mbar_wait(bar2, phase2);
+          phase2 ^= 1;
+          tc::fence_after_sync();
+        } else {
+          mma_done();
+        }
         LP_PT(4)
         // ---- B6: this half's dH channels -> fp32 staging over H[b] (Z and dW are done with it)
         {
@@ -1169,6 +1181,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwdpScatterWarps, 1) lp_bwd_
           constexpr int HK = KP / 2;
           float dh[HK];
           tc::tmem_ld<HK>(tDH + tq + (uint32_t)(hf * HK), dh);
+          if constexpr (LP_TCP_SPLIT) mma_done();   // dW has read H[b]
 #pragma unroll
           for (int k4 = 0; k4 < HK / 4; ++k4)
             if (hf * HK + 4 * k4 < K)

@@ -378,7 +378,7 @@ struct BwdTcv2Smem : Tcv2Shape<KIND, K> {
   static constexpr uint32_t PTAPS = TAPS + CG * T::TAPS;
   static constexpr uint32_t XO = PTAPS + T::TAPS;           // [CG][64] float4 partial outputs
   static constexpr uint32_t BAR = (XO + CG * 64 * 16 + 127) & ~127u;   // MMA, staged, drained, tmem slot
-  static constexpr uint32_t BYTES = BAR + 32;
+  static constexpr uint32_t BYTES = BAR + 40;   // + the split-commit mbarrier at BAR + 32
   static constexpr uint32_t TMEM_COLS = 512;
   static_assert(CG == 1 || CG == 2, "column groups");
   static_assert(BYTES <= 227 * 1024, "shared memory");
@@ -386,6 +386,9 @@ struct BwdTcv2Smem : Tcv2Shape<KIND, K> {
 
 #ifndef LP_BWDV2_SW
 #define LP_BWDV2_SW 2
+#endif
+#ifndef LP_TCV2_SPLIT   // commit dA1 / dH ahead of the weight-gradient MMAs of their round
+#define LP_TCV2_SPLIT 0
 #endif
 constexpr int kBwdv2ScatterWarps = LP_BWDV2_SW;
 
@@ -421,6 +424,7 @@ __global__ void __launch_bounds__(128 * kBwdv2CG + 32 * kBwdv2ScatterWarps, 1) l
     tc::mbar_init(bar, 1);
     tc::mbar_init(bar_st, NC);
     tc::mbar_init(bar_dr, 32 * SW);
+    tc::mbar_init(bar + 4, 1);
   }
   if (threadIdx.x < 32) tc::tmem_alloc(tslot, L::TMEM_COLS);
   if (threadIdx.x < 64) {   // ones columns (piece 0; never overwritten): X[:, KP + EP] -> db0, A1[:, 128] -> db1
@@ -483,7 +487,19 @@ __global__ void __launch_bounds__(128 * kBwdv2CG + 32 * kBwdv2ScatterWarps, 1) l
     const float* bv1 = fp + F::BV1 + u0;
     const float* ws2 = fp + F::WS2 + u0;
     const float4* wv2 = reinterpret_cast<const float4*>(fp + F::WV2T) + u0;
-    uint32_t phase = 0, wacc1 = 0, wacc0 = 0, dphase = 0;
+    uint32_t phase = 0, phase2 = 0, wacc1 = 0, wacc0 = 0, dphase = 0;
+    uint64_t* bar2 = bar + 4;   // the gradient-input half of a split MMA round (LP_TCV2_SPLIT)
+    auto grad_inputs_done = [&]() {
+      if constexpr (LP_TCV2_SPLIT) {
+        tc::mbar_wait(bar2, phase2);
+        phase2 ^= 1;
+        tc::fence_after_sync();
+      } else {
+        tc::mbar_wait(bar, phase);
+        phase ^= 1;
+        tc::fence_after_sync();
+      }
+    };
     bool staged = false;
     float dbo[kOut] = {0.0f, 0.0f, 0.0f, 0.0f};
 
@@ -663,6 +679,7 @@ __global__ void __launch_bounds__(128 * kBwdv2CG + 32 * kBwdv2ScatterWarps, 1) l
                            (ks | c) != 0);
             }
           }
+          if constexpr (LP_TCV2_SPLIT) tc::mma_commit(bar2);   // dA1 complete
           // [dW1 | db1 | .] += D2^T [A1 | 1 | DOUT]  (M = 128 units, K = the 64 samples of this step)
 #pragma unroll
           for (int c = 0; c < 3; ++c)
@@ -674,11 +691,12 @@ __global__ void __launch_bounds__(128 * kBwdv2CG + 32 * kBwdv2ScatterWarps, 1) l
             }
           tc::mma_commit(bar);
         }
-        mma_done();
+        grad_inputs_done();
         {   // delta1 = ReLU'(z1) dA1 -> D (over delta2, consumed); a2 -> A1 columns [0, 128) (consumed)
           float da_s[UPT], da_v[UPT];
           tc::tmem_ld16x2<UPT, UPT>(tZ1 + tl + tc0, da_s);
           tc::tmem_ld16x2<UPT, UPT>(tZ1 + tl + tc0 + 64, da_v);
+          if constexpr (LP_TCV2_SPLIT) mma_done();   // dW1 has read D2 and A1
 #pragma unroll
           for (int c8 = 0; c8 < UPT / 8; ++c8) {
             float ds8[8], dv8[8];
@@ -720,6 +738,7 @@ __global__ void __launch_bounds__(128 * kBwdv2CG + 32 * kBwdv2ScatterWarps, 1) l
             for (int ks = 0; ks < 4; ++ks)
               tc::mma_bf16(tZ2, tc::dplus(kD, pa + (4 + ks) * 256), tc::dplus(mW0V, pw + ks * MSW0V), id_dh, 1);
           }
+          if constexpr (LP_TCV2_SPLIT) tc::mma_commit(bar2);   // dH complete
           // [dW0 | db0] += D1^T [H | E | 1 | 0];  dWo^T += A2^T [1 | 0 | DOUT | 0]
 #pragma unroll
           for (int c = 0; c < 3; ++c)
@@ -734,7 +753,7 @@ __global__ void __launch_bounds__(128 * kBwdv2CG + 32 * kBwdv2ScatterWarps, 1) l
             }
           tc::mma_commit(bar);
         }
-        mma_done();
+        grad_inputs_done();
         // ---- B6: dH rows -> fp32 staging for the scatter warps
         if (staged) {   // the staging still holds the previous step
           tc::mbar_wait(bar_dr, dphase);
@@ -744,6 +763,7 @@ __global__ void __launch_bounds__(128 * kBwdv2CG + 32 * kBwdv2ScatterWarps, 1) l
           constexpr int DHC = 32 / (2 * CG);   // channels of dH per thread
           float dh[DHC];
           tc::tmem_ld16x2<DHC, DHC>(tZ2 + tl + (uint32_t)(2 * DHC * cg), dh);
+          if constexpr (LP_TCV2_SPLIT) mma_done();   // dW0 and dWo have read D1, X and A2 (the next step's writes)
 #pragma unroll
           for (int k4 = 0; k4 < DHC / 4; ++k4)
             *reinterpret_cast<float4*>(dhs + rt * (K + 4) + 2 * DHC * cg + DHC * hf + 4 * k4) =
