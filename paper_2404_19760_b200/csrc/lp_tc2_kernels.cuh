@@ -305,6 +305,9 @@ constexpr int kBwd2ScatterWarps = LP_BWD2_SW;
 #ifndef LP_TC2P_UNROLL
 #define LP_TC2P_UNROLL 2
 #endif
+#ifndef LP_TC2P_PAIR   // paired H-tile stores in the producers' gather
+#define LP_TC2P_PAIR 1
+#endif
 #ifndef LP_TC2P_SPLIT   // commit the gradient-input MMAs (dA1, dH) ahead of the weight-gradient ones
 #define LP_TC2P_SPLIT 1
 #endif
@@ -425,7 +428,7 @@ __global__ void __launch_bounds__(256 + 128 + 32 * kBwd2ScatterWarps, 1) lp_bwd_
         sample_point(ray, q, a.contract, x);
         write_taps<KIND, K>(taps + row * NPL, x, a.dims);
         __syncwarp();
-        coop_gather<KIND, K, HCP, 3, false, true, LP_TC2P_UNROLL>(planes, taps, a.dims, Hb, L::HP_PIECE, pw * 32, lane);
+        coop_gather<KIND, K, HCP, 3, false, LP_TC2P_PAIR != 0, LP_TC2P_UNROLL>(planes, taps, a.dims, Hb, L::HP_PIECE, pw * 32, lane);
         tc::fence_async_smem();
         tc::mbar_arrive(&full[b]);
         LP_PTP(1)
