@@ -103,6 +103,9 @@ __device__ __forceinline__ void mma_split6(uint32_t d, uint32_t a, uint32_t a_pi
 }
 
 // ================================================================= K1tc2 forward
+#ifndef LP_FWD2_UNROLL   // cooperative-gather iterations in flight in K1tc2
+#define LP_FWD2_UNROLL 2
+#endif
 template <int KIND, int K, int HID, int G>
 struct Fwd2Smem : Tc2Shape<KIND, K, HID> {
   using T = Tc2Shape<KIND, K, HID>;
@@ -177,7 +180,8 @@ __global__ void __launch_bounds__(256 * G, 1) lp_fwd_tc2_kernel(const KernelArgs
       sample_point(ray, j, a.contract, x);                                                // F2
       write_taps<KIND, K>(taps + rt * NPL, x, a.dims);                     // F3 (cells)
       __syncwarp();
-      coop_gather<KIND, K, KP, kTc2Pieces>(planes, taps, a.dims, X, L::H_PIECE, wq * 32, lane, nullptr, nullptr, nullptr,
+      coop_gather<KIND, K, KP, kTc2Pieces, false, true, LP_FWD2_UNROLL>(planes, taps, a.dims, X, L::H_PIECE, wq * 32, lane,
+                                                                        nullptr, nullptr, nullptr,
                                   it0, it1);                               // F3 (gather)
       tc::fence_async_smem();
       tc::fence_before_sync();
